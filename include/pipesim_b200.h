@@ -1,0 +1,200 @@
+/*
+ * pipesim_b200.h — C ABI of the B200-native TiMePReSt pipeline step.
+ *
+ * Plain C: int status codes, plain pointers and sizes, no C++ or torch types.
+ * Every function returns PB_OK (0) or one of the PB_ERR_* codes below and
+ * leaves a message retrievable with pb_last_error() (thread-local).
+ *
+ * The reference ("pipesim", /root/reference/proj) has no FFI: its boundary is
+ * the C++ API in proj/include/pipesim/ (*.hpp).  This header is the thin layer
+ * that (a) the drop-in C++ API (include/pipesim/pipesim_b200.hpp) calls into,
+ * and (b) a foreign-language host binds (the Python mirror in
+ * paper_2410_14312_b200/pipesim.py binds it with ctypes).  Each entry point
+ * cites the reference interface it replaces.
+ */
+#ifndef PIPESIM_B200_H_
+#define PIPESIM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes
+ * Mirrors the reference's exception taxonomy (proj/include/pipesim/errors.hpp:25-65). */
+enum {
+  PB_OK = 0,
+  PB_ERR_DOMAIN = 1,               /* pipesim::domain_error              */
+  PB_ERR_STRUCTURAL = 2,           /* pipesim::structural_error          */
+  PB_ERR_INSUFFICIENT_HORIZON = 3, /* pipesim::insufficient_horizon_error */
+  PB_ERR_INTEGRITY = 4,            /* pipesim::integrity_error           */
+  PB_ERR_IO = 5,                   /* pipesim::io_error                  */
+  PB_ERR_CUDA = 6,                 /* CUDA runtime / driver failure      */
+  PB_ERR_CAPACITY = 7,             /* caller buffer too small            */
+  PB_ERR_INVALID = 8,              /* bad argument                       */
+  PB_ERR_INTERNAL = 9
+};
+
+/* Copies the calling thread's last error message (NUL-terminated, truncated
+ * to cap). Returns the full message length. */
+int pb_last_error(char* buf, int cap);
+/* Field name carried by the last PB_ERR_DOMAIN (domain_error::field()). */
+int pb_last_error_field(char* buf, int cap);
+/* Stage / epoch carried by the last PB_ERR_INTEGRITY. */
+int pb_last_error_stage_epoch(int* stage, int* epoch);
+
+const char* pb_version(void);
+
+/* ------------------------------------------------------------ plan layer
+ * Host-side schedule / version ledger.  Bit-exact with the reference. */
+
+typedef struct {
+  int workers;              /* W */
+  int micro_batches;        /* N */
+  int mini_batches;         /* M */
+  double backward_cost_factor;
+  int samples_per_mini_batch;
+  uint64_t seed;
+} pb_sim_config;            /* proj/include/pipesim/config.hpp:32-40 */
+
+enum { PB_MODE_TIMEPREST = 0, PB_MODE_PIPEDREAM = 1 };      /* schedule_mode */
+enum { PB_TASK_IDLE = 0, PB_TASK_FORWARD = 1, PB_TASK_BACKWARD = 2 };
+
+typedef struct { int kind, mini, micro; } pb_task;           /* schedule.hpp:34-44 */
+typedef struct { int version, mini, stage, slot; } pb_commit; /* ledger.hpp:31-36 */
+typedef struct { int mini, micro, slot, version; } pb_pin;    /* ledger.hpp:38-43 */
+typedef struct { int mini, stage, slot, version; } pb_consume;/* ledger.hpp:45-50 */
+typedef struct { int version, from_slot, freed_slot; } pb_interval; /* ledger.hpp:104-108 */
+
+/* validate(sim_config) — config.hpp:44-62. */
+int pb_validate_config(const pb_sim_config* cfg);
+
+/* build_nf1b_schedule / build_1f1b_schedule — schedule.hpp:84,89.
+ * cells is row-major [W][cap_slots]; *horizon is always set.  Returns
+ * PB_ERR_CAPACITY when cap_slots < horizon (cells untouched). */
+int pb_schedule_build(const pb_sim_config* cfg, int mode, int* horizon,
+                      pb_task* cells, int cap_slots);
+
+/* validate_schedule — schedule.hpp:108-109.  Violations are data: kinds[i]
+ * (0 task_invariant, 1 stage_continuity, 2 completeness, 3 backward_priority)
+ * and '\n'-separated messages. */
+int pb_schedule_validate(const pb_sim_config* cfg, int mode,
+                         const pb_task* cells, int horizon, int* n_violations,
+                         int* kinds, int cap_kinds, char* messages,
+                         int cap_messages);
+
+/* assign_versions — ledger.hpp:70-71.  Output arrays are caller-owned:
+ * commits[M*W], pins[M*units] (units = N for timeprest, 1 for pipedream),
+ * consumptions[M*W], update_source[M], full_commit_slot[M+1]. */
+int pb_assign_versions(const pb_sim_config* cfg, int mode, const pb_task* cells,
+                       int horizon, pb_commit* commits, pb_pin* pins,
+                       pb_consume* consumptions, int* update_source,
+                       int* full_commit_slot);
+
+/* measure_version_difference — ledger.hpp:77-78 (reads update_source). */
+int pb_measure_version_difference(const pb_sim_config* cfg,
+                                  const int* update_source, int strict,
+                                  int* v);
+int pb_closed_form_v(int workers, int micro_batches, int* v);   /* :81 */
+int pb_forward_span(int workers, int micro_batches, int mini_ordinal,
+                    int* span);                                 /* :85 */
+int pb_backward_span(int workers, int* span);                   /* :88 */
+int pb_overlap_condition(int workers, int micro_batches, int* out); /* :92 */
+
+/* decompose_sequences — ledger.hpp:101-102.  seq_mini[] holds the chains
+ * back to back, seq_len[] their lengths. */
+int pb_decompose_sequences(const pb_sim_config* cfg, const int* update_source,
+                           int mini_batches, int* n_sequences, int* seq_len,
+                           int* seq_mini, int* v_measured);
+
+/* build_retention_timeline — ledger.hpp:119-120.  intervals is
+ * [W][M+1]; peak[W]. */
+int pb_retention_timeline(const pb_sim_config* cfg, int mode,
+                          const pb_task* cells, int horizon, const pb_pin* pins,
+                          pb_interval* intervals, int* peak);
+
+/* staleness_report — ledger.hpp:138. staleness[i] matches consumptions[i]. */
+int pb_staleness(const pb_sim_config* cfg, const pb_commit* commits,
+                 const pb_consume* consumptions, int* staleness);
+
+/* ------------------------------------------------------------ model helpers
+ * partition_model / init_network_params / make_synthetic_task
+ * (trainer.hpp:89-115) and the digest (trainer.hpp:106). */
+
+enum { PB_ACT_LINEAR = 0, PB_ACT_RELU = 1, PB_ACT_TANH = 2, PB_ACT_SIGMOID = 3 };
+enum { PB_LOSS_MSE = 0, PB_LOSS_SOFTMAX_CE = 1 };
+
+typedef struct {
+  int n_layers;
+  const int* widths;       /* n_layers + 1 */
+  const int* activations;  /* n_layers, PB_ACT_* */
+  int loss;                /* PB_LOSS_* */
+} pb_net_spec;             /* trainer.hpp:55-64 */
+
+/* stage_layers[s] = number of layers of stage s+1, first_layer[s] likewise. */
+int pb_partition_model(const pb_net_spec* net, int workers, int* first_layer,
+                       int* n_layers);
+int64_t pb_param_count(const pb_net_spec* net);
+int pb_init_network_params(const pb_net_spec* net, uint64_t seed, double* out,
+                           int64_t n);
+int pb_make_synthetic_task(int samples, uint64_t seed, double* x, double* y);
+/* FNV-1a over shortest round-trip decimals ("%.17g"-free, std::to_chars) of
+ * values[0..n) each followed by '\n'; out receives 16 hex chars + NUL. */
+int pb_params_digest(const double* values, int64_t n, char* out17);
+
+/* ------------------------------------------------------------ device layer
+ * Per-op kernels on device pointers (bf16 = uint16 storage).  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Leading dimensions are in
+ * elements and must be multiples of 8 for bf16 operands (TMA 16-byte rule). */
+
+int pb_device_count(int* n);
+int pb_set_device(int device);
+int pb_synchronize(void);
+
+/* y = act(x * w^T + b).  x: rows x in (ld_x), w: out x in (ld_w),
+ * y16 (bf16, may be NULL) and/or y32 (fp32, may be NULL).  Replaces the
+ * forward loop nest of stage_forward (trainer.cpp:186-204). */
+int pb_linear_fwd(void* stream, const uint16_t* x, int rows, int in, int ld_x,
+                  const uint16_t* w, int out, int ld_w, const float* bias,
+                  int act, uint16_t* y16, int ld_y16, float* y32, int ld_y32);
+
+/* d = (dz * w) .* act'(xin).  dz: rows x out, w: out x in, xin: rows x in
+ * (activation the layer consumed, act' recovered from it), d: rows x in.
+ * Replaces stage_backward's delta loop (trainer.cpp:239-242, :255-262). */
+int pb_linear_bwd_dx(void* stream, const uint16_t* dz, int rows, int out,
+                     int ld_dz, const uint16_t* w, int in, int ld_w,
+                     const uint16_t* xin, int ld_xin, int act_prev, uint16_t* d,
+                     int ld_d);
+
+/* w_new = w_cur - lr * dz^T x ; w16 = bf16(w_new).  w_cur may equal w_new.
+ * Replaces the dW loop (trainer.cpp:244-249) fused with SGD (:484-488). */
+int pb_linear_bwd_dw_sgd(void* stream, const uint16_t* dz, int rows, int out,
+                         int ld_dz, const uint16_t* x, int in, int ld_x,
+                         const float* w_cur, float* w_new, int ld_w32,
+                         uint16_t* w16, int ld_w16, float lr);
+
+/* b_new = b_cur - lr * colsum(dz); b_copy (may be NULL) = b_new.
+ * Replaces trainer.cpp:250-252 + :484-488 for the bias. */
+int pb_bias_sgd(void* stream, const uint16_t* dz, int rows, int out, int ld_dz,
+                const float* b_cur, float* b_new, float* b_copy, float lr);
+
+/* Fused loss + gradient over the stacked mini-batch output (loss_mean +
+ * loss_grad, trainer.cpp:270-312): y rows x cols (fp32), targets rows x cols
+ * (fp32), dz = dL/dy / denom .* act'(y) (bf16), row_loss[r] = per-row sum. */
+int pb_loss_fwd_bwd(void* stream, const float* y, int rows, int cols, int ld_y,
+                    const float* targets, int ld_t, int loss, int act_last,
+                    float denom, uint16_t* dz, int ld_dz, float* row_loss);
+
+/* Elementwise conversions used at the host boundary. */
+int pb_convert_f64_to_bf16(void* stream, const double* src, int rows, int cols,
+                           int ld_src, uint16_t* dst, int ld_dst);
+int pb_convert_f32_to_bf16(void* stream, const float* src, int rows, int cols,
+                           int ld_src, uint16_t* dst, int ld_dst);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PIPESIM_B200_H_ */

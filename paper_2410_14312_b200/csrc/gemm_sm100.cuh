@@ -1,0 +1,273 @@
+// tcgen05 / TMEM / TMA GEMM for the three contractions of a Linear layer.
+//
+//   forward   Z = X * W^T        A = X   (K-major)   B = W   (K-major)
+//   dgrad     D = dZ * W         A = dZ  (K-major)   B = W   (MN-major)
+//   wgrad     G = dZ^T * X       A = dZ  (MN-major)  B = X   (MN-major)
+//
+// (reference loops: proj/src/trainer.cpp:186-204 forward, :255-262 dgrad,
+//  :244-253 wgrad, :484-488 SGD).  All operands are row-major bf16 in HBM; the
+// "major-ness" is only how the tile is described to the tensor core, so no
+// transposed copies are ever materialised.
+//
+// One CTA computes one 128 x BN output tile.  Roles (128 threads):
+//   warp 0 / lane 0 : TMA producer, kStages-deep smem ring (128B swizzle)
+//   warp 1 / lane 0 : MMA issuer, tcgen05.mma kind::f16 into TMEM (fp32)
+//   warp 2          : TMEM allocator
+//   warps 0-3       : epilogue; warp w owns TMEM lanes [32w, 32w+32), i.e.
+//                     output rows m0+32w..; the fused epilogue (bias+act,
+//                     act'-gating, or SGD update) runs on the fp32 values.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda.h>
+
+#include "gemm_types.hpp"
+#include "sm100_ptx.cuh"
+
+namespace pb {
+
+__device__ __forceinline__ float act_fwd(float z, int act) {
+  switch (act) {
+    case kRelu: return z > 0.f ? z : 0.f;
+    case kTanh: return tanhf(z);
+    case kSigmoid: return 1.f / (1.f + expf(-z));
+    default: return z;
+  }
+}
+
+// Derivative expressed through the activation value a = act(z).
+__device__ __forceinline__ float act_grad_from_out(float a, int act) {
+  switch (act) {
+    case kRelu: return a > 0.f ? 1.f : 0.f;
+    case kTanh: return 1.f - a * a;
+    case kSigmoid: return a * (1.f - a);
+    default: return 1.f;
+  }
+}
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kBM = 128;
+  static constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
+  static constexpr int kStages = BN >= 256 ? 4 : 6;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256;
+  static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+};
+
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v,
+                                              int valid, bool vec_ok) {
+  if (vec_ok && valid >= 16) {
+    uint32_t p[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      p[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    d4[0] = make_uint4(p[0], p[1], p[2], p[3]);
+    d4[1] = make_uint4(p[4], p[5], p[6], p[7]);
+  } else {
+    for (int i = 0; i < valid && i < 16; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(128, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
+                      const __grid_constant__ CUtensorMap tmap_b, GemmShape sh,
+                      EpiParams ep) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* accum_bar = empty_bar + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * Cfg::kBM;
+  const int n0 = blockIdx.x * BN;
+  const int num_kb = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&tmap_a);
+    ptx::tma_prefetch_desc(&tmap_b);
+    for (int i = 0; i < S; ++i) {
+      ptx::mbar_init(&full_bar[i], 1);
+      ptx::mbar_init(&empty_bar[i], 1);
+    }
+    ptx::mbar_init(accum_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % S;
+      if (kb >= S) ptx::mbar_wait(&empty_bar[s], ((kb / S) - 1) & 1);
+      ptx::mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+      const int k0 = kb * Cfg::kBK;
+      uint8_t* a_dst = sA + s * Cfg::kABytes;
+      uint8_t* b_dst = sB + s * Cfg::kBBytes;
+      if constexpr (!A_MN) {
+        ptx::tma_load_2d(a_dst, &tmap_a, &full_bar[s], k0 + sh.a_k_off,
+                         m0 + sh.a_mn_off);
+      } else {
+#pragma unroll
+        for (int h = 0; h < Cfg::kBM / 64; ++h)
+          ptx::tma_load_2d(a_dst + h * 8192, &tmap_a, &full_bar[s],
+                           m0 + h * 64 + sh.a_mn_off, k0 + sh.a_k_off);
+      }
+      if constexpr (!B_MN) {
+        ptx::tma_load_2d(b_dst, &tmap_b, &full_bar[s], k0 + sh.b_k_off,
+                         n0 + sh.b_mn_off);
+      } else {
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h)
+          ptx::tma_load_2d(b_dst + h * 8192, &tmap_b, &full_bar[s],
+                           n0 + h * 64 + sh.b_mn_off, k0 + sh.b_k_off);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, BN, A_MN, B_MN);
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % S;
+      ptx::mbar_wait(&full_bar[s], (kb / S) & 1);
+      ptx::tc_fence_after();
+      const uint32_t a_addr = ptx::smem_u32(sA + s * Cfg::kABytes);
+      const uint32_t b_addr = ptx::smem_u32(sB + s * Cfg::kBBytes);
+#pragma unroll
+      for (int kk = 0; kk < Cfg::kBK / 16; ++kk) {
+        // K-major: step 16 elements = 32 B inside the swizzle row.
+        // MN-major: step 16 K-rows = 16 * 128 B; MN blocks of 64 are 8 KB apart.
+        const uint64_t a_desc =
+            A_MN ? ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                 : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+        const uint64_t b_desc =
+            B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                 : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+        ptx::mma_bf16(tmem_base, a_desc, b_desc, idesc, (kb | kk) != 0);
+      }
+      ptx::mma_commit(&empty_bar[s]);
+    }
+    ptx::mma_commit(accum_bar);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue (all 4 warps)
+  ptx::mbar_wait(accum_bar, 0);
+  ptx::tc_fence_after();
+
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < sh.M;
+  const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+
+  if (EPI == kEpiFwd || EPI == kEpiDgrad) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && ep.tag_src &&
+        ep.tag_dst)
+      *ep.tag_dst = *ep.tag_src;
+  }
+
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    const int n = n0 + c;
+    if (n >= sh.N) break;  // warp-uniform
+    uint32_t r[16];
+    ptx::tmem_ld16(t_row + c, r);
+    ptx::tmem_ld_wait();
+    if (!row_ok) continue;
+    const int valid = sh.N - n < 16 ? sh.N - n : 16;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+
+    if constexpr (EPI == kEpiFwd) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float b = (ep.bias && i < valid) ? ep.bias[n + i] : 0.f;
+        v[i] = act_fwd(v[i] + b, ep.act);
+      }
+      const size_t yr = static_cast<size_t>(row + ep.y_row_off);
+      if (ep.y16)
+        store_bf16x16(ep.y16 + yr * ep.ld_y16 + n, v, valid,
+                      (ep.ld_y16 % 8) == 0);
+      if (ep.y32) {
+        float* dst = ep.y32 + yr * ep.ld_y32 + n;
+        if (valid == 16 && (ep.ld_y32 % 4) == 0) {
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+          for (int i = 0; i < valid; ++i) dst[i] = v[i];
+        }
+      }
+    } else if constexpr (EPI == kEpiDgrad) {
+      if (ep.act_prev != kLinear) {
+        const __nv_bfloat16* xr = ep.xin + static_cast<size_t>(row) * ep.ld_xin + n;
+        if (valid == 16 && (ep.ld_xin % 8) == 0) {
+          const uint4* x4 = reinterpret_cast<const uint4*>(xr);
+          uint4 q[2] = {x4[0], x4[1]};
+          const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(q);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            v[i] *= act_grad_from_out(__bfloat162float(xh[i]), ep.act_prev);
+        } else {
+          for (int i = 0; i < valid; ++i)
+            v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
+        }
+      }
+      store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
+                    (ep.ld_d16 % 8) == 0);
+    } else {  // kEpiWgradSgd
+      const size_t o32 = static_cast<size_t>(row) * ep.ld_w32 + n;
+      if (valid == 16 && (ep.ld_w32 % 4) == 0) {
+        const float4* c4 = reinterpret_cast<const float4*>(ep.w_cur + o32);
+        float4* n4 = reinterpret_cast<float4*>(ep.w_new + o32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 w = c4[i];
+          w.x -= ep.lr * v[4 * i];
+          w.y -= ep.lr * v[4 * i + 1];
+          w.z -= ep.lr * v[4 * i + 2];
+          w.w -= ep.lr * v[4 * i + 3];
+          v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+          n4[i] = w;
+        }
+      } else {
+        for (int i = 0; i < valid; ++i) {
+          const float w = ep.w_cur[o32 + i] - ep.lr * v[i];
+          ep.w_new[o32 + i] = w;
+          v[i] = w;
+        }
+      }
+      if (ep.w16)
+        store_bf16x16(ep.w16 + static_cast<size_t>(row) * ep.ld_w16 + n, v, valid,
+                      (ep.ld_w16 % 8) == 0);
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace pb

@@ -1,0 +1,47 @@
+// Plain (host-compilable) parameter types of the layer GEMMs.
+#pragma once
+
+#include <cuda_bf16.h>
+
+namespace pb {
+
+enum Act : int { kLinear = 0, kRelu = 1, kTanh = 2, kSigmoid = 3 };
+enum Epi : int { kEpiFwd = 0, kEpiDgrad = 1, kEpiWgradSgd = 2 };
+
+// Problem extents plus TMA coordinate offsets (row offsets inside a larger
+// buffer, e.g. micro-batch j of an activation slot).
+struct GemmShape {
+  int M, N, K;
+  int a_mn_off, a_k_off;
+  int b_mn_off, b_k_off;
+};
+
+struct EpiParams {
+  // forward: y = act(acc + bias)
+  const float* bias;
+  int act;
+  __nv_bfloat16* y16;
+  int ld_y16;
+  float* y32;
+  int ld_y32;
+  int y_row_off;
+  // dgrad: d = acc * act'(xin)   (act' recovered from the stored activation)
+  const __nv_bfloat16* xin;
+  int ld_xin;
+  int act_prev;
+  __nv_bfloat16* d16;
+  int ld_d16;
+  // wgrad + SGD: w_new = w_cur - lr * acc ; w16 = bf16(w_new)
+  const float* w_cur;
+  float* w_new;
+  int ld_w32;
+  __nv_bfloat16* w16;
+  int ld_w16;
+  float lr;
+  // version tag propagation (device-side version accounting): if both are
+  // set, CTA (0,0) copies *tag_src into *tag_dst.
+  const int* tag_src;
+  int* tag_dst;
+};
+
+}  // namespace pb

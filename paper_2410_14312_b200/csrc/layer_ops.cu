@@ -1,0 +1,312 @@
+// Layer kernels and their launchers: GEMM instantiations, fused loss,
+// bias+SGD, and boundary conversions.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm_sm100.cuh"
+#include "layer_ops.cuh"
+#include "status.hpp"
+
+namespace pb {
+
+// ------------------------------------------------------------ tensor maps
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    PB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p,
+                                    cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw cuda_failure("cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn) {
+  if ((m.ld % 8) != 0)
+    throw std::invalid_argument("bf16 leading dimension must be a multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(m.ptr) & 15) != 0)
+    throw std::invalid_argument("bf16 operand must be 16-byte aligned");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(m.cols),
+                        static_cast<cuuint64_t>(m.rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(m.ld) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(k_major ? box_mn : 64)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+      const_cast<void*>(static_cast<const void*>(m.ptr)), dims, strides, box,
+      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeTiled failed (code " +
+                       std::to_string(static_cast<int>(r)) + ")");
+  return map;
+}
+
+int pick_bn(int M, int N) {
+  const long tiles256 = static_cast<long>((M + 127) / 128) * ((N + 255) / 256);
+  return (N > 128 && tiles256 >= 132) ? 256 : 128;
+}
+
+namespace {
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch_one(const GemmLaunch& g, cudaStream_t st) {
+  auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
+  constexpr int smem = GemmCfg<BN>::kSmem;
+  static bool attr_set = false;  // per-instantiation, per-process
+  if (!attr_set) {
+    PB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+    attr_set = true;
+  }
+  dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128);
+  kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+  PB_CUDA(cudaGetLastError());
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+void launch_bn(const GemmLaunch& g, cudaStream_t st) {
+  if (g.bn == 256)
+    launch_one<256, A_MN, B_MN, EPI>(g, st);
+  else
+    launch_one<128, A_MN, B_MN, EPI>(g, st);
+}
+
+EpiParams empty_epi() {
+  EpiParams e{};
+  return e;
+}
+
+}  // namespace
+
+GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
+                    const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
+                    float* y32, int ld_y32, int y_row_off) {
+  GemmLaunch g;
+  g.bn = pick_bn(rows, w.rows);
+  g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
+  g.tb = make_operand_tmap(w, /*k_major=*/true, g.bn);
+  g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0};
+  g.ep = empty_epi();
+  g.ep.bias = bias;
+  g.ep.act = act;
+  g.ep.y16 = y16;
+  g.ep.ld_y16 = ld_y16;
+  g.ep.y32 = y32;
+  g.ep.ld_y32 = ld_y32;
+  g.ep.y_row_off = y_row_off;
+  return g;
+}
+
+GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
+                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d) {
+  GemmLaunch g;
+  g.bn = pick_bn(dz.rows, w.cols);
+  g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
+  g.tb = make_operand_tmap(w, /*k_major=*/false, 64);
+  g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0};
+  g.ep = empty_epi();
+  g.ep.xin = xin;
+  g.ep.ld_xin = ld_xin;
+  g.ep.act_prev = act_prev;
+  g.ep.d16 = d;
+  g.ep.ld_d16 = ld_d;
+  return g;
+}
+
+GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
+                          const float* w_cur, float* w_new, int ld_w32,
+                          __nv_bfloat16* w16, int ld_w16, float lr) {
+  GemmLaunch g;
+  g.bn = pick_bn(dz.cols, x.cols);
+  g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
+  g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
+  g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};
+  g.ep = empty_epi();
+  g.ep.w_cur = w_cur;
+  g.ep.w_new = w_new;
+  g.ep.ld_w32 = ld_w32;
+  g.ep.w16 = w16;
+  g.ep.ld_w16 = ld_w16;
+  g.ep.lr = lr;
+  return g;
+}
+
+void launch_fwd(const GemmLaunch& g, cudaStream_t st) {
+  launch_bn<false, false, kEpiFwd>(g, st);
+}
+void launch_dgrad(const GemmLaunch& g, cudaStream_t st) {
+  launch_bn<false, true, kEpiDgrad>(g, st);
+}
+void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
+  launch_bn<true, true, kEpiWgradSgd>(g, st);
+}
+
+// ------------------------------------------------------------ bias + SGD
+// One thread column per output feature, 8 row groups reduced in smem; the
+// summation order is fixed, so the result is deterministic.
+__global__ void bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows,
+                                int out, int ld_dz, const float* b_cur,
+                                float* b_new, float* b_copy, float lr,
+                                int* tag_slot, int* cur_version, int version) {
+  __shared__ float part[8][33];
+  const int col = blockIdx.x * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (col < out)
+    for (int r = threadIdx.y; r < rows; r += 8)
+      acc += __bfloat162float(dz[static_cast<size_t>(r) * ld_dz + col]);
+  part[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && col < out) {
+    float g = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g += part[i][threadIdx.x];
+    const float b = b_cur[col] - lr * g;
+    b_new[col] = b;
+    if (b_copy) b_copy[col] = b;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+    if (tag_slot) *tag_slot = version;
+    if (cur_version) *cur_version = version;
+  }
+}
+
+void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
+                     int out, int ld_dz, const float* b_cur, float* b_new,
+                     float* b_copy, float lr, int* tag_slot, int* cur_version,
+                     int version) {
+  dim3 block(32, 8);
+  dim3 grid((out + 31) / 32);
+  bias_sgd_kernel<<<grid, block, 0, st>>>(dz, rows, out, ld_dz, b_cur, b_new,
+                                          b_copy, lr, tag_slot, cur_version,
+                                          version);
+  PB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ loss
+// One warp per row.  Softmax-CE: max-subtracted log-softmax, loss counts
+// targets > 0.5 (trainer.cpp:278-286); grad = (softmax - t)/denom
+// (:301-309).  MSE: sum (y-t)^2, grad 2(y-t)/denom (:273-276, :297-299).
+__global__ void loss_kernel(const float* __restrict__ y, int rows, int cols,
+                            int ld_y, const float* __restrict__ t, int ld_t,
+                            int loss, int act_last, float denom,
+                            __nv_bfloat16* __restrict__ dz, int ld_dz,
+                            float* __restrict__ row_loss) {
+  const int warps = blockDim.x / 32;
+  const int row = blockIdx.x * warps + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float* yr = y + static_cast<size_t>(row) * ld_y;
+  const float* tr = t + static_cast<size_t>(row) * ld_t;
+  __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
+  float acc = 0.f;
+  if (loss == 0) {  // mse
+    for (int c = lane; c < cols; c += 32) {
+      const float d = yr[c] - tr[c];
+      acc += d * d;
+      float g = 2.f * d / denom;
+      if (act_last != kLinear) g *= act_grad_from_out(yr[c], act_last);
+      dr[c] = __float2bfloat16_rn(g);
+    }
+  } else {
+    float mx = -INFINITY;
+    for (int c = lane; c < cols; c += 32) mx = fmaxf(mx, yr[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
+    float se = 0.f;
+    for (int c = lane; c < cols; c += 32) se += expf(yr[c] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(~0u, se, o);
+    const float lse = logf(se);
+    for (int c = lane; c < cols; c += 32) {
+      const float z = yr[c] - mx;
+      const float tc = tr[c];
+      if (tc > 0.5f) acc += -(z - lse) * tc;
+      float g = (expf(z) / se - tc) / denom;
+      if (act_last != kLinear) g *= act_grad_from_out(yr[c], act_last);
+      dr[c] = __float2bfloat16_rn(g);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
+  if (lane == 0) row_loss[row] = acc;
+}
+
+void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
+                 const float* targets, int ld_t, int loss, int act_last,
+                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss) {
+  const int warps = 8;
+  loss_kernel<<<(rows + warps - 1) / warps, warps * 32, 0, st>>>(
+      y, rows, cols, ld_y, targets, ld_t, loss, act_last, denom, dz, ld_dz,
+      row_loss);
+  PB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ conversions
+template <typename T>
+__global__ void to_bf16_kernel(const T* __restrict__ src, int rows, int cols,
+                               int ld_src, __nv_bfloat16* __restrict__ dst,
+                               int ld_dst) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    dst[r * ld_dst + c] = __float2bfloat16_rn(static_cast<float>(src[r * ld_src + c]));
+  }
+}
+
+__global__ void f64_f32_kernel(const double* __restrict__ src,
+                               float* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<float>(src[i]);
+}
+
+namespace {
+int grid_for(size_t n) {
+  size_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+}  // namespace
+
+void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst) {
+  to_bf16_kernel<double><<<grid_for(static_cast<size_t>(rows) * cols), 256, 0, st>>>(
+      src, rows, cols, ld_src, dst, ld_dst);
+  PB_CUDA(cudaGetLastError());
+}
+
+void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst) {
+  to_bf16_kernel<float><<<grid_for(static_cast<size_t>(rows) * cols), 256, 0, st>>>(
+      src, rows, cols, ld_src, dst, ld_dst);
+  PB_CUDA(cudaGetLastError());
+}
+
+void launch_f32_to_bf16_rows(cudaStream_t st, const float* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst) {
+  launch_convert_f32_bf16(st, src, rows, cols, ld_src, dst, ld_dst);
+}
+
+void launch_convert_f64_f32(cudaStream_t st, const double* src, float* dst,
+                            size_t n) {
+  f64_f32_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
+  PB_CUDA(cudaGetLastError());
+}
+
+}  // namespace pb

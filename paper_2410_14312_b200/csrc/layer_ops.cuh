@@ -1,0 +1,75 @@
+// Host-side launchers for the layer kernels (used by the C ABI and by the
+// pipeline executor).  Tensor maps are built once per buffer/role and can be
+// cached by the caller (the executor precomputes them at plan time).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gemm_types.hpp"
+
+namespace pb {
+
+// Row-major bf16 matrix view in HBM: rows x cols, leading dim ld (elements).
+struct Mat16 {
+  const __nv_bfloat16* ptr;
+  int rows, cols, ld;
+};
+
+// Operand tensor map for the GEMM: `k_major` picks the box orientation.
+//  K-major: inner dim = cols (K), box {64, box_mn}.
+//  MN-major: inner dim = cols (MN), box {64, 64}.
+CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn);
+
+// GEMM tile width chosen for a problem (128 or 256 columns).
+int pick_bn(int M, int N);
+
+struct GemmLaunch {
+  CUtensorMap ta, tb;
+  GemmShape sh;
+  EpiParams ep;
+  int bn;
+};
+
+// forward: out = act(x[rows, in] * w[out, in]^T + b)
+GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
+                    const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
+                    float* y32, int ld_y32, int y_row_off);
+// dgrad: d[rows, in] = (dz[rows,out] * w[out,in]) .* act'(xin)
+GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
+                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d);
+// wgrad+SGD: w_new[out,in] = w_cur - lr * dz[rows,out]^T x[rows,in]
+// (x rows start at x_row_off inside its buffer)
+GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
+                          const float* w_cur, float* w_new, int ld_w32,
+                          __nv_bfloat16* w16, int ld_w16, float lr);
+
+void launch_fwd(const GemmLaunch& g, cudaStream_t st);
+void launch_dgrad(const GemmLaunch& g, cudaStream_t st);
+void launch_wgrad(const GemmLaunch& g, cudaStream_t st);
+
+void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
+                     int out, int ld_dz, const float* b_cur, float* b_new,
+                     float* b_copy, float lr, int* tag_slot, int* cur_version,
+                     int version);
+
+void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
+                 const float* targets, int ld_t, int loss, int act_last,
+                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss);
+
+void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst);
+void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst);
+void launch_convert_f64_f32(cudaStream_t st, const double* src, float* dst,
+                            size_t n);
+void launch_f32_to_bf16_rows(cudaStream_t st, const float* src, int rows,
+                             int cols, int ld_src, __nv_bfloat16* dst,
+                             int ld_dst);
+
+}  // namespace pb

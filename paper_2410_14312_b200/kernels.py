@@ -1,0 +1,73 @@
+"""Per-op access to the sm_100a layer kernels on torch CUDA tensors.
+
+Torch is only the device-memory / stream plumbing here: every op is a call
+through the C ABI (``pb_linear_fwd`` ...), which launches the hand-written
+kernels.  Used by the kernel parity tests and by diagnostics.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _native
+
+ACT = {"linear": 0, "relu": 1, "tanh": 2, "sigmoid": 3}
+LOSS = {"mse": 0, "softmax_cross_entropy": 1}
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ld(t):
+    assert t.dim() == 2 and t.stride(1) == 1
+    return t.stride(0)
+
+
+def padded_bf16(rows: int, cols: int, device="cuda") -> torch.Tensor:
+    """bf16 [rows, cols] view over a buffer whose row stride is a multiple of 8."""
+    ld = (cols + 7) // 8 * 8
+    return torch.zeros(rows, ld, dtype=torch.bfloat16, device=device)[:, :cols]
+
+
+def linear_fwd(x, w, bias, act="linear", y16=None, y32=None):
+    rows, inn = x.shape
+    out = w.shape[0]
+    _native.check(_native.lib().pb_linear_fwd(
+        _stream(), _ptr(x), rows, inn, _ld(x), _ptr(w), out, _ld(w), _ptr(bias),
+        ACT[act], _ptr(y16), _ld(y16) if y16 is not None else 0,
+        _ptr(y32), _ld(y32) if y32 is not None else 0))
+
+
+def linear_bwd_dx(dz, w, xin, act_prev, d):
+    rows, out = dz.shape
+    inn = w.shape[1]
+    _native.check(_native.lib().pb_linear_bwd_dx(
+        _stream(), _ptr(dz), rows, out, _ld(dz), _ptr(w), inn, _ld(w), _ptr(xin),
+        _ld(xin) if xin is not None else 0, ACT[act_prev], _ptr(d), _ld(d)))
+
+
+def linear_bwd_dw_sgd(dz, x, w_cur, w_new, w16, lr):
+    rows, out = dz.shape
+    inn = x.shape[1]
+    _native.check(_native.lib().pb_linear_bwd_dw_sgd(
+        _stream(), _ptr(dz), rows, out, _ld(dz), _ptr(x), inn, _ld(x), _ptr(w_cur),
+        _ptr(w_new), _ld(w_cur), _ptr(w16), _ld(w16) if w16 is not None else 0,
+        float(lr)))
+
+
+def bias_sgd(dz, b_cur, b_new, b_copy, lr):
+    rows, out = dz.shape
+    _native.check(_native.lib().pb_bias_sgd(
+        _stream(), _ptr(dz), rows, out, _ld(dz), _ptr(b_cur), _ptr(b_new),
+        _ptr(b_copy), float(lr)))
+
+
+def loss_fwd_bwd(y, t, loss, act_last, denom, dz, row_loss):
+    rows, cols = y.shape
+    _native.check(_native.lib().pb_loss_fwd_bwd(
+        _stream(), _ptr(y), rows, cols, _ld(y), _ptr(t), _ld(t), LOSS[loss],
+        ACT[act_last], float(denom), _ptr(dz), _ld(dz), _ptr(row_loss)))
