@@ -193,6 +193,80 @@ int pb_convert_f64_to_bf16(void* stream, const double* src, int rows, int cols,
 int pb_convert_f32_to_bf16(void* stream, const float* src, int rows, int cols,
                            int ld_src, uint16_t* dst, int ld_dst);
 
+
+/* ------------------------------------------------------------ pipeline session
+ * The B200 executor of the pipeline-parallel training step: train_epoch ->
+ * replay_grid (proj/src/trainer.cpp:642-660, :388-508) and sequential_epoch
+ * (:510-553).  A session keeps every stage's weights, version pool and
+ * activation slots resident in HBM; the caller moves data in and results out. */
+
+typedef struct pb_session pb_session;
+
+enum { PB_TRAIN_TIMEPREST = 0, PB_TRAIN_PIPEDREAM = 1, PB_TRAIN_SEQUENTIAL = 2 };
+enum { PB_DTYPE_F64 = 0, PB_DTYPE_F32 = 1, PB_DTYPE_LABELS_I32 = 2 };
+
+typedef struct {
+  int workers;          /* W (stages) */
+  int micro_batches;    /* N */
+  int mini_batch_size;  /* B, divisible by N */
+  int mini_batches;     /* M per epoch */
+  double learning_rate;
+  int mode;             /* PB_TRAIN_* */
+  int device;           /* CUDA device of all stages */
+  int use_graph;        /* capture the epoch as one CUDA graph */
+  int snapshots;        /* keep fp32 host snapshots of every committed version */
+} pb_train_config;      /* train_config, trainer.hpp:117-126 */
+
+typedef struct {
+  double* mini_loss;  /* [M] loss of each mini-batch before its update */
+  int* pinned;        /* [M*units] forward versions (ledger) */
+  int* consumed;      /* [M] update_source (ledger) */
+  int* dev_fwd;       /* [M*units*W] version tags read by forwards, on device */
+  int* dev_bwd;       /* [M*W] version tags propagated through by backwards */
+  int* dev_current;   /* [W] current version per stage after the epoch */
+  float device_ms;    /* device time of the epoch (CUDA events) */
+} pb_epoch_out;       /* epoch_log / mini_log, trainer.hpp:133-147 (+ device trace) */
+
+typedef struct {
+  int horizon;
+  int units;             /* N for timeprest, 1 otherwise */
+  int kernels_per_epoch; /* our kernel launches per epoch */
+  int64_t device_bytes;
+  int64_t param_count;
+  int* pool_sizes;       /* [W] (optional) weight versions held per stage */
+  int* act_slots;        /* [W] (optional) activation slots per stage */
+  int* stage_first_layer;/* [W] (optional) */
+  int* stage_layers;     /* [W] (optional) */
+} pb_session_info;
+
+int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
+                      pb_session** out);
+int pb_session_destroy(pb_session* s);
+int pb_session_info_get(pb_session* s, pb_session_info* info);
+/* load_network_params(stages, flat, 0) — trainer.hpp:99-100 */
+int pb_session_load_params(pb_session* s, const double* flat, int64_t n);
+/* gather_network_params — trainer.hpp:102-103 (current versions, fp32 -> f64) */
+int pb_session_read_params(pb_session* s, double* flat, int64_t n);
+/* Host (pinned or pageable) -> HBM copy of an epoch's data: x [M*B][in],
+ * y [M*B][out] (f64/f32) or [M*B] int32 class labels (one-hot implied). */
+int pb_session_upload(pb_session* s, const void* x, int x_dtype, const void* y,
+                      int y_dtype);
+/* One epoch over the uploaded data (the pipeline step). */
+int pb_session_run_epoch(pb_session* s, pb_epoch_out* out);
+/* upload + run_epoch. */
+int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
+                           const void* y, int y_dtype, pb_epoch_out* out);
+/* fp32 snapshot of stage `stage` (1-based) at `version`, widened to f64. */
+int pb_session_snapshot(pb_session* s, int stage, int version, double* out,
+                        int64_t n);
+
+/* Synthetic classification data: x ~ U[0,1) from
+ * mt19937_64(seed) row-major via (rng()>>11)*2^-53, then labels rng() % C.
+ * Either of x64 / x32 / labels may be NULL. */
+int pb_make_classification_task(int rows, int features, int classes,
+                                uint64_t seed, double* x64, float* x32,
+                                int* labels);
+
 #ifdef __cplusplus
 }
 #endif

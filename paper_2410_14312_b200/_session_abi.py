@@ -1,6 +1,46 @@
-"""ctypes signatures of the session (pipeline executor) entry points."""
+"""ctypes structs and signatures of the session entry points
+(include/pipesim_b200.h, "pipeline session")."""
 from __future__ import annotations
+
+import ctypes as C
+
+
+class pb_train_config(C.Structure):
+    _fields_ = [("workers", C.c_int), ("micro_batches", C.c_int),
+                ("mini_batch_size", C.c_int), ("mini_batches", C.c_int),
+                ("learning_rate", C.c_double), ("mode", C.c_int), ("device", C.c_int),
+                ("use_graph", C.c_int), ("snapshots", C.c_int)]
+
+
+class pb_epoch_out(C.Structure):
+    _fields_ = [("mini_loss", C.POINTER(C.c_double)), ("pinned", C.POINTER(C.c_int)),
+                ("consumed", C.POINTER(C.c_int)), ("dev_fwd", C.POINTER(C.c_int)),
+                ("dev_bwd", C.POINTER(C.c_int)), ("dev_current", C.POINTER(C.c_int)),
+                ("device_ms", C.c_float)]
+
+
+class pb_session_info(C.Structure):
+    _fields_ = [("horizon", C.c_int), ("units", C.c_int), ("kernels_per_epoch", C.c_int),
+                ("device_bytes", C.c_int64), ("param_count", C.c_int64),
+                ("pool_sizes", C.POINTER(C.c_int)), ("act_slots", C.POINTER(C.c_int)),
+                ("stage_first_layer", C.POINTER(C.c_int)),
+                ("stage_layers", C.POINTER(C.c_int))]
 
 
 def signatures():
-    return {}
+    from ._native import pb_net_spec
+    i, p, i64, u64 = C.c_int, C.c_void_p, C.c_int64, C.c_uint64
+    P = C.POINTER
+    return {
+        "pb_session_create": (i, [P(pb_net_spec), P(pb_train_config), P(p)]),
+        "pb_session_destroy": (i, [p]),
+        "pb_session_info_get": (i, [p, P(pb_session_info)]),
+        "pb_session_load_params": (i, [p, P(C.c_double), i64]),
+        "pb_session_read_params": (i, [p, P(C.c_double), i64]),
+        "pb_session_upload": (i, [p, p, i, p, i]),
+        "pb_session_run_epoch": (i, [p, P(pb_epoch_out)]),
+        "pb_session_train_epoch": (i, [p, p, i, p, i, P(pb_epoch_out)]),
+        "pb_session_snapshot": (i, [p, i, i, P(C.c_double), i64]),
+        "pb_make_classification_task": (i, [i, i, i, u64, P(C.c_double), P(C.c_float),
+                                            P(C.c_int)]),
+    }

@@ -1,0 +1,196 @@
+// C ABI over the pipeline session (include/pipesim_b200.h, "pipeline session").
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "session.hpp"
+#include "status.hpp"
+
+namespace pb {
+int translate_exception();
+}
+
+struct pb_session {
+  std::unique_ptr<pb::Session> impl;
+};
+
+#define PB_GUARD_BEGIN try {
+#define PB_GUARD_END \
+  return PB_OK;      \
+  }                  \
+  catch (...) {      \
+    return pb::translate_exception(); \
+  }
+
+namespace {
+
+pb::Session& S(pb_session* s) {
+  if (!s || !s->impl) throw std::invalid_argument("null session");
+  return *s->impl;
+}
+
+pb::HostDType dtype(int d) {
+  switch (d) {
+    case PB_DTYPE_F64: return pb::HostDType::f64;
+    case PB_DTYPE_F32: return pb::HostDType::f32;
+    case PB_DTYPE_LABELS_I32: return pb::HostDType::labels_i32;
+    default: throw std::invalid_argument("bad dtype " + std::to_string(d));
+  }
+}
+
+void fill(const pb::EpochResult& r, const pb::Session& s, pb_epoch_out* out) {
+  if (!out) return;
+  const int M = s.config().M, W = s.config().W, U = s.units();
+  auto put = [](auto* dst, const auto& v, size_t n) {
+    if (dst)
+      for (size_t i = 0; i < n && i < v.size(); ++i) dst[i] = v[i];
+  };
+  put(out->mini_loss, r.mini_loss, M);
+  put(out->pinned, r.pinned, static_cast<size_t>(M) * U);
+  put(out->consumed, r.consumed, M);
+  put(out->dev_fwd, r.dev_fwd, static_cast<size_t>(M) * U * W);
+  put(out->dev_bwd, r.dev_bwd, static_cast<size_t>(M) * W);
+  put(out->dev_current, r.dev_current, W);
+  out->device_ms = r.device_ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
+                      pb_session** out) {
+  PB_GUARD_BEGIN
+  if (!net || !cfg || !out) throw std::invalid_argument("null argument");
+  if (cfg->micro_batches < 1)
+    throw pipesim::domain_error("micro_batches", "micro-batch count must be >= 1");
+  if (cfg->mini_batch_size < 1 || cfg->mini_batches < 1)
+    throw pipesim::domain_error("mini_batches", "mini-batch count/size must be >= 1");
+  pb::SessionConfig c;
+  c.widths.assign(net->widths, net->widths + net->n_layers + 1);
+  c.acts.assign(net->activations, net->activations + net->n_layers);
+  c.loss = net->loss;
+  c.W = cfg->workers;
+  c.N = cfg->micro_batches;
+  c.B = cfg->mini_batch_size;
+  c.M = cfg->mini_batches;
+  c.lr = cfg->learning_rate;
+  c.mode = static_cast<pb::RunMode>(cfg->mode);
+  c.device = cfg->device;
+  c.use_graph = cfg->use_graph != 0;
+  c.snapshots = cfg->snapshots != 0;
+  auto* s = new pb_session;
+  try {
+    s->impl = std::make_unique<pb::Session>(c);
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  *out = s;
+  PB_GUARD_END
+}
+
+int pb_session_destroy(pb_session* s) {
+  PB_GUARD_BEGIN
+  delete s;
+  PB_GUARD_END
+}
+
+int pb_session_info_get(pb_session* s, pb_session_info* info) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  info->horizon = x.horizon();
+  info->units = x.units();
+  info->kernels_per_epoch = x.kernels_per_epoch();
+  info->device_bytes = x.device_bytes();
+  info->param_count = x.param_count();
+  const auto ps = x.pool_sizes();
+  const auto as = x.act_slot_counts();
+  for (size_t i = 0; i < ps.size(); ++i) {
+    if (info->pool_sizes) info->pool_sizes[i] = ps[i];
+    if (info->act_slots) info->act_slots[i] = as[i];
+  }
+  pipesim::network_spec net;
+  net.widths = x.config().widths;
+  for (int a : x.config().acts) net.activations.push_back(static_cast<pipesim::activation_kind>(a));
+  const auto part = pipesim::partition_model(net, x.config().W);
+  for (size_t i = 0; i < part.size(); ++i) {
+    if (info->stage_first_layer) info->stage_first_layer[i] = part[i].first_layer;
+    if (info->stage_layers) info->stage_layers[i] = static_cast<int>(part[i].layers.size());
+  }
+  PB_GUARD_END
+}
+
+int pb_session_load_params(pb_session* s, const double* flat, int64_t n) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  if (n != x.param_count())
+    throw pipesim::structural_error(n < x.param_count()
+                                        ? "parameter vector shorter than the network"
+                                        : "parameter vector longer than the network");
+  x.load_params(flat);
+  PB_GUARD_END
+}
+
+int pb_session_read_params(pb_session* s, double* flat, int64_t n) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  if (n != x.param_count()) throw pb::capacity_error("parameter count mismatch");
+  x.read_params(flat);
+  PB_GUARD_END
+}
+
+int pb_session_upload(pb_session* s, const void* x, int x_dtype, const void* y,
+                      int y_dtype) {
+  PB_GUARD_BEGIN
+  S(s).upload(x, dtype(x_dtype), y, dtype(y_dtype));
+  PB_GUARD_END
+}
+
+int pb_session_run_epoch(pb_session* s, pb_epoch_out* out) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  const pb::EpochResult r = x.run_epoch();
+  fill(r, x, out);
+  PB_GUARD_END
+}
+
+int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
+                           const void* y, int y_dtype, pb_epoch_out* out) {
+  PB_GUARD_BEGIN
+  pb::Session& ss = S(s);
+  ss.upload(x, dtype(x_dtype), y, dtype(y_dtype));
+  const pb::EpochResult r = ss.run_epoch();
+  fill(r, ss, out);
+  PB_GUARD_END
+}
+
+int pb_session_snapshot(pb_session* s, int stage, int version, double* out, int64_t n) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  if (n != x.stage_param_count(stage)) throw pb::capacity_error("stage parameter count mismatch");
+  const float* p = x.snapshot(stage, version);
+  for (int64_t i = 0; i < n; ++i) out[i] = p[i];
+  PB_GUARD_END
+}
+
+int pb_make_classification_task(int rows, int features, int classes, uint64_t seed,
+                                double* x64, float* x32, int* labels) {
+  PB_GUARD_BEGIN
+  if (rows < 0 || features < 1 || classes < 1) throw std::invalid_argument("bad shape");
+  std::mt19937_64 g(seed);
+  const size_t n = static_cast<size_t>(rows) * features;
+  for (size_t i = 0; i < n; ++i) {
+    const double v = static_cast<double>(g() >> 11) * 0x1.0p-53;
+    if (x64) x64[i] = v;
+    if (x32) x32[i] = static_cast<float>(v);
+  }
+  for (int r = 0; r < rows; ++r) {
+    const int c = static_cast<int>(g() % static_cast<uint64_t>(classes));
+    if (labels) labels[r] = c;
+  }
+  PB_GUARD_END
+}
+
+}  // extern "C"

@@ -63,15 +63,17 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_one(const GemmLaunch& g, cudaStream_t st) {
   auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
   constexpr int smem = GemmCfg<BN>::kSmem;
-  static bool attr_set = false;  // per-instantiation, per-process
-  if (!attr_set) {
-    PB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem));
-    attr_set = true;
-  }
+  init_gemm_attributes();
   dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128);
   kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
   PB_CUDA(cudaGetLastError());
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void set_attr() {
+  PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               GemmCfg<BN>::kSmem));
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -81,6 +83,22 @@ void launch_bn(const GemmLaunch& g, cudaStream_t st) {
   else
     launch_one<128, A_MN, B_MN, EPI>(g, st);
 }
+
+}  // namespace
+
+void init_gemm_attributes() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    set_attr<128, false, false, kEpiFwd>();
+    set_attr<256, false, false, kEpiFwd>();
+    set_attr<128, false, true, kEpiDgrad>();
+    set_attr<256, false, true, kEpiDgrad>();
+    set_attr<128, true, true, kEpiWgradSgd>();
+    set_attr<256, true, true, kEpiWgradSgd>();
+  });
+}
+
+namespace {
 
 EpiParams empty_epi() {
   EpiParams e{};
@@ -158,7 +176,8 @@ void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
 __global__ void bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows,
                                 int out, int ld_dz, const float* b_cur,
                                 float* b_new, float* b_copy, float lr,
-                                int* tag_slot, int* cur_version, int version) {
+                                int* tag_slot, int* cur_version, int version,
+                                const int* trace_src, int* trace_dst) {
   __shared__ float part[8][33];
   const int col = blockIdx.x * 32 + threadIdx.x;
   float acc = 0.f;
@@ -176,6 +195,7 @@ __global__ void bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows,
     if (b_copy) b_copy[col] = b;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+    if (trace_src && trace_dst) *trace_dst = *trace_src;
     if (tag_slot) *tag_slot = version;
     if (cur_version) *cur_version = version;
   }
@@ -184,12 +204,12 @@ __global__ void bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows,
 void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int out, int ld_dz, const float* b_cur, float* b_new,
                      float* b_copy, float lr, int* tag_slot, int* cur_version,
-                     int version) {
+                     int version, const int* trace_src, int* trace_dst) {
   dim3 block(32, 8);
   dim3 grid((out + 31) / 32);
   bias_sgd_kernel<<<grid, block, 0, st>>>(dz, rows, out, ld_dz, b_cur, b_new,
                                           b_copy, lr, tag_slot, cur_version,
-                                          version);
+                                          version, trace_src, trace_dst);
   PB_CUDA(cudaGetLastError());
 }
 

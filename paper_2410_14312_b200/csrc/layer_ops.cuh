@@ -54,7 +54,12 @@ void launch_wgrad(const GemmLaunch& g, cudaStream_t st);
 void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int out, int ld_dz, const float* b_cur, float* b_new,
                      float* b_copy, float lr, int* tag_slot, int* cur_version,
-                     int version);
+                     int version, const int* trace_src = nullptr,
+                     int* trace_dst = nullptr);
+
+// Sets the dynamic-smem attribute of every GEMM instantiation (call before
+// any stream capture).
+void init_gemm_attributes();
 
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,

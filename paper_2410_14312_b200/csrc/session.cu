@@ -1,0 +1,876 @@
+// Session implementation — see session.hpp for the design summary.
+#include "session.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+
+#include "status.hpp"
+
+namespace pb {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+int ld8(int cols) { return (cols + 7) / 8 * 8; }
+
+// Greedy interval colouring over [start, end] (inclusive ends): a colour is
+// reusable by an interval starting strictly after the colour's last end.
+// Intervals are given in the order colours should be assigned (by start).
+std::vector<int> colour(const std::vector<std::pair<int, int>>& iv, int* n_colours,
+                        bool half_open) {
+  std::vector<int> order(iv.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return iv[a].first < iv[b].first; });
+  std::vector<int> busy_until;  // per colour: last end
+  std::vector<int> out(iv.size(), -1);
+  for (int i : order) {
+    int pick = -1;
+    for (size_t c = 0; c < busy_until.size(); ++c) {
+      const bool free = half_open ? busy_until[c] <= iv[i].first
+                                  : busy_until[c] < iv[i].first;
+      if (free) {
+        pick = static_cast<int>(c);
+        break;
+      }
+    }
+    if (pick < 0) {
+      pick = static_cast<int>(busy_until.size());
+      busy_until.push_back(0);
+    }
+    busy_until[pick] = iv[i].second;
+    out[i] = pick;
+  }
+  *n_colours = static_cast<int>(busy_until.size());
+  return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Impl
+struct Session::Impl {
+  struct LayerDev {
+    int in = 0, out = 0, act = 0;
+    int ld_in = 0, ld_out = 0;
+    float* w32[2] = {nullptr, nullptr};
+    float* b32[2] = {nullptr, nullptr};
+  };
+  struct PoolSlot {
+    std::vector<__nv_bfloat16*> w16;
+    std::vector<float*> b32;
+    int* tag = nullptr;
+  };
+  struct ActSlot {
+    std::vector<__nv_bfloat16*> out16;  // per layer (null for the logits layer)
+    float* out32 = nullptr;              // last stage: logits / final output
+    __nv_bfloat16* dzin = nullptr;       // delta into this stage's top layer
+  };
+  struct Stage {
+    int id = 0, first_layer = 0, L = 0;
+    std::vector<LayerDev> layers;
+    std::vector<PoolSlot> pool;
+    std::vector<ActSlot> acts;
+    std::vector<__nv_bfloat16*> scratch_dz;  // per layer < L-1
+    std::vector<int> version_colour;         // [M+1]
+    std::vector<int> mini_act;               // [M+1]
+    int* cur_version = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t param_offset = 0, param_count = 0;
+  };
+
+  struct Task {
+    bool fwd = true;
+    int k = 0, jj = 0, s = 0, slot = 0;
+    int version = 0;  // fwd: pinned; bwd: propagation version
+  };
+
+  enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot };
+  struct Op {
+    OpKind kind;
+    int stream = 0;  // stage index (0-based); -1 = origin stream
+    cudaEvent_t ev = nullptr;
+    GemmLaunch g{};
+    // bias
+    const __nv_bfloat16* dz = nullptr;
+    int rows = 0, cols = 0, ld = 0;
+    const float* b_cur = nullptr;
+    float* b_new = nullptr;
+    float* b_copy = nullptr;
+    int* tag_slot = nullptr;
+    int* cur_version = nullptr;
+    const int* trace_src = nullptr;
+    int* trace_dst = nullptr;
+    int version = 0;
+    // loss
+    const float* y = nullptr;
+    const float* t = nullptr;
+    int ld_t = 0, loss = 0, act_last = 0, ld_dz = 0;
+    float lr = 0.f;
+    float denom = 1.f;
+    __nv_bfloat16* dz_out = nullptr;
+    float* row_loss = nullptr;
+    // copy / memset
+    void* dst = nullptr;
+    const void* src = nullptr;
+    size_t bytes = 0;
+    int value = 0;
+  };
+
+  const SessionConfig& cfg;
+  int W, N, B, M, U, Rm;
+  std::vector<Stage> stages;
+  // data
+  __nv_bfloat16* x16 = nullptr;
+  int ld_x = 0;
+  float* y32 = nullptr;
+  int n_out = 0;
+  void* stage_buf = nullptr;  // upload staging (f64 or f32 or i32)
+  size_t stage_bytes = 0;
+  float* row_loss = nullptr;
+  int* fwd_trace = nullptr;  // [M][U][W]
+  int* bwd_trace = nullptr;  // [M][W]
+  // arena
+  char* arena = nullptr;
+  size_t arena_used = 0, arena_cap = 0;
+  // program
+  std::vector<Task> tasks;  // issue order
+  std::vector<Op> ops;
+  std::vector<cudaEvent_t> events;
+  cudaStream_t origin = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> join_ev;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  // snapshots: [W][M+1] host pinned fp32
+  std::vector<std::vector<float*>> snaps;
+  int kernels = 0;
+  int W_lo = 1, W_hi = 0;
+
+  explicit Impl(const SessionConfig& c) : cfg(c) {}
+
+  template <typename T>
+  T* carve(size_t count) {
+    size_t bytes = (count * sizeof(T) + kAlign - 1) / kAlign * kAlign;
+    if (bytes == 0) bytes = kAlign;
+    if (arena_used + bytes > arena_cap) throw std::runtime_error("arena overflow");
+    T* p = reinterpret_cast<T*>(arena + arena_used);
+    arena_used += bytes;
+    return p;
+  }
+
+  ~Impl() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+    for (Stage& s : stages)
+      if (s.stream) cudaStreamDestroy(s.stream);
+    if (origin) cudaStreamDestroy(origin);
+    for (auto& v : snaps)
+      for (float* p : v)
+        if (p) cudaFreeHost(p);
+    if (arena) cudaFree(arena);
+  }
+
+  cudaEvent_t new_event() {
+    cudaEvent_t e;
+    PB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    events.push_back(e);
+    return e;
+  }
+};
+
+// ------------------------------------------------------------------ ctor
+Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
+  SessionConfig& c = cfg_;
+  if (c.widths.size() < 2 || c.acts.size() + 1 != c.widths.size())
+    throw std::invalid_argument("bad network description");
+  if (c.stage_hi == 0) c.stage_hi = c.W;
+  if (c.B % (c.mode == RunMode::timeprest ? c.N : 1) != 0)
+    throw pipesim::domain_error("mini_batch_size",
+                                "mini-batch size " + std::to_string(c.B) +
+                                    " is not divisible by micro-batch count " +
+                                    std::to_string(c.N));
+  PB_CUDA(cudaSetDevice(c.device));
+  init_gemm_attributes();
+  impl_ = std::make_unique<Impl>(cfg_);
+  Impl& I = *impl_;
+  I.W = c.W;
+  I.N = c.N;
+  I.B = c.B;
+  I.M = c.M;
+  I.U = units();
+  I.Rm = c.B / I.U;
+  I.W_lo = c.stage_lo;
+  I.W_hi = c.stage_hi;
+  const int W = c.W, M = c.M, U = I.U;
+
+  // ---------------- network partition (trainer.cpp:104-135)
+  pipesim::network_spec net;
+  net.widths = c.widths;
+  for (int a : c.acts) net.activations.push_back(static_cast<pipesim::activation_kind>(a));
+  net.loss = c.loss == 0 ? pipesim::loss_kind::mse : pipesim::loss_kind::softmax_cross_entropy;
+  const std::vector<pipesim::stage_model> part = pipesim::partition_model(net, W);
+  total_params_ = net.param_count();
+
+  // ---------------- plan
+  // Per stage: ordered tasks (slot numbers) and the pins / prop versions.
+  std::vector<std::vector<std::pair<int, int>>> version_iv(W);  // [s][v] = [from, freed)
+  std::vector<std::vector<std::pair<int, int>>> act_iv(W);      // [s][k-1] = [first fwd, bwd]
+  for (int s = 0; s < W; ++s) {
+    version_iv[s].assign(M + 1, {0, 0});
+    act_iv[s].assign(M, {1 << 30, 0});
+  }
+
+  if (c.mode == RunMode::sequential) {
+    // sequential_epoch (trainer.cpp:510-553): whole mini-batch forward through
+    // all stages, then backward W..1.  Synthetic slots keep the same machinery.
+    int slot = 0;
+    for (int k = 1; k <= M; ++k) {
+      for (int s = 1; s <= W; ++s) {
+        Impl::Task t;
+        t.fwd = true;
+        t.k = k;
+        t.jj = 0;
+        t.s = s;
+        t.slot = ++slot;
+        t.version = k - 1;
+        I.tasks.push_back(t);
+        auto& a = act_iv[s - 1][k - 1];
+        a.first = std::min(a.first, t.slot);
+      }
+      for (int s = W; s >= 1; --s) {
+        Impl::Task t;
+        t.fwd = false;
+        t.k = k;
+        t.s = s;
+        t.slot = ++slot;
+        t.version = k - 1;
+        I.tasks.push_back(t);
+        act_iv[s - 1][k - 1].second = t.slot;
+        version_iv[s - 1][k].first = t.slot;
+        if (k >= 1) version_iv[s - 1][k - 1].second = t.slot + 1;
+      }
+    }
+    for (int s = 0; s < W; ++s) version_iv[s][M].second = slot + 1;
+    horizon_ = slot;
+    ledger_.cfg.workers = W;
+    ledger_.cfg.micro_batches = c.N;
+    ledger_.cfg.mini_batches = M;
+    for (int k = 1; k <= M; ++k) {
+      ledger_.pins.push_back({k, 0, 0, k - 1});
+      ledger_.update_source.push_back(k - 1);
+    }
+  } else {
+    pipesim::sim_config sc;
+    sc.workers = W;
+    sc.micro_batches = c.N;
+    sc.mini_batches = M;
+    sc.samples_per_mini_batch = c.B;
+    const bool nf1b = c.mode == RunMode::timeprest;
+    grid_ = std::make_unique<pipesim::schedule_grid>(
+        nf1b ? pipesim::build_nf1b_schedule(sc) : pipesim::build_1f1b_schedule(sc));
+    ledger_ = pipesim::assign_versions(*grid_, sc);
+    const pipesim::retention_timeline rt =
+        pipesim::build_retention_timeline(ledger_, *grid_);
+    horizon_ = grid_->horizon();
+    std::map<std::pair<int, int>, int> pin;
+    for (const auto& p : ledger_.pins) pin[{p.mini, p.micro}] = p.version;
+    for (int t = 1; t <= horizon_; ++t)
+      for (int s = 1; s <= W; ++s) {
+        const pipesim::task& cell = grid_->at(s, t);
+        if (cell.is_idle()) continue;
+        Impl::Task tk;
+        tk.fwd = cell.is_forward();
+        tk.k = cell.mini;
+        tk.s = s;
+        tk.slot = t;
+        if (tk.fwd) {
+          tk.jj = nf1b ? cell.micro - 1 : 0;
+          tk.version = pin.at({cell.mini, cell.micro});
+          auto& a = act_iv[s - 1][tk.k - 1];
+          a.first = std::min(a.first, t);
+        } else {
+          // nF1B propagates through the latest stage weights (trainer.cpp:479-480);
+          // 1F1B through the stashed pin.  Per-stage latest == k-1 (commits in order).
+          tk.version = nf1b ? tk.k - 1 : pin.at({cell.mini, 0});
+          act_iv[s - 1][tk.k - 1].second = t;
+        }
+        I.tasks.push_back(tk);
+      }
+    for (int s = 0; s < W; ++s)
+      for (int v = 0; v <= M; ++v)
+        version_iv[s][v] = {rt.per_stage[s][v].retained_from_slot,
+                            rt.per_stage[s][v].freed_at_slot};
+  }
+
+  // ---------------- colouring: version pool and activation slots
+  I.stages.resize(W);
+  std::vector<int> pool_n(W), act_n(W);
+  for (int s = 0; s < W; ++s) {
+    Impl::Stage& st = I.stages[s];
+    st.id = s + 1;
+    st.first_layer = part[s].first_layer;
+    st.L = static_cast<int>(part[s].layers.size());
+    st.version_colour = colour(version_iv[s], &pool_n[s], /*half_open=*/true);
+    std::vector<int> ac = colour(act_iv[s], &act_n[s], /*half_open=*/false);
+    st.mini_act.assign(M + 1, 0);
+    for (int k = 1; k <= M; ++k) st.mini_act[k] = ac[k - 1];
+  }
+
+  // ---------------- sizes
+  I.n_out = c.widths.back();
+  I.ld_x = ld8(c.widths.front());
+  auto bytes_of = [](size_t n, size_t sz) { return (n * sz + kAlign - 1) / kAlign * kAlign + kAlign; };
+  size_t need = 0;
+  int64_t off = 0;
+  for (int s = 0; s < W; ++s) {
+    Impl::Stage& st = I.stages[s];
+    st.param_offset = off;
+    for (int l = 0; l < st.L; ++l) {
+      const int gl = st.first_layer + l;
+      Impl::LayerDev d;
+      d.in = c.widths[gl];
+      d.out = c.widths[gl + 1];
+      d.act = c.acts[gl];
+      d.ld_in = ld8(d.in);
+      d.ld_out = ld8(d.out);
+      st.layers.push_back(d);
+      st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
+      need += 2 * (bytes_of(static_cast<size_t>(d.in) * d.out, 4) + bytes_of(d.out, 4));
+      need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2) + bytes_of(d.out, 4));
+      need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
+      if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
+    }
+    off += st.param_count;
+    need += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
+    need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2);
+    if (s == W - 1) need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
+  }
+  const size_t rows = static_cast<size_t>(M) * c.B;
+  need += bytes_of(rows * I.ld_x, 2) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4);
+  I.stage_bytes = rows * std::max<size_t>(c.widths.front(), I.n_out) * 8;
+  need += bytes_of(I.stage_bytes, 1);
+  need += bytes_of(static_cast<size_t>(M) * U * W, 4) + bytes_of(static_cast<size_t>(M) * W, 4);
+  need += 64 * kAlign;
+
+  PB_CUDA(cudaMalloc(&I.arena, need));
+  PB_CUDA(cudaMemset(I.arena, 0, need));
+  I.arena_cap = need;
+  arena_bytes_ = static_cast<int64_t>(need);
+
+  for (int s = 0; s < W; ++s) {
+    Impl::Stage& st = I.stages[s];
+    for (auto& d : st.layers)
+      for (int p = 0; p < 2; ++p) {
+        d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out);
+        d.b32[p] = I.carve<float>(d.out);
+      }
+    st.pool.resize(pool_n[s]);
+    for (auto& ps : st.pool) {
+      for (auto& d : st.layers) {
+        ps.w16.push_back(I.carve<__nv_bfloat16>(static_cast<size_t>(d.out) * d.ld_in));
+        ps.b32.push_back(I.carve<float>(d.out));
+      }
+      ps.tag = I.carve<int>(1);
+    }
+    st.cur_version = I.carve<int>(1);
+    st.acts.resize(act_n[s]);
+    for (auto& as : st.acts) {
+      for (int l = 0; l < st.L; ++l) {
+        const bool logits = (s == W - 1) && (l == st.L - 1);
+        as.out16.push_back(logits ? nullptr
+                                  : I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) *
+                                                           st.layers[l].ld_out));
+      }
+      if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out);
+      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().ld_out);
+    }
+    for (int l = 0; l + 1 < st.L; ++l)
+      st.scratch_dz.push_back(
+          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].ld_out));
+  }
+  I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x);
+  I.y32 = I.carve<float>(rows * I.n_out);
+  I.row_loss = I.carve<float>(rows);
+  I.stage_buf = I.carve<char>(I.stage_bytes);
+  I.fwd_trace = I.carve<int>(static_cast<size_t>(M) * U * W);
+  I.bwd_trace = I.carve<int>(static_cast<size_t>(M) * W);
+
+  PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
+  for (auto& st : I.stages) PB_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+  PB_CUDA(cudaEventCreate(&I.t0));
+  PB_CUDA(cudaEventCreate(&I.t1));
+
+  if (c.snapshots) {
+    I.snaps.assign(W, std::vector<float*>(M + 1, nullptr));
+    for (int s = 0; s < W; ++s)
+      for (int v = 0; v <= M; ++v)
+        PB_CUDA(cudaMallocHost(&I.snaps[s][v], sizeof(float) * std::max<int64_t>(1, I.stages[s].param_count)));
+  }
+
+  // ---------------- compile the program into ops
+  using OK = Impl::OpKind;
+  auto push = [&](Impl::Op op) { I.ops.push_back(op); };
+  const int last_s = W - 1;
+
+  // Rebase (trainer.cpp:372-379): version 0 of this epoch = the previous
+  // epoch's final version.  Masters ping-pong by parity, pool colours are
+  // fixed by the plan, so copy when they differ.
+  for (int s = 0; s < W; ++s) {
+    Impl::Stage& st = I.stages[s];
+    const int cM = st.version_colour[M], c0 = st.version_colour[0];
+    for (int l = 0; l < st.L; ++l) {
+      auto& d = st.layers[l];
+      if (M % 2 == 1) {
+        Impl::Op o{OK::copy};
+        o.stream = s;
+        o.dst = d.w32[0];
+        o.src = d.w32[1];
+        o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
+        push(o);
+        o.dst = d.b32[0];
+        o.src = d.b32[1];
+        o.bytes = sizeof(float) * d.out;
+        push(o);
+      }
+      if (cM != c0) {
+        Impl::Op o{OK::copy};
+        o.stream = s;
+        o.dst = st.pool[c0].w16[l];
+        o.src = st.pool[cM].w16[l];
+        o.bytes = sizeof(__nv_bfloat16) * d.out * static_cast<size_t>(d.ld_in);
+        push(o);
+        o.dst = st.pool[c0].b32[l];
+        o.src = st.pool[cM].b32[l];
+        o.bytes = sizeof(float) * d.out;
+        push(o);
+      }
+    }
+    Impl::Op z{OK::memset_i32};
+    z.stream = s;
+    z.dst = st.pool[c0].tag;
+    z.value = 0;
+    push(z);
+    z.dst = st.cur_version;
+    push(z);
+  }
+
+  std::map<std::tuple<int, int, int>, cudaEvent_t> fwd_done;  // (k, jj, s)
+  std::map<std::pair<int, int>, cudaEvent_t> bwd_done;         // (k, s)
+
+  auto stage_input = [&](int s, int k, int* row_off) -> Mat16 {
+    // Activation entering stage s (0-based) for mini k: data rows or the
+    // previous stage's output slot.
+    if (s == 0) {
+      *row_off = (k - 1) * c.B;
+      return Mat16{I.x16, M * c.B, c.widths.front(), I.ld_x};
+    }
+    const Impl::Stage& pv = I.stages[s - 1];
+    *row_off = 0;
+    const auto& pl = pv.layers.back();
+    return Mat16{pv.acts[pv.mini_act[k]].out16.back(), c.B, pl.out, pl.ld_out};
+  };
+
+  for (const Impl::Task& tk : I.tasks) {
+    const int s = tk.s - 1;
+    Impl::Stage& st = I.stages[s];
+    const int a = st.mini_act[tk.k];
+    Impl::ActSlot& as = st.acts[a];
+    if (tk.fwd) {
+      if (s > 0) {
+        Impl::Op w{OK::wait};
+        w.stream = s;
+        w.ev = fwd_done.at({tk.k, tk.jj, s - 1});
+        push(w);
+      }
+      const Impl::PoolSlot& ps = st.pool[st.version_colour[tk.version]];
+      const int r0 = tk.jj * I.Rm;
+      for (int l = 0; l < st.L; ++l) {
+        const auto& d = st.layers[l];
+        int in_off = 0;
+        Mat16 x;
+        if (l == 0) {
+          x = stage_input(s, tk.k, &in_off);
+        } else {
+          x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
+        }
+        const bool logits = (s == last_s) && (l == st.L - 1);
+        Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
+        Impl::Op o{OK::fwd};
+        o.stream = s;
+        o.g = plan_fwd(x, in_off + r0, I.Rm, w, ps.b32[l], d.act,
+                       logits ? nullptr : as.out16[l], d.ld_out,
+                       logits ? as.out32 : nullptr, I.n_out, r0);
+        if (l == 0) {
+          o.g.ep.tag_src = ps.tag;
+          o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + tk.jj) * W + s;
+        }
+        push(o);
+        ++kernels_per_epoch_;
+      }
+      Impl::Op r{OK::record};
+      r.stream = s;
+      r.ev = I.new_event();
+      fwd_done[{tk.k, tk.jj, s}] = r.ev;
+      push(r);
+      continue;
+    }
+
+    // ---------------- backward of mini k on stage s
+    if (s < last_s) {
+      Impl::Op w{OK::wait};
+      w.stream = s;
+      w.ev = bwd_done.at({tk.k, s + 1});
+      push(w);
+    } else {
+      // fused loss + gradient over the stacked mini-batch (trainer.cpp:461-473)
+      Impl::Op o{OK::loss};
+      o.stream = s;
+      o.y = as.out32;
+      o.rows = c.B;
+      o.cols = I.n_out;
+      o.ld = I.n_out;
+      o.t = I.y32 + static_cast<size_t>(tk.k - 1) * c.B * I.n_out;
+      o.ld_t = I.n_out;
+      o.loss = c.loss;
+      o.act_last = st.layers.back().act;
+      o.denom = static_cast<float>(c.B);
+      o.dz_out = as.dzin;
+      o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
+      o.ld_dz = st.layers.back().ld_out;
+      push(o);
+      ++kernels_per_epoch_;
+    }
+    const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
+    Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
+    const int cur = (tk.k - 1) % 2, nxt = tk.k % 2;
+    for (int l = st.L - 1; l >= 0; --l) {
+      const auto& d = st.layers[l];
+      __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
+      int x_off = 0;
+      Mat16 x;
+      if (l == 0)
+        x = stage_input(s, tk.k, &x_off);
+      else
+        x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
+      Mat16 mdz{dz, c.B, d.out, d.ld_out};
+      // dgrad: delta for the layer below (or the previous stage)
+      if (l > 0 || s > 0) {
+        __nv_bfloat16* dst;
+        int act_prev;
+        if (l > 0) {
+          dst = st.scratch_dz[l - 1];
+          act_prev = st.layers[l - 1].act;
+        } else {
+          const Impl::Stage& pv = I.stages[s - 1];
+          dst = pv.acts[pv.mini_act[tk.k]].dzin;
+          act_prev = pv.layers.back().act;
+        }
+        // act' of the layer below, recovered from the activation it produced
+        // (= this layer's input x).
+        const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld;
+        Impl::Op o{OK::dgrad};
+        o.stream = s;
+        o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
+                         dst, d.ld_in);
+        push(o);
+        ++kernels_per_epoch_;
+      }
+      // wgrad + SGD into the new version (trainer.cpp:244-249, :484-488)
+      {
+        Impl::Op o{OK::wgrad};
+        o.stream = s;
+        o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
+                             d.ld_in, static_cast<float>(c.lr));
+        push(o);
+        ++kernels_per_epoch_;
+      }
+      // bias gradient + SGD; the last one stamps the commit
+      {
+        Impl::Op o{OK::bias};
+        o.stream = s;
+        o.dz = dz;
+        o.rows = c.B;
+        o.cols = d.out;
+        o.ld = d.ld_out;
+        o.b_cur = d.b32[cur];
+        o.b_new = d.b32[nxt];
+        o.b_copy = next.b32[l];
+        o.lr = static_cast<float>(c.lr);
+        if (l == 0) {
+          o.trace_src = prop.tag;
+          o.trace_dst = I.bwd_trace + static_cast<size_t>(tk.k - 1) * W + s;
+          o.tag_slot = next.tag;
+          o.cur_version = st.cur_version;
+          o.version = tk.k;
+        }
+        push(o);
+        ++kernels_per_epoch_;
+      }
+    }
+    if (c.snapshots) {
+      for (int l = 0, po = 0; l < st.L; ++l) {
+        const auto& d = st.layers[l];
+        Impl::Op o{OK::snapshot};
+        o.stream = s;
+        o.dst = I.snaps[s][tk.k] + po;
+        o.src = d.w32[nxt];
+        o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
+        push(o);
+        o.dst = I.snaps[s][tk.k] + po + static_cast<size_t>(d.in) * d.out;
+        o.src = d.b32[nxt];
+        o.bytes = sizeof(float) * d.out;
+        push(o);
+        po += d.in * d.out + d.out;
+      }
+    }
+    Impl::Op r{OK::record};
+    r.stream = s;
+    r.ev = I.new_event();
+    bwd_done[{tk.k, s}] = r.ev;
+    push(r);
+  }
+}
+
+Session::~Session() = default;
+
+int64_t Session::stage_param_count(int s) const { return impl_->stages.at(s - 1).param_count; }
+int64_t Session::stage_param_offset(int s) const {
+  return impl_->stages.at(s - 1).param_offset;
+}
+
+std::vector<int> Session::pool_sizes() const {
+  std::vector<int> v;
+  for (const auto& s : impl_->stages) v.push_back(static_cast<int>(s.pool.size()));
+  return v;
+}
+
+std::vector<int> Session::act_slot_counts() const {
+  std::vector<int> v;
+  for (const auto& s : impl_->stages) v.push_back(static_cast<int>(s.acts.size()));
+  return v;
+}
+
+const float* Session::snapshot(int s, int version) const {
+  if (impl_->snaps.empty()) throw std::invalid_argument("session has no snapshots");
+  return impl_->snaps.at(s - 1).at(version);
+}
+
+// ------------------------------------------------------------------ params
+void Session::load_params(const double* flat) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  std::vector<float> host;
+  for (auto& st : I.stages) {
+    const int c0 = st.version_colour[0];
+    size_t po = static_cast<size_t>(st.param_offset);
+    for (int l = 0; l < st.L; ++l) {
+      auto& d = st.layers[l];
+      const size_t nw = static_cast<size_t>(d.in) * d.out;
+      host.assign(flat + po, flat + po + nw + d.out);
+      PB_CUDA(cudaMemcpy(d.w32[0], host.data(), nw * 4, cudaMemcpyHostToDevice));
+      PB_CUDA(cudaMemcpy(d.b32[0], host.data() + nw, d.out * 4, cudaMemcpyHostToDevice));
+      PB_CUDA(cudaMemcpy(st.pool[c0].b32[l], host.data() + nw, d.out * 4,
+                         cudaMemcpyHostToDevice));
+      launch_f32_to_bf16_rows(I.origin, d.w32[0], d.out, d.in, d.in, st.pool[c0].w16[l],
+                              d.ld_in);
+      // keep the odd master in sync so an M-odd rebase copy is always valid
+      PB_CUDA(cudaMemcpyAsync(d.w32[1], d.w32[0], nw * 4, cudaMemcpyDeviceToDevice, I.origin));
+      PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
+      po += nw + d.out;
+    }
+    // the rebase copies pool[colour(M)] -> pool[colour(0)]: make it a no-op
+    const int cM = st.version_colour[cfg_.M];
+    if (cM != c0)
+      for (int l = 0; l < st.L; ++l) {
+        auto& d = st.layers[l];
+        PB_CUDA(cudaMemcpyAsync(st.pool[cM].w16[l], st.pool[c0].w16[l],
+                                sizeof(__nv_bfloat16) * d.out * static_cast<size_t>(d.ld_in),
+                                cudaMemcpyDeviceToDevice, I.origin));
+        PB_CUDA(cudaMemcpyAsync(st.pool[cM].b32[l], st.pool[c0].b32[l], 4 * d.out,
+                                cudaMemcpyDeviceToDevice, I.origin));
+      }
+  }
+  PB_CUDA(cudaStreamSynchronize(I.origin));
+  if (!I.snaps.empty())
+    for (auto& st : I.stages) {
+      const int s = st.id - 1;
+      std::vector<float> h(flat + st.param_offset, flat + st.param_offset + st.param_count);
+      std::copy(h.begin(), h.end(), I.snaps[s][0]);
+    }
+}
+
+void Session::read_params(double* flat) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  PB_CUDA(cudaDeviceSynchronize());
+  const int p = cfg_.M % 2;  // current version M lives in master[M % 2]
+  std::vector<float> host;
+  for (auto& st : I.stages) {
+    size_t po = static_cast<size_t>(st.param_offset);
+    for (auto& d : st.layers) {
+      const size_t nw = static_cast<size_t>(d.in) * d.out;
+      host.resize(nw + d.out);
+      PB_CUDA(cudaMemcpy(host.data(), d.w32[p], nw * 4, cudaMemcpyDeviceToHost));
+      PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[p], d.out * 4, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < host.size(); ++i) flat[po + i] = host[i];
+      po += nw + d.out;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ data
+__global__ void labels_to_onehot(const int* labels, int rows, int classes, float* y) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<size_t>(rows) * classes; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / classes;
+    y[i] = (labels[r] == static_cast<int>(i % classes)) ? 1.f : 0.f;
+  }
+}
+
+void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
+                     cudaStream_t st) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  if (!st) st = I.origin;
+  const size_t rows = static_cast<size_t>(cfg_.M) * cfg_.B;
+  const int in = cfg_.widths.front();
+  if (xt == HostDType::f64) {
+    PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 8, cudaMemcpyHostToDevice, st));
+    launch_convert_f64_bf16(st, static_cast<const double*>(I.stage_buf), static_cast<int>(rows),
+                            in, in, I.x16, I.ld_x);
+  } else if (xt == HostDType::f32) {
+    PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 4, cudaMemcpyHostToDevice, st));
+    launch_convert_f32_bf16(st, static_cast<const float*>(I.stage_buf), static_cast<int>(rows),
+                            in, in, I.x16, I.ld_x);
+  } else {
+    throw std::invalid_argument("x must be f64 or f32");
+  }
+  if (yt == HostDType::f64) {
+    PB_CUDA(cudaMemcpyAsync(I.stage_buf, y, rows * I.n_out * 8, cudaMemcpyHostToDevice, st));
+    launch_convert_f64_f32(st, static_cast<const double*>(I.stage_buf), I.y32, rows * I.n_out);
+  } else if (yt == HostDType::f32) {
+    PB_CUDA(cudaMemcpyAsync(I.y32, y, rows * I.n_out * 4, cudaMemcpyHostToDevice, st));
+  } else {
+    PB_CUDA(cudaMemcpyAsync(I.stage_buf, y, rows * 4, cudaMemcpyHostToDevice, st));
+    labels_to_onehot<<<1184, 256, 0, st>>>(static_cast<const int*>(I.stage_buf),
+                                            static_cast<int>(rows), I.n_out, I.y32);
+    PB_CUDA(cudaGetLastError());
+  }
+  if (st != I.origin) {
+    cudaEvent_t e = I.new_event();
+    PB_CUDA(cudaEventRecord(e, st));
+    PB_CUDA(cudaStreamWaitEvent(I.origin, e, 0));
+  }
+}
+
+// ------------------------------------------------------------------ run
+namespace {
+void issue(Session::Impl& I, cudaStream_t origin) {
+  using OK = Session::Impl::OpKind;
+  if (!I.fork_ev) {
+    I.fork_ev = I.new_event();
+    for (size_t i = 0; i < I.stages.size(); ++i) I.join_ev.push_back(I.new_event());
+  }
+  cudaEvent_t fork = I.fork_ev;
+  PB_CUDA(cudaEventRecord(fork, origin));
+  for (auto& st : I.stages) PB_CUDA(cudaStreamWaitEvent(st.stream, fork, 0));
+  for (const auto& o : I.ops) {
+    cudaStream_t s = o.stream < 0 ? origin : I.stages[o.stream].stream;
+    switch (o.kind) {
+      case OK::wait: PB_CUDA(cudaStreamWaitEvent(s, o.ev, 0)); break;
+      case OK::record: PB_CUDA(cudaEventRecord(o.ev, s)); break;
+      case OK::fwd: launch_fwd(o.g, s); break;
+      case OK::dgrad: launch_dgrad(o.g, s); break;
+      case OK::wgrad: launch_wgrad(o.g, s); break;
+      case OK::bias:
+        launch_bias_sgd(s, o.dz, o.rows, o.cols, o.ld, o.b_cur, o.b_new, o.b_copy, o.lr,
+                        o.tag_slot, o.cur_version, o.version, o.trace_src, o.trace_dst);
+        break;
+      case OK::loss:
+        launch_loss(s, o.y, o.rows, o.cols, o.ld, o.t, o.ld_t, o.loss, o.act_last, o.denom,
+                    o.dz_out, o.ld_dz, o.row_loss);
+        break;
+      case OK::copy:
+        PB_CUDA(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, s));
+        break;
+      case OK::snapshot:
+        PB_CUDA(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToHost, s));
+        break;
+      case OK::memset_i32:
+        PB_CUDA(cudaMemsetAsync(o.dst, 0, sizeof(int), s));
+        break;
+    }
+  }
+  for (size_t i = 0; i < I.stages.size(); ++i) {
+    PB_CUDA(cudaEventRecord(I.join_ev[i], I.stages[i].stream));
+    PB_CUDA(cudaStreamWaitEvent(origin, I.join_ev[i], 0));
+  }
+}
+}  // namespace
+
+EpochResult Session::run_epoch() {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  PB_CUDA(cudaEventRecord(I.t0, I.origin));
+  if (cfg_.use_graph) {
+    if (!I.exec) {
+      PB_CUDA(cudaStreamBeginCapture(I.origin, cudaStreamCaptureModeThreadLocal));
+      try {
+        issue(I, I.origin);
+      } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(I.origin, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      PB_CUDA(cudaStreamEndCapture(I.origin, &I.graph));
+      PB_CUDA(cudaGraphInstantiate(&I.exec, I.graph, 0));
+    }
+    PB_CUDA(cudaGraphLaunch(I.exec, I.origin));
+  } else {
+    issue(I, I.origin);
+  }
+  PB_CUDA(cudaEventRecord(I.t1, I.origin));
+  PB_CUDA(cudaEventSynchronize(I.t1));
+
+  EpochResult r;
+  PB_CUDA(cudaEventElapsedTime(&r.device_ms, I.t0, I.t1));
+  const int M = cfg_.M, U = I.U, W = cfg_.W, B = cfg_.B;
+  std::vector<float> rl(static_cast<size_t>(M) * B);
+  PB_CUDA(cudaMemcpy(rl.data(), I.row_loss, rl.size() * 4, cudaMemcpyDeviceToHost));
+  r.dev_fwd.resize(static_cast<size_t>(M) * U * W);
+  r.dev_bwd.resize(static_cast<size_t>(M) * W);
+  PB_CUDA(cudaMemcpy(r.dev_fwd.data(), I.fwd_trace, r.dev_fwd.size() * 4, cudaMemcpyDeviceToHost));
+  PB_CUDA(cudaMemcpy(r.dev_bwd.data(), I.bwd_trace, r.dev_bwd.size() * 4, cudaMemcpyDeviceToHost));
+  for (auto& st : I.stages) {
+    int v = 0;
+    PB_CUDA(cudaMemcpy(&v, st.cur_version, 4, cudaMemcpyDeviceToHost));
+    r.dev_current.push_back(v);
+  }
+  // mini loss: mean over micro-batches of the micro mean (trainer.cpp:462-469)
+  const int Rm = I.Rm;
+  for (int k = 0; k < M; ++k) {
+    double tot = 0.0;
+    for (int j = 0; j < U; ++j) {
+      double part = 0.0;
+      for (int q = 0; q < Rm; ++q) part += rl[static_cast<size_t>(k) * B + j * Rm + q];
+      tot += part / Rm;
+    }
+    r.mini_loss.push_back(tot / U);
+  }
+  for (const auto& p : ledger_.pins) r.pinned.push_back(p.version);
+  r.consumed = ledger_.update_source;
+  return r;
+}
+
+}  // namespace pb

@@ -1,0 +1,110 @@
+// Session: the B200 executor of the pipeline-parallel training step
+// (reference: proj/src/trainer.cpp:388-508 replay_grid, :510-553
+// sequential_epoch).
+//
+// A session owns, for one network / train configuration, every device buffer
+// of every pipeline stage and a static program derived from the schedule
+// grid and version ledger (plan.cpp):
+//   * one CUDA stream per stage; a stage executes its grid row in slot order;
+//   * cross-stage edges (activation s -> s+1, delta s+1 -> s) are CUDA events;
+//   * weight versions live in a per-stage bf16 pool sized by the retention
+//     timeline's peak (interval colouring), fp32 masters ping-pong by version
+//     parity; a commit writes the next version in the wgrad+SGD epilogue;
+//   * per-stage activation slots are interval-coloured over
+//     [first forward of mini k, backward of mini k];
+//   * the whole epoch is captured once as a CUDA graph and relaunched.
+// Version accounting is observed on the device: every forward copies the tag
+// of the pool slot it read, every backward the tag of the weights it
+// propagated through, every commit stamps the new slot / current version.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "layer_ops.cuh"
+#include "pipesim_core.hpp"
+
+namespace pb {
+
+enum class RunMode { timeprest = 0, pipedream = 1, sequential = 2 };
+enum class HostDType { f64 = 0, f32 = 1, labels_i32 = 2 };
+
+struct SessionConfig {
+  std::vector<int> widths;
+  std::vector<int> acts;
+  int loss = 1;
+  int W = 2, N = 2, B = 20, M = 10;
+  double lr = 0.05;
+  RunMode mode = RunMode::timeprest;
+  int device = 0;
+  bool use_graph = true;
+  bool snapshots = false;  // per-commit fp32 host snapshots (per-mini digests)
+  // stage range owned by this process (multi-GPU: one process per GPU);
+  // [stage_lo, stage_hi] 1-based inclusive.  Default: all stages.
+  int stage_lo = 1, stage_hi = 0;
+};
+
+struct EpochResult {
+  std::vector<double> mini_loss;  // [M]
+  std::vector<int> pinned;        // [M * units] (ledger)
+  std::vector<int> consumed;      // [M] update_source (ledger)
+  std::vector<int> dev_fwd;       // [M * units * W] tags seen by forwards
+  std::vector<int> dev_bwd;       // [M * W] tags propagated through by backwards
+  std::vector<int> dev_current;   // [W] current version after the epoch
+  float device_ms = 0.f;          // graph/stream time of the epoch
+};
+
+class Session {
+ public:
+  explicit Session(const SessionConfig& cfg);
+  ~Session();
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  const SessionConfig& config() const { return cfg_; }
+  int units() const { return cfg_.mode == RunMode::timeprest ? cfg_.N : 1; }
+  int64_t param_count() const { return total_params_; }
+  int64_t stage_param_count(int s) const;  // 1-based
+  int64_t stage_param_offset(int s) const;
+
+  // Installs a flat whole-network parameter vector as version 0.
+  void load_params(const double* flat);
+  // Copies the current version's fp32 masters out as doubles (flat layout).
+  void read_params(double* flat);
+  // fp32 snapshot of `version` of stage s (requires snapshots=true).
+  const float* snapshot(int s, int version) const;
+
+  // Host -> device copy of the epoch's data (rows = M*B), then conversion.
+  void upload(const void* x, HostDType xt, const void* y, HostDType yt,
+              cudaStream_t st = nullptr);
+  // Runs one epoch on the uploaded data.  `epoch` only tags the result.
+  EpochResult run_epoch();
+
+  // Ledger / plan of the session (for logs and checks).
+  const pipesim::version_ledger& ledger() const { return ledger_; }
+  const pipesim::schedule_grid* grid() const { return grid_.get(); }
+  int horizon() const { return horizon_; }
+  std::vector<int> pool_sizes() const;
+  std::vector<int> act_slot_counts() const;
+  int64_t device_bytes() const { return arena_bytes_; }
+  int kernels_per_epoch() const { return kernels_per_epoch_; }
+
+  struct Impl;  // public so the program-issue helpers can see it
+
+ private:
+  SessionConfig cfg_;
+  std::unique_ptr<Impl> impl_;
+  std::unique_ptr<pipesim::schedule_grid> grid_;
+  pipesim::version_ledger ledger_;
+  int horizon_ = 0;
+  int64_t total_params_ = 0;
+  int64_t arena_bytes_ = 0;
+  int kernels_per_epoch_ = 0;
+};
+
+}  // namespace pb
