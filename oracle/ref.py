@@ -63,6 +63,18 @@ def schedule(w, n, m, mode=0):
     return cells
 
 
+def validate(w, n, m, mode, cells):
+    """validate_schedule on a [W][H][3] grid -> [(kind, message)]."""
+    cells = np.ascontiguousarray(cells, np.int32)
+    nv = C.c_int()
+    kinds = np.zeros(4096, np.int32)
+    msg = C.create_string_buffer(1 << 20)
+    _check(lib().ref_validate(w, n, m, mode, _ip(cells), cells.shape[1], C.byref(nv),
+                              _ip(kinds), 4096, msg, 1 << 20))
+    lines = msg.value.decode().split("\n")
+    return [(int(kinds[i]), lines[i]) for i in range(nv.value)]
+
+
 def render_ascii(w, n, m, mode=0):
     buf = C.create_string_buffer(1 << 20)
     _check(lib().ref_render_ascii(w, n, m, mode, buf, 1 << 20))

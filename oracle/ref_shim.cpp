@@ -106,6 +106,32 @@ int ref_schedule(int w, int n, int m, int mode, int* horizon, int* cells, int ca
   }
 }
 
+// validate_schedule on an arbitrary (possibly hand-mutated) grid given as
+// [W][H][3] cells; kinds[i] / '\n'-joined messages.
+int ref_validate(int w, int n, int m, int mode, const int* cells, int h, int* n_viol,
+                 int* kinds, int cap, char* msgs, int msg_cap) {
+  try {
+    const sim_config c = mk(w, n, m);
+    schedule_grid g(c, mode == 0 ? schedule_mode::timeprest : schedule_mode::pipedream);
+    for (int s = 1; s <= w; ++s)
+      for (int t = 1; t <= h; ++t) {
+        const int* x = cells + 3 * (static_cast<size_t>(s - 1) * h + (t - 1));
+        g.put(s, t, task{static_cast<task_kind>(x[0]), x[1], x[2]});
+      }
+    const validation_report r = validate_schedule(g, c);
+    *n_viol = static_cast<int>(r.violations.size());
+    std::string text;
+    for (size_t i = 0; i < r.violations.size(); ++i) {
+      if (static_cast<int>(i) < cap) kinds[i] = static_cast<int>(r.violations[i].kind);
+      text += r.violations[i].message + "\n";
+    }
+    put_str(text, msgs, msg_cap);
+    return 0;
+  } catch (...) {
+    return fail();
+  }
+}
+
 int ref_render_ascii(int w, int n, int m, int mode, char* buf, int cap) {
   try {
     put_str(render_ascii(build(w, n, m, mode)), buf, cap);

@@ -104,7 +104,7 @@ def lib() -> C.CDLL:
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `make -C "
                 f"{_HERE}` or __graft_entry__.build(); there is no CPU fallback")
-        _lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+        _lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_LOCAL)
         _declare(_lib)
     return _lib
 
