@@ -75,6 +75,202 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
   }
 }
 
+// Fused epilogue on one 16-column chunk of one output row (fp32 values).
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmShape& sh,
+                                               int row, int n, int valid, float (&v)[16]) {
+  if constexpr (EPI == kEpiFwd) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float b = (ep.bias && i < valid) ? ep.bias[n + i] : 0.f;
+      v[i] = act_fwd(v[i] + b, ep.act);
+    }
+    const size_t yr = static_cast<size_t>(row + ep.y_row_off);
+    if (ep.y16)
+      store_bf16x16(ep.y16 + yr * ep.ld_y16 + n, v, valid,
+                    (ep.ld_y16 % 8) == 0);
+    if (ep.y32) {
+      float* dst = ep.y32 + yr * ep.ld_y32 + n;
+      if (valid == 16 && (ep.ld_y32 % 4) == 0) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      } else {
+        for (int i = 0; i < valid; ++i) dst[i] = v[i];
+      }
+    }
+  } else if constexpr (EPI == kEpiDgrad) {
+    if (ep.act_prev != kLinear) {
+      const __nv_bfloat16* xr = ep.xin + static_cast<size_t>(row) * ep.ld_xin + n;
+      if (valid == 16 && (ep.ld_xin % 8) == 0) {
+        const uint4* x4 = reinterpret_cast<const uint4*>(xr);
+        uint4 q[2] = {x4[0], x4[1]};
+        const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(q);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          v[i] *= act_grad_from_out(__bfloat162float(xh[i]), ep.act_prev);
+      } else {
+        for (int i = 0; i < valid; ++i)
+          v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
+      }
+    }
+    store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
+                  (ep.ld_d16 % 8) == 0);
+  } else {  // kEpiWgradSgd
+    const size_t o32 = static_cast<size_t>(row) * ep.ld_w32 + n;
+    if (valid == 16 && (ep.ld_w32 % 4) == 0) {
+      const float4* c4 = reinterpret_cast<const float4*>(ep.w_cur + o32);
+      float4* n4 = reinterpret_cast<float4*>(ep.w_new + o32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 w = c4[i];
+        w.x -= ep.lr * v[4 * i];
+        w.y -= ep.lr * v[4 * i + 1];
+        w.z -= ep.lr * v[4 * i + 2];
+        w.w -= ep.lr * v[4 * i + 3];
+        v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
+        n4[i] = w;
+      }
+    } else {
+      for (int i = 0; i < valid; ++i) {
+        const float w = ep.w_cur[o32 + i] - ep.lr * v[i];
+        ep.w_new[o32 + i] = w;
+        v[i] = w;
+      }
+    }
+    if (ep.w16)
+      store_bf16x16(ep.w16 + static_cast<size_t>(row) * ep.ld_w16 + n, v, valid,
+                    (ep.ld_w16 % 8) == 0);
+  }
+}
+
+// Epilogue of one warp's 32 output rows x BN columns of an accumulator.
+//
+// tcgen05.ld hands thread i row i (32 consecutive columns per load).  Each
+// 32x32 block is transposed through padded smem (conflict-free: 33-float
+// rows) so that afterwards lane l owns column l of all 32 rows: every global
+// access of the epilogue (bias, activations in, weights in/out) becomes one
+// 128-byte (fp32) or 64-byte (bf16) contiguous row segment per instruction,
+// and the 32 row loads of a block are issued back to back (memory-level
+// parallelism for the HBM-bound SGD update).
+template <int EPI>
+__device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const GemmShape& sh,
+                                                   int row_base, int n_base, int n_cols,
+                                                   uint32_t t_row, float* T) {
+  const int lane = threadIdx.x % 32;
+  int rows_valid = sh.M - row_base;
+  rows_valid = rows_valid > 32 ? 32 : rows_valid;
+  // SGD: master weights of the next chunk are prefetched while this chunk
+  // is processed (two chunks of row loads in flight per warp).
+  float wnext[32];
+  if constexpr (EPI == kEpiWgradSgd) {
+    const int n = n_base + lane;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      wnext[i] = (i < rows_valid && n < sh.N)
+                     ? ep.w_cur[static_cast<size_t>(row_base + i) * ep.ld_w32 + n]
+                     : 0.f;
+  }
+#pragma unroll 1
+  for (int c = 0; c < n_cols; c += 32) {
+    if (n_base + c >= sh.N) break;  // warp-uniform
+    float wcur[32];
+    if constexpr (EPI == kEpiWgradSgd) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) wcur[i] = wnext[i];
+      const int nn = n_base + c + 32 + lane;
+      if (c + 32 < n_cols) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          wnext[i] = (i < rows_valid && nn < sh.N)
+                         ? ep.w_cur[static_cast<size_t>(row_base + i) * ep.ld_w32 + nn]
+                         : 0.f;
+      }
+    }
+    uint32_t r[32];
+    ptx::tmem_ld32(t_row + c, r);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
+    __syncwarp();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = T[i * 33 + lane];
+    __syncwarp();
+    const int n = n_base + c + lane;
+    const bool col_ok = n < sh.N;
+    int rows = sh.M - row_base;
+    rows = rows > 32 ? 32 : rows;  // valid rows of this warp block
+
+    if constexpr (EPI == kEpiFwd) {
+      const float b = (ep.bias && col_ok) ? ep.bias[n] : 0.f;
+      if (col_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i >= rows) break;
+          const float a = act_fwd(v[i] + b, ep.act);
+          const size_t yr = static_cast<size_t>(row_base + i + ep.y_row_off);
+          if (ep.y16) ep.y16[yr * ep.ld_y16 + n] = __float2bfloat16_rn(a);
+          if (ep.y32) ep.y32[yr * ep.ld_y32 + n] = a;
+        }
+      }
+    } else if constexpr (EPI == kEpiDgrad) {
+      if (col_ok) {
+        if (ep.act_prev != kLinear) {
+          float g[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            g[i] = i < rows ? __bfloat162float(
+                                  ep.xin[static_cast<size_t>(row_base + i) * ep.ld_xin + n])
+                            : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(g[i], ep.act_prev);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i >= rows) break;
+          ep.d16[static_cast<size_t>(row_base + i) * ep.ld_d16 + n] = __float2bfloat16_rn(v[i]);
+        }
+      }
+    } else {  // kEpiWgradSgd: w_new = w_cur - lr * g ; w16 = bf16(w_new)
+      if (col_ok) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i >= rows) break;
+          const float nw = wcur[i] - ep.lr * v[i];
+          ep.w_new[static_cast<size_t>(row_base + i) * ep.ld_w32 + n] = nw;
+          if (ep.w16)
+            ep.w16[static_cast<size_t>(row_base + i) * ep.ld_w16 + n] = __float2bfloat16_rn(nw);
+        }
+      }
+    }
+  }
+}
+
+// Row-per-thread epilogue (thread i owns row i; 16-column vector chunks).
+template <int EPI>
+__device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const GemmShape& sh,
+                                                   int row_base, int n_base, int n_cols,
+                                                   uint32_t t_row) {
+  const int row = row_base + static_cast<int>(threadIdx.x % 32);
+  const bool row_ok = row < sh.M;
+#pragma unroll 1
+  for (int c = 0; c < n_cols; c += 16) {
+    const int n = n_base + c;
+    if (n >= sh.N) break;  // warp-uniform
+    uint32_t r[16];
+    ptx::tmem_ld16(t_row + c, r);
+    ptx::tmem_ld_wait();
+    if (!row_ok) continue;
+    const int valid = sh.N - n < 16 ? sh.N - n : 16;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    epilogue_chunk<EPI>(ep, sh, row, n, valid, v);
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
@@ -173,8 +369,6 @@ __global__ void __launch_bounds__(128, 1)
   ptx::mbar_wait(accum_bar, 0);
   ptx::tc_fence_after();
 
-  const int row = m0 + warp * 32 + lane;
-  const bool row_ok = row < sh.M;
   const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
 
   if (EPI == kEpiFwd || EPI == kEpiDgrad) {
@@ -182,91 +376,204 @@ __global__ void __launch_bounds__(128, 1)
         ep.tag_dst)
       *ep.tag_dst = *ep.tag_src;
   }
-
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    const int n = n0 + c;
-    if (n >= sh.N) break;  // warp-uniform
-    uint32_t r[16];
-    ptx::tmem_ld16(t_row + c, r);
-    ptx::tmem_ld_wait();
-    if (!row_ok) continue;
-    const int valid = sh.N - n < 16 ? sh.N - n : 16;
-    float v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-
-    if constexpr (EPI == kEpiFwd) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float b = (ep.bias && i < valid) ? ep.bias[n + i] : 0.f;
-        v[i] = act_fwd(v[i] + b, ep.act);
-      }
-      const size_t yr = static_cast<size_t>(row + ep.y_row_off);
-      if (ep.y16)
-        store_bf16x16(ep.y16 + yr * ep.ld_y16 + n, v, valid,
-                      (ep.ld_y16 % 8) == 0);
-      if (ep.y32) {
-        float* dst = ep.y32 + yr * ep.ld_y32 + n;
-        if (valid == 16 && (ep.ld_y32 % 4) == 0) {
-          float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-          for (int i = 0; i < valid; ++i) dst[i] = v[i];
-        }
-      }
-    } else if constexpr (EPI == kEpiDgrad) {
-      if (ep.act_prev != kLinear) {
-        const __nv_bfloat16* xr = ep.xin + static_cast<size_t>(row) * ep.ld_xin + n;
-        if (valid == 16 && (ep.ld_xin % 8) == 0) {
-          const uint4* x4 = reinterpret_cast<const uint4*>(xr);
-          uint4 q[2] = {x4[0], x4[1]};
-          const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(q);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            v[i] *= act_grad_from_out(__bfloat162float(xh[i]), ep.act_prev);
-        } else {
-          for (int i = 0; i < valid; ++i)
-            v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
-        }
-      }
-      store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
-                    (ep.ld_d16 % 8) == 0);
-    } else {  // kEpiWgradSgd
-      const size_t o32 = static_cast<size_t>(row) * ep.ld_w32 + n;
-      if (valid == 16 && (ep.ld_w32 % 4) == 0) {
-        const float4* c4 = reinterpret_cast<const float4*>(ep.w_cur + o32);
-        float4* n4 = reinterpret_cast<float4*>(ep.w_new + o32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float4 w = c4[i];
-          w.x -= ep.lr * v[4 * i];
-          w.y -= ep.lr * v[4 * i + 1];
-          w.z -= ep.lr * v[4 * i + 2];
-          w.w -= ep.lr * v[4 * i + 3];
-          v[4 * i] = w.x; v[4 * i + 1] = w.y; v[4 * i + 2] = w.z; v[4 * i + 3] = w.w;
-          n4[i] = w;
-        }
-      } else {
-        for (int i = 0; i < valid; ++i) {
-          const float w = ep.w_cur[o32 + i] - ep.lr * v[i];
-          ep.w_new[o32 + i] = w;
-          v[i] = w;
-        }
-      }
-      if (ep.w16)
-        store_bf16x16(ep.w16 + static_cast<size_t>(row) * ep.ld_w16 + n, v, valid,
-                      (ep.ld_w16 % 8) == 0);
-    }
-  }
+  // the operand ring is idle now: reuse it for the per-warp transpose blocks
+  float* T = reinterpret_cast<float*>(sA) + warp * 32 * 33;
+  if (ep.rowwise)
+    epilogue_warp_rows<EPI>(ep, sh, m0 + warp * 32, n0, BN, t_row);
+  else
+    epilogue_warp_tile<EPI>(ep, sh, m0 + warp * 32, n0, BN, t_row, T);
 
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ===========================================================================
+// Persistent CTA-pair kernel (cta_group::2).
+//
+// A cluster of 2 CTAs on neighbouring SMs computes 256 x BN output tiles:
+// CTA r holds A rows [128r, 128r+128) and B rows [r*BN/2, (r+1)*BN/2) of the
+// tile in its own smem; one tcgen05.mma.cta_group::2 (M=256) issued by the
+// leader reads both halves and accumulates into both CTAs' TMEM (CTA r gets
+// output rows [128r, +128)).  Per SM this halves the B-operand bytes per FLOP
+// versus a 128 x BN single-CTA tile.  The pair walks a static tile schedule;
+// TMEM holds two accumulators so the epilogue of tile i (4 warps) overlaps
+// the mainloop of tile i+1.
+//
+// Warps: 0 TMA producer (both CTAs), 1 MMA issuer (leader) + TMEM owner,
+//        2..5 epilogue (TMEM lanes 32*(warp%4) .. +32).
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int kBK = 64;
+  static constexpr int kAHalf = 128 * kBK * 2;         // this CTA's A rows
+  static constexpr int kBHalf = (BN / 2) * kBK * 2;    // this CTA's B rows
+  static constexpr int kStageBytes = kAHalf + kBHalf;
+  static constexpr int kStages = BN >= 256 ? 6 : 8;
+  static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;  // per-warp transpose blocks
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 512;
+  static constexpr uint32_t kTmemCols = 2 * BN;        // double-buffered accumulator
+};
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThreads, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a,
+                           const __grid_constant__ CUtensorMap tmap_b, GemmShape sh,
+                           EpiParams ep) {
+  using Cfg = Gemm2Cfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kAHalf;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;   // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's are used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* epi_smem = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + 512);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x / 2;
+  const int num_pairs = gridDim.x / 2;
+  const int tiles_m = (sh.M + 255) / 256;
+  const int tiles_n = (sh.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch_desc(&tmap_a);
+    ptx::tma_prefetch_desc(&tmap_b);
+    for (int i = 0; i < S; ++i) {
+      ptx::mbar_init(&full_bar[i], 1);
+      ptx::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull_bar[i], 1);
+      ptx::mbar_init(&tempty_bar[i], 2);  // one arrival per CTA of the pair
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs), completion on the leader's barrier
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        const int tm = tile / tiles_n, tn = tile % tiles_n;
+        const int m0 = tm * 256 + static_cast<int>(rank) * 128;
+        const int nb0 = tn * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % S;
+          if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
+          const uint32_t fb = ptx::map_to_rank(&full_bar[s], 0);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * Cfg::kStageBytes);
+          const int k0 = kb * Cfg::kBK;
+          uint8_t* a_dst = sA + s * Cfg::kAHalf;
+          uint8_t* b_dst = sB + s * Cfg::kBHalf;
+          if constexpr (!A_MN) {
+            ptx::tma_load_2d_pair(a_dst, &tmap_a, fb, k0 + sh.a_k_off, m0 + sh.a_mn_off);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ptx::tma_load_2d_pair(a_dst + h * 8192, &tmap_a, fb, m0 + h * 64 + sh.a_mn_off,
+                                    k0 + sh.a_k_off);
+          }
+          if constexpr (!B_MN) {
+            ptx::tma_load_2d_pair(b_dst, &tmap_b, fb, k0 + sh.b_k_off, nb0 + sh.b_mn_off);
+          } else {
+#pragma unroll
+            for (int h = 0; h < BN / 128; ++h)
+              ptx::tma_load_2d_pair(b_dst + h * 8192, &tmap_b, fb, nb0 + h * 64 + sh.b_mn_off,
+                                    k0 + sh.b_k_off);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
+      int it = 0, local = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+        const int acc = local & 1;
+        const int use = local >> 1;
+        ptx::mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % S;
+          ptx::mbar_wait(&full_bar[s], (it / S) & 1);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + s * Cfg::kAHalf);
+          const uint32_t b_addr = ptx::smem_u32(sB + s * Cfg::kBHalf);
+#pragma unroll
+          for (int kk = 0; kk < Cfg::kBK / 16; ++kk) {
+            const uint64_t a_desc =
+                A_MN ? ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                     : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t b_desc =
+                B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                     : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+            ptx::mma_bf16_pair(d_tmem, a_desc, b_desc, idesc, (kb | kk) != 0);
+          }
+          ptx::mma_commit_pair(&empty_bar[s], 0x3);
+        }
+        ptx::mma_commit_pair(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2.., both CTAs.  Warp e covers TMEM lane
+    // quarter (warp % 4) and column half e / 4 of the tile.
+    const int e = warp - 2;
+    const int q = warp % 4;  // TMEM lane quarter this warp may access
+    constexpr int kColsPerWarp = BN / (Cfg::kEpiWarps / 4);
+    const int c_off = (e / 4) * kColsPerWarp;
+    float* T = epi_smem + e * 32 * 33;
+    const uint32_t tempty_leader_0 = ptx::map_to_rank(&tempty_bar[0], 0);
+    const uint32_t tempty_leader_1 = ptx::map_to_rank(&tempty_bar[1], 0);
+    int local = 0;
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+      const int acc = local & 1;
+      const int use = local >> 1;
+      const int tm = tile / tiles_n, tn = tile % tiles_n;
+      ptx::mbar_wait(&tfull_bar[acc], use & 1);
+      ptx::tc_fence_after();
+      const int row_base = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
+      const uint32_t t_row =
+          tmem_base + acc * BN + c_off + (static_cast<uint32_t>(q * 32) << 16);
+      if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && rank == 0 && e == 0 &&
+          lane == 0 && ep.tag_src && ep.tag_dst)
+        *ep.tag_dst = *ep.tag_src;
+      if (ep.rowwise)
+        epilogue_warp_rows<EPI>(ep, sh, row_base, tn * BN + c_off, kColsPerWarp, t_row);
+      else
+        epilogue_warp_tile<EPI>(ep, sh, row_base, tn * BN + c_off, kColsPerWarp, t_row, T);
+      ptx::tc_fence_before();
+      ptx::named_bar_sync(1, 32 * Cfg::kEpiWarps);
+      if (e == 0 && lane == 0)
+        ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader_0 : tempty_leader_1);
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
   }
 }
 

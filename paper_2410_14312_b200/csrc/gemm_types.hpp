@@ -42,6 +42,9 @@ struct EpiParams {
   // set, CTA (0,0) copies *tag_src into *tag_dst.
   const int* tag_src;
   int* tag_dst;
+  // epilogue access pattern: 0 = transposed (coalesced rows, lane = column),
+  // 1 = row-per-thread vectors
+  int rowwise;
 };
 
 }  // namespace pb

@@ -2,7 +2,10 @@
 // bias+SGD, and boundary conversions.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "gemm_sm100.cuh"
 #include "layer_ops.cuh"
@@ -52,20 +55,55 @@ CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn) {
   return map;
 }
 
+// Kernel choice.  Tall problems (M > 128) use the persistent CTA-pair kernel
+// (256 x BN tiles, overlapped epilogue); M <= 128 (micro-batch forwards of
+// <=128 rows, tiny nets) use the single-CTA 128 x BN kernel.
+// PIPESIM_GEMM=single forces the single-CTA kernel (A/B comparisons).
+namespace {
+bool pair_allowed() {
+  static const bool ok = [] {
+    const char* e = std::getenv("PIPESIM_GEMM");
+    return !(e && std::string(e) == "single");
+  }();
+  return ok;
+}
+}  // namespace
+
 int pick_bn(int M, int N) {
+  if (M > 128 && pair_allowed()) return N > 128 ? 256 : 128;
   const long tiles256 = static_cast<long>((M + 127) / 128) * ((N + 255) / 256);
   return (N > 128 && tiles256 >= 132) ? 256 : 128;
 }
 
+static bool use_pair(int M) { return M > 128 && pair_allowed(); }
+
 namespace {
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_one(const GemmLaunch& g, cudaStream_t st) {
-  auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
-  constexpr int smem = GemmCfg<BN>::kSmem;
   init_gemm_attributes();
-  dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128);
-  kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+  if (g.pair) {
+    auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>;
+    constexpr int smem = Gemm2Cfg<BN>::kSmem;
+    const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
+    const int pairs = std::min(tiles, std::max(1, sm_count() / 2));
+    kern<<<dim3(2 * pairs), Gemm2Cfg<BN>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+  } else {
+    auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
+    constexpr int smem = GemmCfg<BN>::kSmem;
+    dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128);
+    kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+  }
   PB_CUDA(cudaGetLastError());
 }
 
@@ -74,6 +112,9 @@ void set_attr() {
   PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                GemmCfg<BN>::kSmem));
+  PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Gemm2Cfg<BN>::kSmem));
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -100,10 +141,27 @@ void init_gemm_attributes() {
 
 namespace {
 
-EpiParams empty_epi() {
+// PIPESIM_EPI=rows|tile|auto (default auto: row-per-thread vectors for the
+// bf16 epilogues, transposed coalesced rows for the fp32 SGD update).
+int epi_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("PIPESIM_EPI");
+    if (e && std::string(e) == "rows") return 1;
+    if (e && std::string(e) == "tile") return 0;
+    return 2;
+  }();
+  return m;
+}
+
+EpiParams empty_epi(int kind) {
   EpiParams e{};
+  const int m = epi_mode();
+  e.rowwise = m == 2 ? (kind == kEpiWgradSgd ? 0 : 1) : m;
   return e;
 }
+
+// B-operand box rows for a K-major B: the pair kernel loads half a tile.
+int b_box(const GemmLaunch& g) { return g.pair ? g.bn / 2 : g.bn; }
 
 }  // namespace
 
@@ -112,10 +170,11 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     float* y32, int ld_y32, int y_row_off) {
   GemmLaunch g;
   g.bn = pick_bn(rows, w.rows);
+  g.pair = use_pair(rows);
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
-  g.tb = make_operand_tmap(w, /*k_major=*/true, g.bn);
+  g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
   g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0};
-  g.ep = empty_epi();
+  g.ep = empty_epi(kEpiFwd);
   g.ep.bias = bias;
   g.ep.act = act;
   g.ep.y16 = y16;
@@ -130,10 +189,11 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
                       int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d) {
   GemmLaunch g;
   g.bn = pick_bn(dz.rows, w.cols);
+  g.pair = use_pair(dz.rows);
   g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0};
-  g.ep = empty_epi();
+  g.ep = empty_epi(kEpiDgrad);
   g.ep.xin = xin;
   g.ep.ld_xin = ld_xin;
   g.ep.act_prev = act_prev;
@@ -147,10 +207,11 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           __nv_bfloat16* w16, int ld_w16, float lr) {
   GemmLaunch g;
   g.bn = pick_bn(dz.cols, x.cols);
+  g.pair = use_pair(dz.cols);
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
   g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};
-  g.ep = empty_epi();
+  g.ep = empty_epi(kEpiWgradSgd);
   g.ep.w_cur = w_cur;
   g.ep.w_new = w_new;
   g.ep.ld_w32 = ld_w32;

@@ -32,6 +32,7 @@ struct GemmLaunch {
   GemmShape sh;
   EpiParams ep;
   int bn;
+  bool pair = false;  // persistent CTA-pair kernel
 };
 
 // forward: out = act(x[rows, in] * w[out, in]^T + b)
