@@ -215,6 +215,7 @@ typedef struct {
   int device;           /* CUDA device of all stages */
   int use_graph;        /* capture the epoch as one CUDA graph */
   int snapshots;        /* keep fp32 host snapshots of every committed version */
+  int fwd_merge;        /* max micro-batches per coalesced forward launch (0 = N) */
 } pb_train_config;      /* train_config, trainer.hpp:117-126 */
 
 typedef struct {

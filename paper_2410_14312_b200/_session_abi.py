@@ -9,7 +9,8 @@ class pb_train_config(C.Structure):
     _fields_ = [("workers", C.c_int), ("micro_batches", C.c_int),
                 ("mini_batch_size", C.c_int), ("mini_batches", C.c_int),
                 ("learning_rate", C.c_double), ("mode", C.c_int), ("device", C.c_int),
-                ("use_graph", C.c_int), ("snapshots", C.c_int)]
+                ("use_graph", C.c_int), ("snapshots", C.c_int),
+                ("fwd_merge", C.c_int)]
 
 
 class pb_epoch_out(C.Structure):

@@ -1,4 +1,5 @@
 // C ABI over the pipeline session (include/pipesim_b200.h, "pipeline session").
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -80,6 +81,8 @@ int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
   c.device = cfg->device;
   c.use_graph = cfg->use_graph != 0;
   c.snapshots = cfg->snapshots != 0;
+  c.fwd_merge = cfg->fwd_merge;
+  if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
   auto* s = new pb_session;
   try {
     s->impl = std::make_unique<pb::Session>(c);

@@ -75,6 +75,14 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
   }
 }
 
+// Device-side version accounting: copy the tag of the weight slot this GEMM
+// read into the trace entries of the micro-batches it served.
+__device__ __forceinline__ void write_tags(const EpiParams& ep) {
+  const int v = *ep.tag_src;
+  const int n = ep.tag_count > 0 ? ep.tag_count : 1;
+  for (int i = 0; i < n; ++i) ep.tag_dst[static_cast<size_t>(i) * ep.tag_stride] = v;
+}
+
 // Fused epilogue on one 16-column chunk of one output row (fp32 values).
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmShape& sh,
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(128, 1)
   if (EPI == kEpiFwd || EPI == kEpiDgrad) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && ep.tag_src &&
         ep.tag_dst)
-      *ep.tag_dst = *ep.tag_src;
+      write_tags(ep);
   }
   // the operand ring is idle now: reuse it for the per-warp transpose blocks
   float* T = reinterpret_cast<float*>(sA) + warp * 32 * 33;
@@ -556,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
           tmem_base + acc * BN + c_off + (static_cast<uint32_t>(q * 32) << 16);
       if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && rank == 0 && e == 0 &&
           lane == 0 && ep.tag_src && ep.tag_dst)
-        *ep.tag_dst = *ep.tag_src;
+        write_tags(ep);
       if (ep.rowwise)
         epilogue_warp_rows<EPI>(ep, sh, row_base, tn * BN + c_off, kColsPerWarp, t_row);
       else

@@ -42,6 +42,8 @@ struct EpiParams {
   // set, CTA (0,0) copies *tag_src into *tag_dst.
   const int* tag_src;
   int* tag_dst;
+  int tag_count;   // entries written (a coalesced forward covers several micro-batches)
+  int tag_stride;  // element stride between entries
   // epilogue access pattern: 0 = transposed (coalesced rows, lane = column),
   // 1 = row-per-thread vectors
   int rowwise;

@@ -232,30 +232,53 @@ void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ bias + SGD
-// One thread column per output feature, 8 row groups reduced in smem; the
-// summation order is fixed, so the result is deterministic.
-__global__ void bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows,
-                                int out, int ld_dz, const float* b_cur,
-                                float* b_new, float* b_copy, float lr,
-                                int* tag_slot, int* cur_version, int version,
-                                const int* trace_src, int* trace_dst) {
-  __shared__ float part[8][33];
-  const int col = blockIdx.x * 32 + threadIdx.x;
-  float acc = 0.f;
-  if (col < out)
-    for (int r = threadIdx.y; r < rows; r += 8)
-      acc += __bfloat162float(dz[static_cast<size_t>(r) * ld_dz + col]);
-  part[threadIdx.y][threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.y == 0 && col < out) {
-    float g = 0.f;
+// b_new = b_cur - lr * colsum(dz).  A block owns 32 output columns; 256
+// threads = 4 column groups (8 bf16 columns each, one 16-byte load) x 64 row
+// groups.  Row-group partials are combined in a fixed order in smem, so the
+// result is deterministic.  (trainer.cpp:250-252 and :484-488.)
+constexpr int kBiasCols = 32;
+constexpr int kBiasRowGroups = 64;
+
+__global__ void __launch_bounds__(256)
+    bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows, int out, int ld_dz,
+                    const float* b_cur, float* b_new, float* b_copy, float lr,
+                    int* tag_slot, int* cur_version, int version, const int* trace_src,
+                    int* trace_dst) {
+  __shared__ float part[kBiasRowGroups][kBiasCols + 1];
+  const int cx = threadIdx.x % 4;
+  const int ry = threadIdx.x / 4;
+  const int c0 = blockIdx.x * kBiasCols + cx * 8;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool vec = (ld_dz % 8) == 0 && c0 + 8 <= out;
+  for (int r = ry; r < rows; r += kBiasRowGroups) {
+    const __nv_bfloat16* p = dz + static_cast<size_t>(r) * ld_dz + c0;
+    if (vec) {
+      const uint4 q = *reinterpret_cast<const uint4*>(p);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) g += part[i][threadIdx.x];
-    const float b = b_cur[col] - lr * g;
-    b_new[col] = b;
-    if (b_copy) b_copy[col] = b;
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    } else {
+      for (int k = 0; k < 8 && c0 + k < out; ++k) acc[k] += __bfloat162float(p[k]);
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) part[ry][cx * 8 + k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < kBiasCols) {
+    const int col = blockIdx.x * kBiasCols + threadIdx.x;
+    if (col < out) {
+      float g = 0.f;
+      for (int i = 0; i < kBiasRowGroups; ++i) g += part[i][threadIdx.x];
+      const float b = b_cur[col] - lr * g;
+      b_new[col] = b;
+      if (b_copy) b_copy[col] = b;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (trace_src && trace_dst) *trace_dst = *trace_src;
     if (tag_slot) *tag_slot = version;
     if (cur_version) *cur_version = version;
@@ -266,70 +289,92 @@ void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int out, int ld_dz, const float* b_cur, float* b_new,
                      float* b_copy, float lr, int* tag_slot, int* cur_version,
                      int version, const int* trace_src, int* trace_dst) {
-  dim3 block(32, 8);
-  dim3 grid((out + 31) / 32);
-  bias_sgd_kernel<<<grid, block, 0, st>>>(dz, rows, out, ld_dz, b_cur, b_new,
-                                          b_copy, lr, tag_slot, cur_version,
-                                          version, trace_src, trace_dst);
+  bias_sgd_kernel<<<(out + kBiasCols - 1) / kBiasCols, 256, 0, st>>>(
+      dz, rows, out, ld_dz, b_cur, b_new, b_copy, lr, tag_slot, cur_version, version,
+      trace_src, trace_dst);
   PB_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------------ loss
-// One warp per row.  Softmax-CE: max-subtracted log-softmax, loss counts
-// targets > 0.5 (trainer.cpp:278-286); grad = (softmax - t)/denom
-// (:301-309).  MSE: sum (y-t)^2, grad 2(y-t)/denom (:273-276, :297-299).
-__global__ void loss_kernel(const float* __restrict__ y, int rows, int cols,
-                            int ld_y, const float* __restrict__ t, int ld_t,
-                            int loss, int act_last, float denom,
-                            __nv_bfloat16* __restrict__ dz, int ld_dz,
-                            float* __restrict__ row_loss) {
-  const int warps = blockDim.x / 32;
-  const int row = blockIdx.x * warps + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
+// One 256-thread block per row (rows are up to 4096 classes wide; the row
+// stays L1-resident across the three passes).  Softmax-CE: max-subtracted
+// log-softmax, loss counts targets > 0.5 (trainer.cpp:278-286); grad =
+// (softmax - t)/denom (:301-309).  MSE: sum (y-t)^2, grad 2(y-t)/denom
+// (:273-276, :297-299).  act' of a non-linear output layer is applied from y.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x / 32); ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(~0u, v, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = -INFINITY;
+  for (int i = 0; i < static_cast<int>(blockDim.x / 32); ++i) s = fmaxf(s, red[i]);
+  return s;
+}
+
+__global__ void __launch_bounds__(256)
+    loss_kernel(const float* __restrict__ y, int rows, int cols, int ld_y,
+                const float* __restrict__ t, int ld_t, int loss, int act_last,
+                float denom, __nv_bfloat16* __restrict__ dz, int ld_dz,
+                float* __restrict__ row_loss) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
   if (row >= rows) return;
   const float* yr = y + static_cast<size_t>(row) * ld_y;
   const float* tr = t + static_cast<size_t>(row) * ld_t;
   __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
   float acc = 0.f;
   if (loss == 0) {  // mse
-    for (int c = lane; c < cols; c += 32) {
-      const float d = yr[c] - tr[c];
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float yv = yr[c];
+      const float d = yv - tr[c];
       acc += d * d;
       float g = 2.f * d / denom;
-      if (act_last != kLinear) g *= act_grad_from_out(yr[c], act_last);
+      if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
       dr[c] = __float2bfloat16_rn(g);
     }
   } else {
     float mx = -INFINITY;
-    for (int c = lane; c < cols; c += 32) mx = fmaxf(mx, yr[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, yr[c]);
+    mx = block_max(mx, red);
     float se = 0.f;
-    for (int c = lane; c < cols; c += 32) se += expf(yr[c] - mx);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(~0u, se, o);
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) se += expf(yr[c] - mx);
+    se = block_sum(se, red);
     const float lse = logf(se);
-    for (int c = lane; c < cols; c += 32) {
-      const float z = yr[c] - mx;
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float yv = yr[c];
+      const float z = yv - mx;
       const float tc = tr[c];
       if (tc > 0.5f) acc += -(z - lse) * tc;
       float g = (expf(z) / se - tc) / denom;
-      if (act_last != kLinear) g *= act_grad_from_out(yr[c], act_last);
+      if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
       dr[c] = __float2bfloat16_rn(g);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
-  if (lane == 0) row_loss[row] = acc;
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) row_loss[row] = acc;
 }
 
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
                  float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss) {
-  const int warps = 8;
-  loss_kernel<<<(rows + warps - 1) / warps, warps * 32, 0, st>>>(
-      y, rows, cols, ld_y, targets, ld_t, loss, act_last, denom, dz, ld_dz,
-      row_loss);
+  if (rows <= 0) return;
+  const int threads = cols >= 256 ? 256 : (cols >= 128 ? 128 : 64);
+  loss_kernel<<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss, act_last,
+                                         denom, dz, ld_dz, row_loss);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -464,8 +464,91 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     push(z);
   }
 
-  std::map<std::tuple<int, int, int>, cudaEvent_t> fwd_done;  // (k, jj, s)
-  std::map<std::pair<int, int>, cudaEvent_t> bwd_done;         // (k, s)
+  // ---------------- program: coalesce forwards, order the task DAG
+  // A node is one backward task, or a run of consecutive forward tasks of one
+  // stage with the same mini-batch and the same pinned version (coalesced
+  // into one taller GEMM per layer: GEMM rows are independent, so the result
+  // is bit-identical to per-micro-batch launches; each micro-batch's version
+  // tag is still written to the device trace).
+  struct Node {
+    bool fwd;
+    int s, k, version, jj0, jj1;  // s 0-based; forward micro range [jj0, jj1]
+    int order;                     // position of the first member in issue order
+    std::vector<int> deps;         // node ids (same-stage predecessor + cross-stage)
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<Node> nodes;
+  const int merge = c.fwd_merge > 0 ? c.fwd_merge : U;
+  {
+    std::vector<int> open(W, -1), last_on_stage(W, -1);
+    std::map<std::tuple<int, int, int>, int> fwd_node;  // (k, jj, s) -> node
+    std::map<std::pair<int, int>, int> bwd_node;         // (k, s) -> node
+    int order = 0;
+    for (const Impl::Task& tk : I.tasks) {
+      const int s = tk.s - 1;
+      ++order;
+      if (tk.fwd) {
+        const int o = open[s];
+        if (o >= 0 && nodes[o].k == tk.k && nodes[o].version == tk.version &&
+            nodes[o].jj1 + 1 == tk.jj && nodes[o].jj1 - nodes[o].jj0 + 1 < merge) {
+          nodes[o].jj1 = tk.jj;
+          fwd_node[{tk.k, tk.jj, s}] = o;
+          continue;
+        }
+        Node n{true, s, tk.k, tk.version, tk.jj, tk.jj, order, {}};
+        if (last_on_stage[s] >= 0) n.deps.push_back(last_on_stage[s]);
+        nodes.push_back(n);
+        const int id = static_cast<int>(nodes.size()) - 1;
+        open[s] = last_on_stage[s] = id;
+        fwd_node[{tk.k, tk.jj, s}] = id;
+      } else {
+        open[s] = -1;
+        Node n{false, s, tk.k, tk.version, 0, 0, order, {}};
+        if (last_on_stage[s] >= 0) n.deps.push_back(last_on_stage[s]);
+        nodes.push_back(n);
+        const int id = static_cast<int>(nodes.size()) - 1;
+        last_on_stage[s] = id;
+        bwd_node[{tk.k, s}] = id;
+      }
+    }
+    for (Node& n : nodes) {
+      if (n.fwd && n.s > 0)
+        for (int jj = n.jj0; jj <= n.jj1; ++jj) n.deps.push_back(fwd_node.at({n.k, jj, n.s - 1}));
+      if (!n.fwd && n.s < last_s) n.deps.push_back(bwd_node.at({n.k, n.s + 1}));
+      std::sort(n.deps.begin(), n.deps.end());
+      n.deps.erase(std::unique(n.deps.begin(), n.deps.end()), n.deps.end());
+    }
+  }
+  // Kahn's algorithm, earliest original position first.
+  std::vector<int> topo;
+  {
+    const int n = static_cast<int>(nodes.size());
+    std::vector<int> indeg(n, 0);
+    std::vector<std::vector<int>> succ(n);
+    for (int i = 0; i < n; ++i)
+      for (int d : nodes[i].deps) {
+        ++indeg[i];
+        succ[d].push_back(i);
+      }
+    std::vector<int> ready;
+    for (int i = 0; i < n; ++i)
+      if (indeg[i] == 0) ready.push_back(i);
+    auto later = [&](int x, int y) { return nodes[x].order > nodes[y].order; };
+    std::make_heap(ready.begin(), ready.end(), later);
+    while (!ready.empty()) {
+      std::pop_heap(ready.begin(), ready.end(), later);
+      const int i = ready.back();
+      ready.pop_back();
+      topo.push_back(i);
+      for (int j : succ[i])
+        if (--indeg[j] == 0) {
+          ready.push_back(j);
+          std::push_heap(ready.begin(), ready.end(), later);
+        }
+    }
+    if (static_cast<int>(topo.size()) != n)
+      throw std::logic_error("coalesced task graph has a cycle");
+  }
 
   auto stage_input = [&](int s, int k, int* row_off) -> Mat16 {
     // Activation entering stage s (0-based) for mini k: data rows or the
@@ -480,20 +563,28 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     return Mat16{pv.acts[pv.mini_act[k]].out16.back(), c.B, pl.out, pl.ld_out};
   };
 
-  for (const Impl::Task& tk : I.tasks) {
-    const int s = tk.s - 1;
+  for (int id : topo) {
+    Node& node = nodes[id];
+    const int s = node.s;
     Impl::Stage& st = I.stages[s];
+    Impl::Task tk;
+    tk.fwd = node.fwd;
+    tk.k = node.k;
+    tk.s = s + 1;
+    tk.version = node.version;
     const int a = st.mini_act[tk.k];
     Impl::ActSlot& as = st.acts[a];
-    if (tk.fwd) {
-      if (s > 0) {
+    for (int d : node.deps)
+      if (nodes[d].s != s) {  // cross-stage edge (same-stage order is the stream)
         Impl::Op w{OK::wait};
         w.stream = s;
-        w.ev = fwd_done.at({tk.k, tk.jj, s - 1});
+        w.ev = nodes[d].done;
         push(w);
       }
+    if (node.fwd) {
       const Impl::PoolSlot& ps = st.pool[st.version_colour[tk.version]];
-      const int r0 = tk.jj * I.Rm;
+      const int r0 = node.jj0 * I.Rm;
+      const int rows = (node.jj1 - node.jj0 + 1) * I.Rm;
       for (int l = 0; l < st.L; ++l) {
         const auto& d = st.layers[l];
         int in_off = 0;
@@ -507,136 +598,127 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
         Impl::Op o{OK::fwd};
         o.stream = s;
-        o.g = plan_fwd(x, in_off + r0, I.Rm, w, ps.b32[l], d.act,
+        o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
                        logits ? as.out32 : nullptr, I.n_out, r0);
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
-          o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + tk.jj) * W + s;
+          o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
+          o.g.ep.tag_count = node.jj1 - node.jj0 + 1;
+          o.g.ep.tag_stride = W;
         }
         push(o);
         ++kernels_per_epoch_;
       }
-      Impl::Op r{OK::record};
-      r.stream = s;
-      r.ev = I.new_event();
-      fwd_done[{tk.k, tk.jj, s}] = r.ev;
-      push(r);
-      continue;
-    }
-
-    // ---------------- backward of mini k on stage s
-    if (s < last_s) {
-      Impl::Op w{OK::wait};
-      w.stream = s;
-      w.ev = bwd_done.at({tk.k, s + 1});
-      push(w);
     } else {
-      // fused loss + gradient over the stacked mini-batch (trainer.cpp:461-473)
-      Impl::Op o{OK::loss};
-      o.stream = s;
-      o.y = as.out32;
-      o.rows = c.B;
-      o.cols = I.n_out;
-      o.ld = I.n_out;
-      o.t = I.y32 + static_cast<size_t>(tk.k - 1) * c.B * I.n_out;
-      o.ld_t = I.n_out;
-      o.loss = c.loss;
-      o.act_last = st.layers.back().act;
-      o.denom = static_cast<float>(c.B);
-      o.dz_out = as.dzin;
-      o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
-      o.ld_dz = st.layers.back().ld_out;
-      push(o);
-      ++kernels_per_epoch_;
-    }
-    const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
-    Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
-    const int cur = (tk.k - 1) % 2, nxt = tk.k % 2;
-    for (int l = st.L - 1; l >= 0; --l) {
-      const auto& d = st.layers[l];
-      __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
-      int x_off = 0;
-      Mat16 x;
-      if (l == 0)
-        x = stage_input(s, tk.k, &x_off);
-      else
-        x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
-      Mat16 mdz{dz, c.B, d.out, d.ld_out};
-      // dgrad: delta for the layer below (or the previous stage)
-      if (l > 0 || s > 0) {
-        __nv_bfloat16* dst;
-        int act_prev;
-        if (l > 0) {
-          dst = st.scratch_dz[l - 1];
-          act_prev = st.layers[l - 1].act;
-        } else {
-          const Impl::Stage& pv = I.stages[s - 1];
-          dst = pv.acts[pv.mini_act[tk.k]].dzin;
-          act_prev = pv.layers.back().act;
-        }
-        // act' of the layer below, recovered from the activation it produced
-        // (= this layer's input x).
-        const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld;
-        Impl::Op o{OK::dgrad};
+      // ---------------- backward of mini k on stage s
+      if (s == last_s) {
+        // fused loss + gradient over the stacked mini-batch (trainer.cpp:461-473)
+        Impl::Op o{OK::loss};
         o.stream = s;
-        o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
-                         dst, d.ld_in);
-        push(o);
-        ++kernels_per_epoch_;
-      }
-      // wgrad + SGD into the new version (trainer.cpp:244-249, :484-488)
-      {
-        Impl::Op o{OK::wgrad};
-        o.stream = s;
-        o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
-                             d.ld_in, static_cast<float>(c.lr));
-        push(o);
-        ++kernels_per_epoch_;
-      }
-      // bias gradient + SGD; the last one stamps the commit
-      {
-        Impl::Op o{OK::bias};
-        o.stream = s;
-        o.dz = dz;
+        o.y = as.out32;
         o.rows = c.B;
-        o.cols = d.out;
-        o.ld = d.ld_out;
-        o.b_cur = d.b32[cur];
-        o.b_new = d.b32[nxt];
-        o.b_copy = next.b32[l];
-        o.lr = static_cast<float>(c.lr);
-        if (l == 0) {
-          o.trace_src = prop.tag;
-          o.trace_dst = I.bwd_trace + static_cast<size_t>(tk.k - 1) * W + s;
-          o.tag_slot = next.tag;
-          o.cur_version = st.cur_version;
-          o.version = tk.k;
-        }
+        o.cols = I.n_out;
+        o.ld = I.n_out;
+        o.t = I.y32 + static_cast<size_t>(tk.k - 1) * c.B * I.n_out;
+        o.ld_t = I.n_out;
+        o.loss = c.loss;
+        o.act_last = st.layers.back().act;
+        o.denom = static_cast<float>(c.B);
+        o.dz_out = as.dzin;
+        o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
+        o.ld_dz = st.layers.back().ld_out;
         push(o);
         ++kernels_per_epoch_;
       }
-    }
-    if (c.snapshots) {
-      for (int l = 0, po = 0; l < st.L; ++l) {
+      const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
+      Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
+      const int cur = (tk.k - 1) % 2, nxt = tk.k % 2;
+      for (int l = st.L - 1; l >= 0; --l) {
         const auto& d = st.layers[l];
-        Impl::Op o{OK::snapshot};
-        o.stream = s;
-        o.dst = I.snaps[s][tk.k] + po;
-        o.src = d.w32[nxt];
-        o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
-        push(o);
-        o.dst = I.snaps[s][tk.k] + po + static_cast<size_t>(d.in) * d.out;
-        o.src = d.b32[nxt];
-        o.bytes = sizeof(float) * d.out;
-        push(o);
-        po += d.in * d.out + d.out;
+        __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
+        int x_off = 0;
+        Mat16 x;
+        if (l == 0)
+          x = stage_input(s, tk.k, &x_off);
+        else
+          x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
+        Mat16 mdz{dz, c.B, d.out, d.ld_out};
+        // dgrad: delta for the layer below (or the previous stage)
+        if (l > 0 || s > 0) {
+          __nv_bfloat16* dst;
+          int act_prev;
+          if (l > 0) {
+            dst = st.scratch_dz[l - 1];
+            act_prev = st.layers[l - 1].act;
+          } else {
+            const Impl::Stage& pv = I.stages[s - 1];
+            dst = pv.acts[pv.mini_act[tk.k]].dzin;
+            act_prev = pv.layers.back().act;
+          }
+          // act' of the layer below, recovered from the activation it produced
+          // (= this layer's input x).
+          const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld;
+          Impl::Op o{OK::dgrad};
+          o.stream = s;
+          o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
+                           dst, d.ld_in);
+          push(o);
+          ++kernels_per_epoch_;
+        }
+        // wgrad + SGD into the new version (trainer.cpp:244-249, :484-488)
+        {
+          Impl::Op o{OK::wgrad};
+          o.stream = s;
+          o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
+                               d.ld_in, static_cast<float>(c.lr));
+          push(o);
+          ++kernels_per_epoch_;
+        }
+        // bias gradient + SGD; the last one stamps the commit
+        {
+          Impl::Op o{OK::bias};
+          o.stream = s;
+          o.dz = dz;
+          o.rows = c.B;
+          o.cols = d.out;
+          o.ld = d.ld_out;
+          o.b_cur = d.b32[cur];
+          o.b_new = d.b32[nxt];
+          o.b_copy = next.b32[l];
+          o.lr = static_cast<float>(c.lr);
+          if (l == 0) {
+            o.trace_src = prop.tag;
+            o.trace_dst = I.bwd_trace + static_cast<size_t>(tk.k - 1) * W + s;
+            o.tag_slot = next.tag;
+            o.cur_version = st.cur_version;
+            o.version = tk.k;
+          }
+          push(o);
+          ++kernels_per_epoch_;
+        }
+      }
+      if (c.snapshots) {
+        for (int l = 0, po = 0; l < st.L; ++l) {
+          const auto& d = st.layers[l];
+          Impl::Op o{OK::snapshot};
+          o.stream = s;
+          o.dst = I.snaps[s][tk.k] + po;
+          o.src = d.w32[nxt];
+          o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
+          push(o);
+          o.dst = I.snaps[s][tk.k] + po + static_cast<size_t>(d.in) * d.out;
+          o.src = d.b32[nxt];
+          o.bytes = sizeof(float) * d.out;
+          push(o);
+          po += d.in * d.out + d.out;
+        }
       }
     }
     Impl::Op r{OK::record};
     r.stream = s;
     r.ev = I.new_event();
-    bwd_done[{tk.k, s}] = r.ev;
+    node.done = r.ev;
     push(r);
   }
 }

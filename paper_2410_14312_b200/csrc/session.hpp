@@ -47,6 +47,8 @@ struct SessionConfig {
   // stage range owned by this process (multi-GPU: one process per GPU);
   // [stage_lo, stage_hi] 1-based inclusive.  Default: all stages.
   int stage_lo = 1, stage_hi = 0;
+  // max micro-batches per coalesced forward launch (0 = N: a whole run)
+  int fwd_merge = 0;
 };
 
 struct EpochResult {

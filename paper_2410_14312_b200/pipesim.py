@@ -573,7 +573,7 @@ class Session:
 
     def __init__(self, net: NetworkSpec, workers, micro_batches, mini_batch_size,
                  mini_batches, learning_rate, mode="timeprest", device=0, use_graph=True,
-                 snapshots=False):
+                 snapshots=False, fwd_merge=0):
         if mode not in TRAIN_MODES:
             raise DomainError(f"unknown training mode: {mode}", "mode")
         self.net = net
@@ -582,7 +582,7 @@ class Session:
         self.units = micro_batches if mode == "timeprest" else 1
         cfg = pb_train_config(workers, micro_batches, mini_batch_size, mini_batches,
                               float(learning_rate), TRAIN_MODES.index(mode), device,
-                              int(use_graph), int(snapshots))
+                              int(use_graph), int(snapshots), int(fwd_merge))
         spec = net._c()
         h = C.c_void_p()
         N.check(_L().pb_session_create(C.byref(spec), C.byref(cfg), C.byref(h)))

@@ -228,3 +228,24 @@ def test_session_resident_epochs_and_labels():
     for a, b in zip(outs[0], outs[1]):
         np.testing.assert_array_equal(a, b)
     assert not np.array_equal(outs[0][0], outs[0][1])  # epoch 2 starts from trained weights
+
+
+@pytest.mark.parametrize("mode", ["timeprest", "pipedream"])
+def test_forward_coalescing_is_bit_identical(mode):
+    """Coalesced forwards (one GEMM over consecutive micro-batches with the same
+    pinned version) must reproduce per-micro-batch launches bit for bit."""
+    net = P.NetworkSpec([256] * 9, ["relu"] * 7 + ["linear"], "softmax_cross_entropy")
+    p0 = P.init_network_params(net, 1)
+    x, lab = P.make_classification_task(6 * 512, 256, 256, seed=7, as_labels=True,
+                                        dtype=np.float32)
+    res = []
+    for merge in (1, 0, 3):
+        s = P.Session(net, 4, 8, 512, 6, 0.05, mode, fwd_merge=merge)
+        s.load_params(p0)
+        s.upload(x, lab, y_labels=True)
+        r = s.run_epoch()
+        res.append((r["mini_loss"], r["dev_fwd"], s.read_params()))
+        s.close()
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            np.testing.assert_array_equal(a, b)
