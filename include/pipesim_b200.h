@@ -261,6 +261,33 @@ int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
 int pb_session_snapshot(pb_session* s, int stage, int version, double* out,
                         int64_t n);
 
+/* Committed weights of `version` on `stage` after an epoch: versions M and
+ * M-1 from the fp32 masters, any version from snapshots (if enabled). */
+int pb_session_read_version(pb_session* s, int stage, int version, double* out,
+                            int64_t n);
+
+/* ------------------------------------------------------------ multi-GPU
+ * One process per GPU; the W stages are split into contiguous ranges (rank r
+ * owns stages [r*W/world, (r+1)*W/world)).  Activations (stage s -> s+1) and
+ * deltas (s+1 -> s) cross GPU boundaries point to point over NVLink (NCCL
+ * send/recv, one 2-rank communicator per boundary and direction). */
+
+/* Writes one NCCL unique id (128 bytes).  Rank 0 makes 2*(world-1) of them
+ * and shares them (e.g. torch.distributed broadcast). */
+int pb_nccl_unique_id(uint8_t* out128);
+
+/* pb_session_create for one rank of a world-size pipeline. */
+int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg,
+                           int rank, int world, const uint8_t* nccl_ids,
+                           size_t ids_bytes, pb_session** out);
+
+/* The point-to-point transfers one rank's program issues, in order, without
+ * touching a GPU: kinds[i] 1 = send / 0 = recv, dirs[i] 0 = activation /
+ * 1 = delta, peers[i], bytes[i].  *n = count (call with cap 0 to size). */
+int pb_plan_transfers(const pb_net_spec* net, const pb_train_config* cfg,
+                      int rank, int world, int* n, int* kinds, int* dirs,
+                      int* peers, int64_t* bytes, int cap);
+
 /* Synthetic classification data: x ~ U[0,1) from
  * mt19937_64(seed) row-major via (rng()>>11)*2^-53, then labels rng() % C.
  * Either of x64 / x32 / labels may be NULL. */

@@ -42,6 +42,12 @@ def signatures():
         "pb_session_run_epoch": (i, [p, P(pb_epoch_out)]),
         "pb_session_train_epoch": (i, [p, p, i, p, i, P(pb_epoch_out)]),
         "pb_session_snapshot": (i, [p, i, i, P(C.c_double), i64]),
+        "pb_session_read_version": (i, [p, i, i, P(C.c_double), i64]),
+        "pb_nccl_unique_id": (i, [C.c_char_p]),
+        "pb_session_create_dist": (i, [P(pb_net_spec), P(pb_train_config), i, i, C.c_char_p,
+                                       C.c_size_t, P(p)]),
+        "pb_plan_transfers": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i), P(i), P(i),
+                                  P(i), P(i64), i]),
         "pb_make_classification_task": (i, [i, i, i, u64, P(C.c_double), P(C.c_float),
                                             P(C.c_int)]),
     }

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "nccl_p2p.hpp"
 #include "session.hpp"
 #include "status.hpp"
 
@@ -60,10 +61,9 @@ void fill(const pb::EpochResult& r, const pb::Session& s, pb_epoch_out* out) {
 
 extern "C" {
 
-int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
-                      pb_session** out) {
-  PB_GUARD_BEGIN
-  if (!net || !cfg || !out) throw std::invalid_argument("null argument");
+namespace {
+pb::SessionConfig make_config(const pb_net_spec* net, const pb_train_config* cfg) {
+  if (!net || !cfg) throw std::invalid_argument("null argument");
   if (cfg->micro_batches < 1)
     throw pipesim::domain_error("micro_batches", "micro-batch count must be >= 1");
   if (cfg->mini_batch_size < 1 || cfg->mini_batches < 1)
@@ -83,6 +83,24 @@ int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
   c.snapshots = cfg->snapshots != 0;
   c.fwd_merge = cfg->fwd_merge;
   if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
+  return c;
+}
+}  // namespace
+
+int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
+                      pb_session** out) {
+  return pb_session_create_dist(net, cfg, 0, 1, nullptr, 0, out);
+}
+
+int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg, int rank,
+                           int world, const uint8_t* nccl_ids, size_t ids_bytes,
+                           pb_session** out) {
+  PB_GUARD_BEGIN
+  if (!out) throw std::invalid_argument("null argument");
+  pb::SessionConfig c = make_config(net, cfg);
+  c.rank = rank;
+  c.world = world;
+  if (nccl_ids && ids_bytes) c.nccl_ids.assign(nccl_ids, nccl_ids + ids_bytes);
   auto* s = new pb_session;
   try {
     s->impl = std::make_unique<pb::Session>(c);
@@ -91,6 +109,33 @@ int pb_session_create(const pb_net_spec* net, const pb_train_config* cfg,
     throw;
   }
   *out = s;
+  PB_GUARD_END
+}
+
+int pb_nccl_unique_id(uint8_t* out128) {
+  PB_GUARD_BEGIN
+  pb::P2P::unique_id(out128);
+  PB_GUARD_END
+}
+
+int pb_plan_transfers(const pb_net_spec* net, const pb_train_config* cfg, int rank, int world,
+                      int* n, int* kinds, int* dirs, int* peers, int64_t* bytes, int cap) {
+  PB_GUARD_BEGIN
+  pb::SessionConfig c = make_config(net, cfg);
+  c.rank = rank;
+  c.world = world;
+  c.plan_only = true;
+  c.use_graph = false;
+  c.snapshots = false;
+  pb::Session sess(c);
+  const std::vector<pb::Transfer> t = sess.transfers();
+  *n = static_cast<int>(t.size());
+  for (int i = 0; i < *n && i < cap; ++i) {
+    if (kinds) kinds[i] = t[i].send ? 1 : 0;
+    if (dirs) dirs[i] = t[i].dir;
+    if (peers) peers[i] = t[i].peer;
+    if (bytes) bytes[i] = t[i].bytes;
+  }
   PB_GUARD_END
 }
 
@@ -175,6 +220,24 @@ int pb_session_snapshot(pb_session* s, int stage, int version, double* out, int6
   if (n != x.stage_param_count(stage)) throw pb::capacity_error("stage parameter count mismatch");
   const float* p = x.snapshot(stage, version);
   for (int64_t i = 0; i < n; ++i) out[i] = p[i];
+  PB_GUARD_END
+}
+
+int pb_session_read_version(pb_session* s, int stage, int version, double* out,
+                            int64_t n) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  if (n != x.stage_param_count(stage)) throw pb::capacity_error("stage parameter count mismatch");
+  const int M = x.config().M;
+  if (x.has_snapshots()) {
+    const float* p = x.snapshot(stage, version);
+    for (int64_t i = 0; i < n; ++i) out[i] = p[i];
+  } else if (version == M || version == M - 1) {
+    x.read_stage_master(stage, version & 1, out);
+  } else {
+    throw pipesim::structural_error("stage " + std::to_string(stage) + " does not hold version " +
+                                    std::to_string(version) + " (no snapshots)");
+  }
   PB_GUARD_END
 }
 

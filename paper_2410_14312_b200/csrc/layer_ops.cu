@@ -250,18 +250,32 @@ __global__ void __launch_bounds__(256)
   const int c0 = blockIdx.x * kBiasCols + cx * 8;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const bool vec = (ld_dz % 8) == 0 && c0 + 8 <= out;
-  for (int r = ry; r < rows; r += kBiasRowGroups) {
-    const __nv_bfloat16* p = dz + static_cast<size_t>(r) * ld_dz + c0;
-    if (vec) {
-      const uint4 q = *reinterpret_cast<const uint4*>(p);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+  if (vec) {
+    // 8 independent 16-byte row loads in flight per thread, then accumulate
+    // in row order (fixed order: deterministic).
+    constexpr int kU = 8;
+    for (int r0 = ry; r0 < rows; r0 += kU * kBiasRowGroups) {
+      uint4 q[kU];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(h[k]);
-        acc[2 * k] += f.x;
-        acc[2 * k + 1] += f.y;
+      for (int u = 0; u < kU; ++u) {
+        const int r = r0 + u * kBiasRowGroups;
+        q[u] = r < rows ? *reinterpret_cast<const uint4*>(dz + static_cast<size_t>(r) * ld_dz + c0)
+                        : make_uint4(0, 0, 0, 0);
       }
-    } else {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h[k]);
+          acc[2 * k] += f.x;
+          acc[2 * k + 1] += f.y;
+        }
+      }
+    }
+  } else {
+    for (int r = ry; r < rows; r += kBiasRowGroups) {
+      const __nv_bfloat16* p = dz + static_cast<size_t>(r) * ld_dz + c0;
       for (int k = 0; k < 8 && c0 + k < out; ++k) acc[k] += __bfloat162float(p[k]);
     }
   }

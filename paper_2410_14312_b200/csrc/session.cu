@@ -9,6 +9,7 @@
 #include <string>
 #include <tuple>
 
+#include "nccl_p2p.hpp"
 #include "status.hpp"
 
 namespace pb {
@@ -70,6 +71,11 @@ struct Session::Impl {
     std::vector<__nv_bfloat16*> out16;  // per layer (null for the logits layer)
     float* out32 = nullptr;              // last stage: logits / final output
     __nv_bfloat16* dzin = nullptr;       // delta into this stage's top layer
+    // cross-GPU boundary buffers (only on a rank's first stage when the
+    // upstream stage lives on another GPU): received input activation and
+    // the outgoing delta for the upstream stage.
+    __nv_bfloat16* in16 = nullptr;
+    __nv_bfloat16* dzsend = nullptr;
   };
   struct Stage {
     int id = 0, first_layer = 0, L = 0;
@@ -90,7 +96,10 @@ struct Session::Impl {
     int version = 0;  // fwd: pinned; bwd: propagation version
   };
 
-  enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot };
+  enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
+                      send, recv };
+  // streams beyond the stage streams (Op::stream values)
+  static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   struct Op {
     OpKind kind;
     int stream = 0;  // stage index (0-based); -1 = origin stream
@@ -120,6 +129,8 @@ struct Session::Impl {
     const void* src = nullptr;
     size_t bytes = 0;
     int value = 0;
+    // send / recv
+    int peer = 0, dir = 0;
   };
 
   const SessionConfig& cfg;
@@ -151,7 +162,17 @@ struct Session::Impl {
   // snapshots: [W][M+1] host pinned fp32
   std::vector<std::vector<float*>> snaps;
   int kernels = 0;
-  int W_lo = 1, W_hi = 0;
+  int W_lo = 1, W_hi = 0;  // local stage range (1-based, inclusive)
+  int rank = 0, world = 1;
+  std::vector<int> owner;  // [stage 0-based] -> rank
+  std::unique_ptr<P2P> p2p;
+  cudaStream_t comm[4] = {nullptr, nullptr, nullptr, nullptr};  // fwd send/recv, bwd send/recv
+  bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
+  cudaStream_t stream_of(int idx) const {
+    if (idx >= 0) return stages[idx].stream;
+    if (idx == -1) return origin;
+    return comm[-idx - 2];
+  }
 
   explicit Impl(const SessionConfig& c) : cfg(c) {}
 
@@ -168,20 +189,26 @@ struct Session::Impl {
   ~Impl() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (!plan_only)
+      for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (t0) cudaEventDestroy(t0);
     if (t1) cudaEventDestroy(t1);
     for (Stage& s : stages)
       if (s.stream) cudaStreamDestroy(s.stream);
     if (origin) cudaStreamDestroy(origin);
+    for (cudaStream_t c : comm)
+      if (c) cudaStreamDestroy(c);
     for (auto& v : snaps)
       for (float* p : v)
         if (p) cudaFreeHost(p);
-    if (arena) cudaFree(arena);
+    if (arena && !plan_only) cudaFree(arena);
   }
 
+  bool plan_only = false;
+  uintptr_t fake_events = 0x10;
   cudaEvent_t new_event() {
     cudaEvent_t e;
+    if (plan_only) return reinterpret_cast<cudaEvent_t>(fake_events += 0x10);
     PB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     events.push_back(e);
     return e;
@@ -199,19 +226,40 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                                 "mini-batch size " + std::to_string(c.B) +
                                     " is not divisible by micro-batch count " +
                                     std::to_string(c.N));
-  PB_CUDA(cudaSetDevice(c.device));
-  init_gemm_attributes();
+  if (!c.plan_only) {
+    PB_CUDA(cudaSetDevice(c.device));
+    init_gemm_attributes();
+  }
   impl_ = std::make_unique<Impl>(cfg_);
   Impl& I = *impl_;
+  I.plan_only = c.plan_only;
   I.W = c.W;
   I.N = c.N;
   I.B = c.B;
   I.M = c.M;
   I.U = units();
   I.Rm = c.B / I.U;
+  const int W = c.W, M = c.M, U = I.U;
+  I.rank = c.rank;
+  I.world = c.world;
+  if (c.world < 1 || c.rank < 0 || c.rank >= c.world || c.world > W)
+    throw std::invalid_argument("bad rank/world for the stage count");
+  I.owner.assign(W, 0);
+  for (int s = 0; s < W; ++s) I.owner[s] = static_cast<int>((static_cast<long>(s) * c.world) / W);
+  if (c.world > 1) {  // even contiguous split of the W stages over the ranks
+    c.stage_lo = W + 1;
+    c.stage_hi = 0;
+    for (int s = 0; s < W; ++s)
+      if (I.owner[s] == c.rank) {
+        c.stage_lo = std::min(c.stage_lo, s + 1);
+        c.stage_hi = std::max(c.stage_hi, s + 1);
+      }
+  } else {
+    c.stage_lo = 1;
+    c.stage_hi = W;
+  }
   I.W_lo = c.stage_lo;
   I.W_hi = c.stage_hi;
-  const int W = c.W, M = c.M, U = I.U;
 
   // ---------------- network partition (trainer.cpp:104-135)
   pipesim::network_spec net;
@@ -312,6 +360,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                             rt.per_stage[s][v].freed_at_slot};
   }
 
+  // A stage fed over the network receives its input while the upstream stage
+  // produces it, so its activation slot is held from the upstream forward.
+  for (int s0 = 1; s0 < W; ++s0)
+    if (I.owner[s0 - 1] != I.owner[s0])
+      for (int k = 0; k < M; ++k)
+        act_iv[s0][k].first = std::min(act_iv[s0][k].first, act_iv[s0 - 1][k].first);
+
   // ---------------- colouring: version pool and activation slots
   I.stages.resize(W);
   std::vector<int> pool_n(W), act_n(W);
@@ -345,12 +400,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       d.ld_out = ld8(d.out);
       st.layers.push_back(d);
       st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
+      if (!I.local(s)) continue;
       need += 2 * (bytes_of(static_cast<size_t>(d.in) * d.out, 4) + bytes_of(d.out, 4));
       need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2) + bytes_of(d.out, 4));
       need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
       if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
     }
     off += st.param_count;
+    if (!I.local(s)) continue;
+    if (s > 0 && !I.local(s - 1))  // boundary buffers: received input + outgoing delta
+      need += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2);
     need += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
     need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2);
     if (s == W - 1) need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
@@ -362,13 +421,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   need += bytes_of(static_cast<size_t>(M) * U * W, 4) + bytes_of(static_cast<size_t>(M) * W, 4);
   need += 64 * kAlign;
 
-  PB_CUDA(cudaMalloc(&I.arena, need));
-  PB_CUDA(cudaMemset(I.arena, 0, need));
+  if (c.plan_only) {
+    I.arena = reinterpret_cast<char*>(uintptr_t{1} << 40);  // addresses only, never touched
+  } else {
+    PB_CUDA(cudaMalloc(&I.arena, need));
+    PB_CUDA(cudaMemset(I.arena, 0, need));
+  }
   I.arena_cap = need;
   arena_bytes_ = static_cast<int64_t>(need);
 
   for (int s = 0; s < W; ++s) {
     Impl::Stage& st = I.stages[s];
+    if (!I.local(s)) continue;
     for (auto& d : st.layers)
       for (int p = 0; p < 2; ++p) {
         d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out);
@@ -393,6 +457,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       }
       if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out);
       as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().ld_out);
+      if (s > 0 && !I.local(s - 1)) {
+        as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in);
+        as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in);
+      }
     }
     for (int l = 0; l + 1 < st.L; ++l)
       st.scratch_dz.push_back(
@@ -405,15 +473,22 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   I.fwd_trace = I.carve<int>(static_cast<size_t>(M) * U * W);
   I.bwd_trace = I.carve<int>(static_cast<size_t>(M) * W);
 
+  if (!c.plan_only) {
   PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
-  for (auto& st : I.stages) PB_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+  for (int s = 0; s < W; ++s)
+    if (I.local(s)) PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].stream, cudaStreamNonBlocking));
+  if (c.world > 1) {
+    for (cudaStream_t& cs : I.comm) PB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    I.p2p = std::make_unique<P2P>(c.rank, c.world, c.nccl_ids.data(), c.nccl_ids.size());
+  }
   PB_CUDA(cudaEventCreate(&I.t0));
   PB_CUDA(cudaEventCreate(&I.t1));
+  }  // !plan_only
 
-  if (c.snapshots) {
+  if (c.snapshots && !c.plan_only) {
     I.snaps.assign(W, std::vector<float*>(M + 1, nullptr));
     for (int s = 0; s < W; ++s)
-      for (int v = 0; v <= M; ++v)
+      for (int v = 0; v <= M && I.local(s); ++v)
         PB_CUDA(cudaMallocHost(&I.snaps[s][v], sizeof(float) * std::max<int64_t>(1, I.stages[s].param_count)));
   }
 
@@ -426,6 +501,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   // epoch's final version.  Masters ping-pong by parity, pool colours are
   // fixed by the plan, so copy when they differ.
   for (int s = 0; s < W; ++s) {
+    if (!I.local(s)) continue;
     Impl::Stage& st = I.stages[s];
     const int cM = st.version_colour[M], c0 = st.version_colour[0];
     for (int l = 0; l < st.L; ++l) {
@@ -557,15 +633,40 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       *row_off = (k - 1) * c.B;
       return Mat16{I.x16, M * c.B, c.widths.front(), I.ld_x};
     }
-    const Impl::Stage& pv = I.stages[s - 1];
     *row_off = 0;
+    if (!I.local(s - 1)) {  // received over the network into this stage's slot
+      const Impl::Stage& me = I.stages[s];
+      const auto& fl = me.layers.front();
+      return Mat16{me.acts[me.mini_act[k]].in16, c.B, fl.in, fl.ld_in};
+    }
+    const Impl::Stage& pv = I.stages[s - 1];
     const auto& pl = pv.layers.back();
     return Mat16{pv.acts[pv.mini_act[k]].out16.back(), c.B, pl.out, pl.ld_out};
   };
 
+  // Cross-GPU plumbing.  Previous occupant of each activation slot (slot reuse
+  // guard for receives), first local forward node of each (k, s), and the
+  // receive events (posted lazily, in the sender's order).
+  std::vector<std::vector<int>> prev_occ(W, std::vector<int>(M + 1, 0));
+  for (int s0 = 0; s0 < W; ++s0) {
+    std::map<int, int> last;
+    for (int k = 1; k <= M; ++k) {
+      auto it = last.find(I.stages[s0].mini_act[k]);
+      prev_occ[s0][k] = it == last.end() ? 0 : it->second;
+      last[I.stages[s0].mini_act[k]] = k;
+    }
+  }
+  std::map<std::pair<int, int>, int> bwd_id, first_fwd_id;  // (k, s0) -> node
+  for (int i = 0; i < static_cast<int>(nodes.size()); ++i) {
+    if (!nodes[i].fwd) bwd_id[{nodes[i].k, nodes[i].s}] = i;
+    else if (!first_fwd_id.count({nodes[i].k, nodes[i].s})) first_fwd_id[{nodes[i].k, nodes[i].s}] = i;
+  }
+  std::map<int, cudaEvent_t> fwd_recv_done;  // upstream node id -> event
+
   for (int id : topo) {
     Node& node = nodes[id];
     const int s = node.s;
+    if (!I.local(s)) continue;  // another GPU's stage
     Impl::Stage& st = I.stages[s];
     Impl::Task tk;
     tk.fwd = node.fwd;
@@ -574,13 +675,57 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     tk.version = node.version;
     const int a = st.mini_act[tk.k];
     Impl::ActSlot& as = st.acts[a];
-    for (int d : node.deps)
-      if (nodes[d].s != s) {  // cross-stage edge (same-stage order is the stream)
-        Impl::Op w{OK::wait};
-        w.stream = s;
-        w.ev = nodes[d].done;
-        push(w);
+    auto wait_on = [&](int stream, cudaEvent_t ev) {
+      Impl::Op w{OK::wait};
+      w.stream = stream;
+      w.ev = ev;
+      push(w);
+    };
+    auto record_on = [&](int stream) {
+      Impl::Op r{OK::record};
+      r.stream = stream;
+      r.ev = I.new_event();
+      push(r);
+      return r.ev;
+    };
+    for (int d : node.deps) {
+      if (nodes[d].s == s) continue;  // same-stage order is the stream order
+      if (I.local(nodes[d].s)) {
+        wait_on(s, nodes[d].done);
+        continue;
       }
+      const Node& up = nodes[d];
+      if (node.fwd) {
+        // activation rows of the remote upstream group -> this stage's slot
+        auto it = fwd_recv_done.find(d);
+        if (it == fwd_recv_done.end()) {
+          const int pk = prev_occ[s][tk.k];
+          if (pk > 0) wait_on(Impl::kFwdRecv, nodes[bwd_id.at({pk, s})].done);
+          const auto& fl = st.layers.front();
+          Impl::Op rv{OK::recv};
+          rv.stream = Impl::kFwdRecv;
+          rv.dst = as.in16 + static_cast<size_t>(up.jj0) * I.Rm * fl.ld_in;
+          rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ld_in * 2;
+          rv.peer = I.owner[up.s];
+          rv.dir = 0;
+          push(rv);
+          it = fwd_recv_done.emplace(d, record_on(Impl::kFwdRecv)).first;
+        }
+        wait_on(s, it->second);
+      } else {
+        // delta of the remote downstream stage -> this slot's dzin; the slot
+        // belongs to mini k since its first forward here
+        wait_on(Impl::kBwdRecv, nodes[first_fwd_id.at({tk.k, s})].done);
+        Impl::Op rv{OK::recv};
+        rv.stream = Impl::kBwdRecv;
+        rv.dst = as.dzin;
+        rv.bytes = static_cast<size_t>(c.B) * st.layers.back().ld_out * 2;
+        rv.peer = I.owner[up.s];
+        rv.dir = 1;
+        push(rv);
+        wait_on(s, record_on(Impl::kBwdRecv));
+      }
+    }
     if (node.fwd) {
       const Impl::PoolSlot& ps = st.pool[st.version_colour[tk.version]];
       const int r0 = node.jj0 * I.Rm;
@@ -598,6 +743,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
         Impl::Op o{OK::fwd};
         o.stream = s;
+        if (!c.plan_only)
         o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
                        logits ? as.out32 : nullptr, I.n_out, r0);
@@ -651,6 +797,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           if (l > 0) {
             dst = st.scratch_dz[l - 1];
             act_prev = st.layers[l - 1].act;
+          } else if (!I.local(s - 1)) {
+            dst = as.dzsend;  // sent to the upstream GPU after this task
+            act_prev = I.stages[s - 1].layers.back().act;
           } else {
             const Impl::Stage& pv = I.stages[s - 1];
             dst = pv.acts[pv.mini_act[tk.k]].dzin;
@@ -661,6 +810,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld;
           Impl::Op o{OK::dgrad};
           o.stream = s;
+          if (!c.plan_only)
           o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
                            dst, d.ld_in);
           push(o);
@@ -670,6 +820,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         {
           Impl::Op o{OK::wgrad};
           o.stream = s;
+          if (!c.plan_only)
           o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
                                d.ld_in, static_cast<float>(c.lr));
           push(o);
@@ -698,7 +849,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           ++kernels_per_epoch_;
         }
       }
-      if (c.snapshots) {
+      if (c.snapshots && !c.plan_only) {
         for (int l = 0, po = 0; l < st.L; ++l) {
           const auto& d = st.layers[l];
           Impl::Op o{OK::snapshot};
@@ -720,10 +871,41 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     r.ev = I.new_event();
     node.done = r.ev;
     push(r);
+    // outgoing cross-GPU edges of this node
+    if (node.fwd && s + 1 < W && !I.local(s + 1)) {
+      const auto& ll = st.layers.back();
+      wait_on(Impl::kFwdSend, node.done);
+      Impl::Op sd{OK::send};
+      sd.stream = Impl::kFwdSend;
+      sd.src = as.out16.back() + static_cast<size_t>(node.jj0) * I.Rm * ll.ld_out;
+      sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.ld_out * 2;
+      sd.peer = I.owner[s + 1];
+      sd.dir = 0;
+      push(sd);
+    }
+    if (!node.fwd && s > 0 && !I.local(s - 1)) {
+      wait_on(Impl::kBwdSend, node.done);
+      Impl::Op sd{OK::send};
+      sd.stream = Impl::kBwdSend;
+      sd.src = as.dzsend;
+      sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ld_in * 2;
+      sd.peer = I.owner[s - 1];
+      sd.dir = 1;
+      push(sd);
+    }
   }
 }
 
 Session::~Session() = default;
+
+std::vector<Transfer> Session::transfers() const {
+  std::vector<Transfer> out;
+  using OK = Impl::OpKind;
+  for (const auto& o : impl_->ops)
+    if (o.kind == OK::send || o.kind == OK::recv)
+      out.push_back(Transfer{o.kind == OK::send, o.dir, o.peer, static_cast<int64_t>(o.bytes)});
+  return out;
+}
 
 int64_t Session::stage_param_count(int s) const { return impl_->stages.at(s - 1).param_count; }
 int64_t Session::stage_param_offset(int s) const {
@@ -753,6 +935,7 @@ void Session::load_params(const double* flat) {
   PB_CUDA(cudaSetDevice(cfg_.device));
   std::vector<float> host;
   for (auto& st : I.stages) {
+    if (!I.local(st.id - 1)) continue;
     const int c0 = st.version_colour[0];
     size_t po = static_cast<size_t>(st.param_offset);
     for (int l = 0; l < st.L; ++l) {
@@ -786,6 +969,7 @@ void Session::load_params(const double* flat) {
   if (!I.snaps.empty())
     for (auto& st : I.stages) {
       const int s = st.id - 1;
+      if (!I.local(s)) continue;
       std::vector<float> h(flat + st.param_offset, flat + st.param_offset + st.param_count);
       std::copy(h.begin(), h.end(), I.snaps[s][0]);
     }
@@ -798,6 +982,7 @@ void Session::read_params(double* flat) {
   const int p = cfg_.M % 2;  // current version M lives in master[M % 2]
   std::vector<float> host;
   for (auto& st : I.stages) {
+    if (!I.local(st.id - 1)) continue;  // other GPUs' stages stay untouched
     size_t po = static_cast<size_t>(st.param_offset);
     for (auto& d : st.layers) {
       const size_t nw = static_cast<size_t>(d.in) * d.out;
@@ -807,6 +992,23 @@ void Session::read_params(double* flat) {
       for (size_t i = 0; i < host.size(); ++i) flat[po + i] = host[i];
       po += nw + d.out;
     }
+  }
+}
+
+void Session::read_stage_master(int stage, int parity, double* out) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  PB_CUDA(cudaDeviceSynchronize());
+  auto& st = I.stages.at(stage - 1);
+  std::vector<float> host;
+  size_t po = 0;
+  for (auto& d : st.layers) {
+    const size_t nw = static_cast<size_t>(d.in) * d.out;
+    host.resize(nw + d.out);
+    PB_CUDA(cudaMemcpy(host.data(), d.w32[parity & 1], nw * 4, cudaMemcpyDeviceToHost));
+    PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[parity & 1], d.out * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < host.size(); ++i) out[po + i] = host[i];
+    po += nw + d.out;
   }
 }
 
@@ -859,15 +1061,21 @@ void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
 namespace {
 void issue(Session::Impl& I, cudaStream_t origin) {
   using OK = Session::Impl::OpKind;
+  // every stream this process drives: local stage streams + P2P streams
+  std::vector<cudaStream_t> streams;
+  for (size_t i = 0; i < I.stages.size(); ++i)
+    if (I.local(static_cast<int>(i))) streams.push_back(I.stages[i].stream);
+  for (cudaStream_t c : I.comm)
+    if (c) streams.push_back(c);
   if (!I.fork_ev) {
     I.fork_ev = I.new_event();
-    for (size_t i = 0; i < I.stages.size(); ++i) I.join_ev.push_back(I.new_event());
+    for (size_t i = 0; i < streams.size(); ++i) I.join_ev.push_back(I.new_event());
   }
   cudaEvent_t fork = I.fork_ev;
   PB_CUDA(cudaEventRecord(fork, origin));
-  for (auto& st : I.stages) PB_CUDA(cudaStreamWaitEvent(st.stream, fork, 0));
+  for (cudaStream_t st : streams) PB_CUDA(cudaStreamWaitEvent(st, fork, 0));
   for (const auto& o : I.ops) {
-    cudaStream_t s = o.stream < 0 ? origin : I.stages[o.stream].stream;
+    cudaStream_t s = I.stream_of(o.stream);
     switch (o.kind) {
       case OK::wait: PB_CUDA(cudaStreamWaitEvent(s, o.ev, 0)); break;
       case OK::record: PB_CUDA(cudaEventRecord(o.ev, s)); break;
@@ -891,10 +1099,16 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::memset_i32:
         PB_CUDA(cudaMemsetAsync(o.dst, 0, sizeof(int), s));
         break;
+      case OK::send:
+        I.p2p->send(o.src, o.bytes, o.peer, o.dir, s);
+        break;
+      case OK::recv:
+        I.p2p->recv(o.dst, o.bytes, o.peer, o.dir, s);
+        break;
     }
   }
-  for (size_t i = 0; i < I.stages.size(); ++i) {
-    PB_CUDA(cudaEventRecord(I.join_ev[i], I.stages[i].stream));
+  for (size_t i = 0; i < streams.size(); ++i) {
+    PB_CUDA(cudaEventRecord(I.join_ev[i], streams[i]));
     PB_CUDA(cudaStreamWaitEvent(origin, I.join_ev[i], 0));
   }
 }
@@ -935,8 +1149,8 @@ EpochResult Session::run_epoch() {
   PB_CUDA(cudaMemcpy(r.dev_fwd.data(), I.fwd_trace, r.dev_fwd.size() * 4, cudaMemcpyDeviceToHost));
   PB_CUDA(cudaMemcpy(r.dev_bwd.data(), I.bwd_trace, r.dev_bwd.size() * 4, cudaMemcpyDeviceToHost));
   for (auto& st : I.stages) {
-    int v = 0;
-    PB_CUDA(cudaMemcpy(&v, st.cur_version, 4, cudaMemcpyDeviceToHost));
+    int v = -1;  // -1: stage owned by another GPU
+    if (I.local(st.id - 1)) PB_CUDA(cudaMemcpy(&v, st.cur_version, 4, cudaMemcpyDeviceToHost));
     r.dev_current.push_back(v);
   }
   // mini loss: mean over micro-batches of the micro mean (trainer.cpp:462-469)

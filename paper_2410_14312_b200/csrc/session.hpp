@@ -47,8 +47,24 @@ struct SessionConfig {
   // stage range owned by this process (multi-GPU: one process per GPU);
   // [stage_lo, stage_hi] 1-based inclusive.  Default: all stages.
   int stage_lo = 1, stage_hi = 0;
+  // multi-GPU: this process's rank among `world` (one process per GPU); the
+  // stage range defaults to an even contiguous split.  nccl_ids holds the
+  // 2*(world-1) NCCL unique ids (boundary x direction), identical on all ranks.
+  int rank = 0, world = 1;
+  std::vector<uint8_t> nccl_ids;
+  // build the program only (no CUDA calls): used to check the cross-GPU
+  // transfer schedule on machines without GPUs
+  bool plan_only = false;
   // max micro-batches per coalesced forward launch (0 = N: a whole run)
   int fwd_merge = 0;
+};
+
+// One point-to-point transfer of the program, in this process's issue order.
+struct Transfer {
+  bool send;      // false: receive
+  int dir;        // 0 activations (s -> s+1), 1 deltas (s+1 -> s)
+  int peer;       // rank
+  int64_t bytes;
 };
 
 struct EpochResult {
@@ -80,6 +96,10 @@ class Session {
   void read_params(double* flat);
   // fp32 snapshot of `version` of stage s (requires snapshots=true).
   const float* snapshot(int s, int version) const;
+  bool has_snapshots() const { return cfg_.snapshots; }
+  // fp32 master buffer `parity` (0/1) of stage s: holds the last committed
+  // version with that parity (versions M and M-1 after an epoch).
+  void read_stage_master(int stage, int parity, double* out);
 
   // Host -> device copy of the epoch's data (rows = M*B), then conversion.
   void upload(const void* x, HostDType xt, const void* y, HostDType yt,
@@ -95,6 +115,7 @@ class Session {
   std::vector<int> act_slot_counts() const;
   int64_t device_bytes() const { return arena_bytes_; }
   int kernels_per_epoch() const { return kernels_per_epoch_; }
+  std::vector<Transfer> transfers() const;
 
   struct Impl;  // public so the program-issue helpers can see it
 
