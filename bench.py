@@ -215,10 +215,18 @@ def main():
 
     W, Nm, B, M = args.stages, CFG["N"], CFG["B"], args.mini_batches
     net = P.NetworkSpec(CFG["widths"], CFG["acts"], CFG["loss"])
-    # Each rank runs the full W-stage pipeline on its GPU (replicas) until the
-    # cross-GPU stage split lands; value aggregates over ranks.
-    sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
-                     use_graph=not args.no_graph)
+    # N GPUs: the W=8 stages are split into N contiguous ranges, one process
+    # per GPU, activations / deltas cross GPUs point to point over NVLink.
+    # PIPESIM_REPLICAS=1 instead runs N independent full pipelines.
+    split = world > 1 and not os.environ.get("PIPESIM_REPLICAS")
+    if split:
+        ids = [P.nccl_unique_ids(world)] if rank == 0 else [None]
+        dist.broadcast_object_list(ids, src=0)
+        sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
+                         use_graph=not args.no_graph, rank=rank, world=world, nccl_ids=ids[0])
+    else:
+        sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
+                         use_graph=not args.no_graph)
     p0 = P.init_network_params(net, CFG["seed"])
     sess.load_params(p0)
     rows = M * B
@@ -264,7 +272,8 @@ def main():
         t = torch.tensor([ms_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    value = world * rows / (ms_step / 1000.0)
+    jobs = 1 if split else world  # a split pipeline processes the step's rows once
+    value = jobs * rows / (ms_step / 1000.0)
 
     # ---- e2e through the C ABI: H2D of the step's inputs + D2H of the losses
     for _ in range(2):
@@ -281,7 +290,7 @@ def main():
         t = torch.tensor([e2e_step_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step_ms = float(t.item())
-    e2e_value = world * rows / (e2e_step_ms / 1000.0)
+    e2e_value = jobs * rows / (e2e_step_ms / 1000.0)
 
     if rank != 0:
         if world > 1:
@@ -306,13 +315,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+        "higher_is_better": True, "scaling": "weak" if (world > 1 and not split) else "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": "deep MLP 16x4096 (BASELINE configs[2]) nF1B pipeline step",
                    "model": "mlp-16x4096-relu-ce4096", "global_batch": B, "seq_len": None,
                    "micro_batches": Nm, "stages": W, "mini_batches_per_step": M,
                    "samples_per_step": rows,
-                   "parallelism": f"pp{W}-on-{world}gpu" + ("-replicas" if world > 1 else ""),
+                   "parallelism": f"pp{W}-on-{world}gpu" + ("-replicas" if world > 1 and not split else ""),
                    "l2": "working set (bf16 weights 537 MB + fp32 masters 1.07 GB) > L2, no flush",
                    "precision": "bf16 operands, fp32 accumulate, fp32 master weights"},
         "roofline": roof,

@@ -71,7 +71,9 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
     d4[0] = make_uint4(p[0], p[1], p[2], p[3]);
     d4[1] = make_uint4(p[4], p[5], p[6], p[7]);
   } else {
-    for (int i = 0; i < valid && i < 16; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < valid) dst[i] = __float2bfloat16_rn(v[i]);
   }
 }
 
@@ -105,7 +107,9 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
         for (int i = 0; i < 4; ++i)
           d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       } else {
-        for (int i = 0; i < valid; ++i) dst[i] = v[i];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < valid) dst[i] = v[i];
       }
     }
   } else if constexpr (EPI == kEpiDgrad) {
@@ -119,8 +123,9 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
         for (int i = 0; i < 16; ++i)
           v[i] *= act_grad_from_out(__bfloat162float(xh[i]), ep.act_prev);
       } else {
-        for (int i = 0; i < valid; ++i)
-          v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < valid) v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
       }
     }
     store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
@@ -141,11 +146,13 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
         n4[i] = w;
       }
     } else {
-      for (int i = 0; i < valid; ++i) {
-        const float w = ep.w_cur[o32 + i] - ep.lr * v[i];
-        ep.w_new[o32 + i] = w;
-        v[i] = w;
-      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < valid) {
+          const float w = ep.w_cur[o32 + i] - ep.lr * v[i];
+          ep.w_new[o32 + i] = w;
+          v[i] = w;
+        }
     }
     if (ep.w16)
       store_bf16x16(ep.w16 + static_cast<size_t>(row) * ep.ld_w16 + n, v, valid,
@@ -287,8 +294,9 @@ __global__ void __launch_bounds__(128, 1)
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (128B swizzle atoms) by offsetting the shared array
+  // itself, so every derived pointer stays in the shared address space.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
@@ -435,8 +443,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
   using Cfg = Gemm2Cfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (128B swizzle atoms) by offsetting the shared array
+  // itself, so every derived pointer stays in the shared address space.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kAHalf;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);

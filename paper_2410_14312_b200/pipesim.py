@@ -573,7 +573,7 @@ class Session:
 
     def __init__(self, net: NetworkSpec, workers, micro_batches, mini_batch_size,
                  mini_batches, learning_rate, mode="timeprest", device=0, use_graph=True,
-                 snapshots=False, fwd_merge=0):
+                 snapshots=False, fwd_merge=0, rank=0, world=1, nccl_ids=b""):
         if mode not in TRAIN_MODES:
             raise DomainError(f"unknown training mode: {mode}", "mode")
         self.net = net
@@ -585,7 +585,12 @@ class Session:
                               int(use_graph), int(snapshots), int(fwd_merge))
         spec = net._c()
         h = C.c_void_p()
-        N.check(_L().pb_session_create(C.byref(spec), C.byref(cfg), C.byref(h)))
+        if world > 1:
+            N.check(_L().pb_session_create_dist(C.byref(spec), C.byref(cfg), rank, world,
+                                                bytes(nccl_ids), len(nccl_ids), C.byref(h)))
+        else:
+            N.check(_L().pb_session_create(C.byref(spec), C.byref(cfg), C.byref(h)))
+        self.rank, self.world = rank, world
         self._h = h
         self.snapshots = snapshots
         self.param_count = net.param_count()
@@ -664,6 +669,38 @@ class Session:
         r["dev_fwd"] = r["dev_fwd"].reshape(M, U, W)
         r["dev_bwd"] = r["dev_bwd"].reshape(M, W)
         return r
+
+
+def nccl_unique_ids(world: int) -> bytes:
+    """2*(world-1) NCCL unique ids (one per pipeline boundary and direction);
+    made on rank 0 and shared with the other ranks by the caller."""
+    out = b""
+    for _ in range(2 * (world - 1)):
+        buf = C.create_string_buffer(128)
+        N.check(_L().pb_nccl_unique_id(buf))
+        out += buf.raw[:128]
+    return out
+
+
+def plan_transfers(net: NetworkSpec, workers, micro_batches, mini_batch_size, mini_batches,
+                   mode="timeprest", rank=0, world=1, fwd_merge=0):
+    """The point-to-point transfers rank `rank` issues in one epoch, in order:
+    list of (kind 'send'|'recv', direction 0 act / 1 delta, peer, bytes).
+    Host only (no GPU)."""
+    cfg = pb_train_config(workers, micro_batches, mini_batch_size, mini_batches, 0.05,
+                          TRAIN_MODES.index(mode), 0, 0, 0, int(fwd_merge))
+    spec = net._c()
+    n = C.c_int()
+    N.check(_L().pb_plan_transfers(C.byref(spec), C.byref(cfg), rank, world, C.byref(n),
+                                   None, None, None, None, 0))
+    k = np.zeros(max(n.value, 1), np.int32)
+    d = np.zeros_like(k)
+    p = np.zeros_like(k)
+    b = np.zeros(max(n.value, 1), np.int64)
+    N.check(_L().pb_plan_transfers(C.byref(spec), C.byref(cfg), rank, world, C.byref(n),
+                                   _ip(k), _ip(d), _ip(p), b.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   n.value))
+    return [("send" if k[i] else "recv", int(d[i]), int(p[i]), int(b[i])) for i in range(n.value)]
 
 
 _SESSIONS: Dict[tuple, Session] = {}
