@@ -83,6 +83,7 @@ pb::SessionConfig make_config(const pb_net_spec* net, const pb_train_config* cfg
   c.snapshots = cfg->snapshots != 0;
   c.fwd_merge = cfg->fwd_merge;
   if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
+  if (const char* e = std::getenv("PIPESIM_SIDE")) c.side_streams = std::atoi(e) != 0;
   return c;
 }
 }  // namespace

@@ -87,6 +87,7 @@ struct Session::Impl {
     std::vector<int> mini_act;               // [M+1]
     int* cur_version = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // wgrad/bias of a backward run beside the dgrad chain
     int64_t param_offset = 0, param_count = 0;
   };
 
@@ -100,6 +101,7 @@ struct Session::Impl {
                       send, recv };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
+  static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
   struct Op {
     OpKind kind;
     int stream = 0;  // stage index (0-based); -1 = origin stream
@@ -170,6 +172,7 @@ struct Session::Impl {
   bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
   cudaStream_t stream_of(int idx) const {
     if (idx >= 0) return stages[idx].stream;
+    if (idx <= kSideBase) return stages[kSideBase - idx].side;
     if (idx == -1) return origin;
     return comm[-idx - 2];
   }
@@ -193,8 +196,10 @@ struct Session::Impl {
       for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (t0) cudaEventDestroy(t0);
     if (t1) cudaEventDestroy(t1);
-    for (Stage& s : stages)
+    for (Stage& s : stages) {
       if (s.stream) cudaStreamDestroy(s.stream);
+      if (s.side) cudaStreamDestroy(s.side);
+    }
     if (origin) cudaStreamDestroy(origin);
     for (cudaStream_t c : comm)
       if (c) cudaStreamDestroy(c);
@@ -476,7 +481,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   if (!c.plan_only) {
   PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
   for (int s = 0; s < W; ++s)
-    if (I.local(s)) PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].stream, cudaStreamNonBlocking));
+    if (I.local(s)) {
+      PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].stream, cudaStreamNonBlocking));
+      if (c.side_streams)
+        PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].side, cudaStreamNonBlocking));
+    }
   if (c.world > 1) {
     for (cudaStream_t& cs : I.comm) PB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     I.p2p = std::make_unique<P2P>(c.rank, c.world, c.nccl_ids.data(), c.nccl_ids.size());
@@ -780,6 +789,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
       Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
       const int cur = (tk.k - 1) % 2, nxt = tk.k % 2;
+      // wgrad+SGD and bias of layer l run on the side stream as soon as dZ_l
+      // exists, overlapping the dgrad chain of the layers below (which only
+      // needs dZ); joined back before the task completes.
+      const int side = c.side_streams ? Impl::kSideBase - s : s;
+      if (c.side_streams) wait_on(side, record_on(s));
       for (int l = st.L - 1; l >= 0; --l) {
         const auto& d = st.layers[l];
         __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
@@ -816,10 +830,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           push(o);
           ++kernels_per_epoch_;
         }
+        // the side stream's work on layer l only reads dZ_l (and x); it was
+        // made ready before this iteration (dZ_{L-1}: task start; dZ_l: the
+        // previous iteration's dgrad, signalled below)
         // wgrad + SGD into the new version (trainer.cpp:244-249, :484-488)
         {
           Impl::Op o{OK::wgrad};
-          o.stream = s;
+          o.stream = side;
           if (!c.plan_only)
           o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
                                d.ld_in, static_cast<float>(c.lr));
@@ -829,7 +846,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         // bias gradient + SGD; the last one stamps the commit
         {
           Impl::Op o{OK::bias};
-          o.stream = s;
+          o.stream = side;
           o.dz = dz;
           o.rows = c.B;
           o.cols = d.out;
@@ -848,7 +865,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           push(o);
           ++kernels_per_epoch_;
         }
+        // dZ_{l-1} (written by this iteration's dgrad on the main stream) is
+        // what the side stream needs next
+        if (c.side_streams && l > 0) wait_on(side, record_on(s));
       }
+      if (c.side_streams) wait_on(s, record_on(side));  // join
       if (c.snapshots && !c.plan_only) {
         for (int l = 0, po = 0; l < st.L; ++l) {
           const auto& d = st.layers[l];
@@ -1064,7 +1085,10 @@ void issue(Session::Impl& I, cudaStream_t origin) {
   // every stream this process drives: local stage streams + P2P streams
   std::vector<cudaStream_t> streams;
   for (size_t i = 0; i < I.stages.size(); ++i)
-    if (I.local(static_cast<int>(i))) streams.push_back(I.stages[i].stream);
+    if (I.local(static_cast<int>(i))) {
+      streams.push_back(I.stages[i].stream);
+      if (I.stages[i].side) streams.push_back(I.stages[i].side);
+    }
   for (cudaStream_t c : I.comm)
     if (c) streams.push_back(c);
   if (!I.fork_ev) {

@@ -57,6 +57,8 @@ struct SessionConfig {
   bool plan_only = false;
   // max micro-batches per coalesced forward launch (0 = N: a whole run)
   int fwd_merge = 0;
+  // per-stage side stream for wgrad/bias (overlaps the dgrad chain)
+  bool side_streams = true;
 };
 
 // One point-to-point transfer of the program, in this process's issue order.
