@@ -257,6 +257,29 @@ int pb_session_run_epoch(pb_session* s, pb_epoch_out* out);
 /* upload + run_epoch. */
 int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
                            const void* y, int y_dtype, pb_epoch_out* out);
+/* Per-node timeline of one epoch (pipeline bubble).  A node is one backward
+ * task or one coalesced run of forward tasks of a stage; its span is taken
+ * on its stage stream after its cross-stage waits.  Arrays are caller
+ * allocated with max_nodes entries (n_nodes reports the count; stage_busy_ms
+ * has W entries, -1 for stages on other GPUs). */
+typedef struct {
+  float makespan_ms;
+  float* stage_busy_ms;
+  int max_nodes;
+  int n_nodes;
+  int* node_stage;      /* 1-based */
+  int* node_fwd;        /* 1 forward run, 0 backward */
+  int* node_mini;
+  int* node_micro_lo;   /* 0-based micro-batch range of a forward run */
+  int* node_micro_hi;
+  float* node_start_ms;
+  float* node_end_ms;
+} pb_epoch_profile;
+
+/* One epoch without the CUDA graph, with CUDA timing events around every
+ * node (for the bubble report; slower than run_epoch). */
+int pb_session_profile_epoch(pb_session* s, pb_epoch_out* out, pb_epoch_profile* prof);
+
 /* fp32 snapshot of stage `stage` (1-based) at `version`, widened to f64. */
 int pb_session_snapshot(pb_session* s, int stage, int version, double* out,
                         int64_t n);

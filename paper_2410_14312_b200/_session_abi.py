@@ -20,6 +20,15 @@ class pb_epoch_out(C.Structure):
                 ("device_ms", C.c_float)]
 
 
+class pb_epoch_profile(C.Structure):
+    _fields_ = [("makespan_ms", C.c_float), ("stage_busy_ms", C.POINTER(C.c_float)),
+                ("max_nodes", C.c_int), ("n_nodes", C.c_int),
+                ("node_stage", C.POINTER(C.c_int)), ("node_fwd", C.POINTER(C.c_int)),
+                ("node_mini", C.POINTER(C.c_int)), ("node_micro_lo", C.POINTER(C.c_int)),
+                ("node_micro_hi", C.POINTER(C.c_int)), ("node_start_ms", C.POINTER(C.c_float)),
+                ("node_end_ms", C.POINTER(C.c_float))]
+
+
 class pb_session_info(C.Structure):
     _fields_ = [("horizon", C.c_int), ("units", C.c_int), ("kernels_per_epoch", C.c_int),
                 ("device_bytes", C.c_int64), ("param_count", C.c_int64),
@@ -41,6 +50,7 @@ def signatures():
         "pb_session_upload": (i, [p, p, i, p, i]),
         "pb_session_run_epoch": (i, [p, P(pb_epoch_out)]),
         "pb_session_train_epoch": (i, [p, p, i, p, i, P(pb_epoch_out)]),
+        "pb_session_profile_epoch": (i, [p, P(pb_epoch_out), P(pb_epoch_profile)]),
         "pb_session_snapshot": (i, [p, i, i, P(C.c_double), i64]),
         "pb_session_read_version": (i, [p, i, i, P(C.c_double), i64]),
         "pb_nccl_unique_id": (i, [C.c_char_p]),

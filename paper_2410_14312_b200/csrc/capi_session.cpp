@@ -215,6 +215,32 @@ int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
   PB_GUARD_END
 }
 
+int pb_session_profile_epoch(pb_session* s, pb_epoch_out* out, pb_epoch_profile* prof) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  pb::EpochProfile p;
+  const pb::EpochResult r = x.profile_epoch(&p);
+  fill(r, x, out);
+  if (prof) {
+    prof->makespan_ms = p.makespan_ms;
+    if (prof->stage_busy_ms)
+      for (size_t i = 0; i < p.busy_ms.size(); ++i) prof->stage_busy_ms[i] = p.busy_ms[i];
+    prof->n_nodes = static_cast<int>(p.nodes.size());
+    const int n = std::min(prof->n_nodes, prof->max_nodes);
+    for (int i = 0; i < n; ++i) {
+      const pb::NodeTiming& t = p.nodes[i];
+      if (prof->node_stage) prof->node_stage[i] = t.stage;
+      if (prof->node_fwd) prof->node_fwd[i] = t.fwd;
+      if (prof->node_mini) prof->node_mini[i] = t.mini;
+      if (prof->node_micro_lo) prof->node_micro_lo[i] = t.micro_lo;
+      if (prof->node_micro_hi) prof->node_micro_hi[i] = t.micro_hi;
+      if (prof->node_start_ms) prof->node_start_ms[i] = t.start_ms;
+      if (prof->node_end_ms) prof->node_end_ms[i] = t.end_ms;
+    }
+  }
+  PB_GUARD_END
+}
+
 int pb_session_snapshot(pb_session* s, int stage, int version, double* out, int64_t n) {
   PB_GUARD_BEGIN
   pb::Session& x = S(s);

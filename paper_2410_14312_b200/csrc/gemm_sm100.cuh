@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda.h>
+#include <type_traits>
 
 #include "gemm_types.hpp"
 #include "sm100_ptx.cuh"
@@ -33,6 +34,45 @@ __device__ __forceinline__ float act_fwd(float z, int act) {
     case kTanh: return tanhf(z);
     case kSigmoid: return 1.f / (1.f + expf(-z));
     default: return z;
+  }
+}
+
+// tanh / sigmoid through expf and a fast divide: no called slow paths in
+// the epilogue (a call forces the kernel's live registers to the stack);
+// absolute error ~1e-7, far below the bf16 rounding of the stored output.
+template <int ACT>
+__device__ __forceinline__ float act_fwd_t(float z) {
+  if constexpr (ACT == kRelu) return z > 0.f ? z : 0.f;
+  else if constexpr (ACT == kTanh) return 1.f - __fdividef(2.f, expf(2.f * z) + 1.f);
+  else if constexpr (ACT == kSigmoid) return __fdividef(1.f, 1.f + expf(-z));
+  else return z;
+}
+
+template <int ACT>
+__device__ __forceinline__ float act_grad_t(float a) {
+  if constexpr (ACT == kRelu) return a > 0.f ? 1.f : 0.f;
+  else if constexpr (ACT == kTanh) return 1.f - a * a;
+  else if constexpr (ACT == kSigmoid) return a * (1.f - a);
+  else return 1.f;
+}
+
+// Runs f(integral_constant<ACT>) for the epilogue's activation: the
+// activation is a compile-time parameter of the epilogue code, so each
+// instantiation stays small (one hot variant per launch keeps the
+// instruction cache warm; a runtime switch inside the unrolled element
+// loops more than doubled the kernel's code size).
+template <int EPI, typename F>
+__device__ __forceinline__ void with_act(const EpiParams& ep, F&& f) {
+  if constexpr (EPI == kEpiWgradSgd) {
+    f(std::integral_constant<int, kLinear>{});
+  } else {
+    const int a = EPI == kEpiFwd ? ep.act : ep.act_prev;
+    switch (a) {
+      case kRelu: f(std::integral_constant<int, kRelu>{}); break;
+      case kTanh: f(std::integral_constant<int, kTanh>{}); break;
+      case kSigmoid: f(std::integral_constant<int, kSigmoid>{}); break;
+      default: f(std::integral_constant<int, kLinear>{}); break;
+    }
   }
 }
 
@@ -56,6 +96,7 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256;
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v,
@@ -86,15 +127,24 @@ __device__ __forceinline__ void write_tags(const EpiParams& ep) {
 }
 
 // Fused epilogue on one 16-column chunk of one output row (fp32 values).
-template <int EPI>
+template <int EPI, int ACT>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmShape& sh,
                                                int row, int n, int valid, float (&v)[16]) {
   if constexpr (EPI == kEpiFwd) {
+    float b[16];
+    if (ep.bias && valid == 16 && (reinterpret_cast<uintptr_t>(ep.bias + n) & 15) == 0) {
+      const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float b = (ep.bias && i < valid) ? ep.bias[n + i] : 0.f;
-      v[i] = act_fwd(v[i] + b, ep.act);
+      for (int i = 0; i < 4; ++i) {
+        const float4 q = __ldg(b4 + i);
+        b[4 * i] = q.x; b[4 * i + 1] = q.y; b[4 * i + 2] = q.z; b[4 * i + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) b[i] = (ep.bias && i < valid) ? ep.bias[n + i] : 0.f;
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = act_fwd_t<ACT>(v[i] + b[i]);
     const size_t yr = static_cast<size_t>(row + ep.y_row_off);
     if (ep.y16)
       store_bf16x16(ep.y16 + yr * ep.ld_y16 + n, v, valid,
@@ -113,7 +163,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
       }
     }
   } else if constexpr (EPI == kEpiDgrad) {
-    if (ep.act_prev != kLinear) {
+    if constexpr (ACT != kLinear) {
       const __nv_bfloat16* xr = ep.xin + static_cast<size_t>(row) * ep.ld_xin + n;
       if (valid == 16 && (ep.ld_xin % 8) == 0) {
         const uint4* x4 = reinterpret_cast<const uint4*>(xr);
@@ -121,11 +171,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
         const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(q);
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          v[i] *= act_grad_from_out(__bfloat162float(xh[i]), ep.act_prev);
+          v[i] *= act_grad_t<ACT>(__bfloat162float(xh[i]));
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          if (i < valid) v[i] *= act_grad_from_out(__bfloat162float(xr[i]), ep.act_prev);
+          if (i < valid) v[i] *= act_grad_t<ACT>(__bfloat162float(xr[i]));
       }
     }
     store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
@@ -169,7 +219,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, const GemmSh
 // 128-byte (fp32) or 64-byte (bf16) contiguous row segment per instruction,
 // and the 32 row loads of a block are issued back to back (memory-level
 // parallelism for the HBM-bound SGD update).
-template <int EPI>
+template <int EPI, int ACT>
 __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const GemmShape& sh,
                                                    int row_base, int n_base, int n_cols,
                                                    uint32_t t_row, float* T) {
@@ -183,7 +233,7 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
     const int n = n_base + lane;
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      wnext[i] = (i < rows_valid && n < sh.N)
+      wnext[i] = (i < rows_valid && n < sh.N && !(ep.dbg_skip & 2))
                      ? ep.w_cur[static_cast<size_t>(row_base + i) * ep.ld_w32 + n]
                      : 0.f;
   }
@@ -198,7 +248,7 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
       if (c + 32 < n_cols) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          wnext[i] = (i < rows_valid && nn < sh.N)
+          wnext[i] = (i < rows_valid && nn < sh.N && !(ep.dbg_skip & 2))
                          ? ep.w_cur[static_cast<size_t>(row_base + i) * ep.ld_w32 + nn]
                          : 0.f;
       }
@@ -224,7 +274,7 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           if (i >= rows) break;
-          const float a = act_fwd(v[i] + b, ep.act);
+          const float a = act_fwd_t<ACT>(v[i] + b);
           const size_t yr = static_cast<size_t>(row_base + i + ep.y_row_off);
           if (ep.y16) ep.y16[yr * ep.ld_y16 + n] = __float2bfloat16_rn(a);
           if (ep.y32) ep.y32[yr * ep.ld_y32 + n] = a;
@@ -232,7 +282,7 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
       }
     } else if constexpr (EPI == kEpiDgrad) {
       if (col_ok) {
-        if (ep.act_prev != kLinear) {
+        if constexpr (ACT != kLinear) {
           float g[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i)
@@ -240,7 +290,7 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
                                   ep.xin[static_cast<size_t>(row_base + i) * ep.ld_xin + n])
                             : 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= act_grad_from_out(g[i], ep.act_prev);
+          for (int i = 0; i < 32; ++i) v[i] *= act_grad_t<ACT>(g[i]);
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -254,8 +304,8 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
         for (int i = 0; i < 32; ++i) {
           if (i >= rows) break;
           const float nw = wcur[i] - ep.lr * v[i];
-          ep.w_new[static_cast<size_t>(row_base + i) * ep.ld_w32 + n] = nw;
-          if (ep.w16)
+          if (!(ep.dbg_skip & 4)) ep.w_new[static_cast<size_t>(row_base + i) * ep.ld_w32 + n] = nw;
+          if (ep.w16 && !(ep.dbg_skip & 8))
             ep.w16[static_cast<size_t>(row_base + i) * ep.ld_w16 + n] = __float2bfloat16_rn(nw);
         }
       }
@@ -264,25 +314,325 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
 }
 
 // Row-per-thread epilogue (thread i owns row i; 16-column vector chunks).
-template <int EPI>
+template <int EPI, int ACT>
 __device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const GemmShape& sh,
                                                    int row_base, int n_base, int n_cols,
                                                    uint32_t t_row) {
   const int row = row_base + static_cast<int>(threadIdx.x % 32);
   const bool row_ok = row < sh.M;
+  // dgrad act' gating: the stored activation of chunk c+1 is loaded while
+  // chunk c is processed (vector path: full 16-column chunks, 16-byte rows)
+  constexpr bool kGate = EPI == kEpiDgrad && ACT != kLinear;
+  const bool vec = kGate && (ep.ld_xin % 8) == 0 && (sh.N % 16) == 0;
+  const __nv_bfloat16* xrow = kGate ? ep.xin + static_cast<size_t>(row) * ep.ld_xin : nullptr;
+  if constexpr (EPI == kEpiWgradSgd) {
+    if ((ep.ld_w32 % 4) == 0 && (ep.ld_w16 % 8) == 0 && (sh.N % 16) == 0) {
+      // SGD rows: this thread's row, 16 columns per step; the fp32 master of
+      // step c+1 is loaded while step c is updated and stored
+      const float* wrow = ep.w_cur + static_cast<size_t>(row) * ep.ld_w32;
+      float* nrow = ep.w_new + static_cast<size_t>(row) * ep.ld_w32;
+      __nv_bfloat16* hrow = ep.w16 ? ep.w16 + static_cast<size_t>(row) * ep.ld_w16 : nullptr;
+      float4 wa[4], wb[4];
+      if (row_ok && n_base < sh.N)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wa[i] = reinterpret_cast<const float4*>(wrow + n_base)[i];
+#pragma unroll 1
+      for (int c = 0; c < n_cols; c += 16) {
+        const int n = n_base + c;
+        if (n >= sh.N) break;  // warp-uniform
+        if (row_ok && c + 16 < n_cols && n + 16 < sh.N)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) wb[i] = reinterpret_cast<const float4*>(wrow + n + 16)[i];
+        uint32_t r[16];
+        ptx::tmem_ld16(t_row + c, r);
+        ptx::tmem_ld_wait();
+        if (row_ok) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            v[4 * i] = wa[i].x - ep.lr * __uint_as_float(r[4 * i]);
+            v[4 * i + 1] = wa[i].y - ep.lr * __uint_as_float(r[4 * i + 1]);
+            v[4 * i + 2] = wa[i].z - ep.lr * __uint_as_float(r[4 * i + 2]);
+            v[4 * i + 3] = wa[i].w - ep.lr * __uint_as_float(r[4 * i + 3]);
+            reinterpret_cast<float4*>(nrow + n)[i] =
+                make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+          if (hrow) store_bf16x16(hrow + n, v, 16, true);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) wa[i] = wb[i];
+      }
+      return;
+    }
+  }
+  uint4 xa[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  if (vec && row_ok && n_base < sh.N) {
+    const uint4* p = reinterpret_cast<const uint4*>(xrow + n_base);
+    xa[0] = p[0];
+    xa[1] = p[1];
+  }
 #pragma unroll 1
   for (int c = 0; c < n_cols; c += 16) {
     const int n = n_base + c;
     if (n >= sh.N) break;  // warp-uniform
+    uint4 xb[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+    if (vec && row_ok && c + 16 < n_cols && n + 16 < sh.N) {
+      const uint4* p = reinterpret_cast<const uint4*>(xrow + n + 16);
+      xb[0] = p[0];
+      xb[1] = p[1];
+    }
     uint32_t r[16];
     ptx::tmem_ld16(t_row + c, r);
     ptx::tmem_ld_wait();
-    if (!row_ok) continue;
-    const int valid = sh.N - n < 16 ? sh.N - n : 16;
+    if (row_ok) {
+      const int valid = sh.N - n < 16 ? sh.N - n : 16;
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+      if constexpr (kGate) {
+        if (vec) {
+          const __nv_bfloat16* xh = reinterpret_cast<const __nv_bfloat16*>(xa);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= act_grad_t<ACT>(__bfloat162float(xh[i]));
+          store_bf16x16(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n, v, valid,
+                        (ep.ld_d16 % 8) == 0);
+        } else {
+          epilogue_chunk<EPI, ACT>(ep, sh, row, n, valid, v);
+        }
+      } else {
+        epilogue_chunk<EPI, ACT>(ep, sh, row, n, valid, v);
+      }
+    }
+    xa[0] = xb[0];
+    xa[1] = xb[1];
+  }
+}
+
+// Vectorised transposed epilogue (the default): one warp's 32 rows x
+// n_cols accumulator, 32 columns per step.  tcgen05.ld hands thread i row i;
+// the 32 x 32 fp32 block is staged row-major in padded smem (row stride 36
+// floats: the float4 stores of 32 rows and the float4 reads of 4 rows x
+// 128 B are both at the 4-wavefront minimum), then lane l serves row
+// 4*rr + l/8, columns 4*(l%8)..+3 of the block for rr = 0..7.  Every global
+// access is a 16-byte (fp32) or 8-byte (bf16) vector and one warp
+// instruction covers 4 full row segments (4 x 128 B fp32 / 4 x 64 B bf16):
+// a quarter of the memory instructions of a lane-per-column layout.  The
+// global inputs of step c+1 (fp32 masters for SGD, stored activations for
+// the dgrad gate) are loaded while step c is processed.
+constexpr int kVecLd = 36;  // staging row stride (floats)
+
+template <int EPI, int ACT>
+__device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const GemmShape& sh,
+                                                  int row_base, int n_base, int n_cols,
+                                                  uint32_t t_row, float* T) {
+  const int lane = threadIdx.x % 32;
+  const int sub_r = lane >> 3;
+  const int c4 = (lane & 7) * 4;
+  constexpr bool kSgd = EPI == kEpiWgradSgd;
+  constexpr bool kGate = EPI == kEpiDgrad && ACT != kLinear;
+  // per-step global inputs: 8 rows per lane
+  float4 win[8];
+  uint2 xin[8];
+  auto load_inputs = [&](int c, float4 (&w)[8], uint2 (&x)[8]) {
+    const int n = n_base + c + c4;
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      const int row = row_base + rr * 4 + sub_r;
+      const bool ok = row < sh.M && n + 3 < sh.N;
+      if constexpr (kSgd) {
+        w[rr] = ok ? __ldcs(reinterpret_cast<const float4*>(ep.w_cur + static_cast<size_t>(row) *
+                                                                           ep.ld_w32 + n))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if constexpr (kGate) {
+        x[rr] = ok ? *reinterpret_cast<const uint2*>(ep.xin + static_cast<size_t>(row) *
+                                                                  ep.ld_xin + n)
+                   : make_uint2(0u, 0u);
+      }
+    }
+  };
+  load_inputs(0, win, xin);
+#pragma unroll 1
+  for (int c = 0; c < n_cols; c += 32) {
+    if (n_base + c >= sh.N) break;  // warp-uniform
+    {
+      uint32_t r[32];
+      ptx::tmem_ld32(t_row + c, r);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(T + lane * kVecLd + 4 * j) =
+            make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+    }
+    // next step's inputs go in flight once the accumulator registers are free
+    float4 wnx[8];
+    uint2 xnx[8];
+    if (c + 32 < n_cols && n_base + c + 32 < sh.N) load_inputs(c + 32, wnx, xnx);
+    __syncwarp();
+    const int n = n_base + c + c4;
+    float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (EPI == kEpiFwd) {
+      if (ep.bias && n + 3 < sh.N) bias4 = __ldg(reinterpret_cast<const float4*>(ep.bias + n));
+    }
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      const int rl = rr * 4 + sub_r;
+      const int row = row_base + rl;
+      const float4 a = *reinterpret_cast<const float4*>(T + rl * kVecLd + c4);
+      float v[4] = {a.x, a.y, a.z, a.w};
+      if (row >= sh.M) continue;
+      if (n + 3 < sh.N) {
+        if constexpr (EPI == kEpiFwd) {
+          v[0] = act_fwd_t<ACT>(v[0] + bias4.x);
+          v[1] = act_fwd_t<ACT>(v[1] + bias4.y);
+          v[2] = act_fwd_t<ACT>(v[2] + bias4.z);
+          v[3] = act_fwd_t<ACT>(v[3] + bias4.w);
+          const size_t yr = static_cast<size_t>(row + ep.y_row_off);
+          if (ep.y16) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+            *reinterpret_cast<uint2*>(ep.y16 + yr * ep.ld_y16 + n) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+          }
+          if (ep.y32)
+            *reinterpret_cast<float4*>(ep.y32 + yr * ep.ld_y32 + n) =
+                make_float4(v[0], v[1], v[2], v[3]);
+        } else if constexpr (EPI == kEpiDgrad) {
+          if constexpr (kGate) {
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xin[rr]);
+            const float2 x01 = __bfloat1622float2(xh[0]);
+            const float2 x23 = __bfloat1622float2(xh[1]);
+            v[0] *= act_grad_t<ACT>(x01.x);
+            v[1] *= act_grad_t<ACT>(x01.y);
+            v[2] *= act_grad_t<ACT>(x23.x);
+            v[3] *= act_grad_t<ACT>(x23.y);
+          }
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+          *reinterpret_cast<uint2*>(ep.d16 + static_cast<size_t>(row) * ep.ld_d16 + n) =
+              make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        } else {
+          const float4 w = win[rr];
+          v[0] = w.x - ep.lr * v[0];
+          v[1] = w.y - ep.lr * v[1];
+          v[2] = w.z - ep.lr * v[2];
+          v[3] = w.w - ep.lr * v[3];
+          // the new master is next read one mini-batch later: stream it past L2
+          __stcs(reinterpret_cast<float4*>(ep.w_new + static_cast<size_t>(row) * ep.ld_w32 + n),
+                 make_float4(v[0], v[1], v[2], v[3]));
+          if (ep.w16) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+            *reinterpret_cast<uint2*>(ep.w16 + static_cast<size_t>(row) * ep.ld_w16 + n) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0),
+                           *reinterpret_cast<uint32_t*>(&h1));
+          }
+        }
+      } else {  // ragged right edge: scalar columns
+        for (int i = 0; i < 4 && n + i < sh.N; ++i) {
+          float x = v[i];
+          const int col = n + i;
+          if constexpr (EPI == kEpiFwd) {
+            x = act_fwd_t<ACT>(x + (ep.bias ? ep.bias[col] : 0.f));
+            const size_t yr = static_cast<size_t>(row + ep.y_row_off);
+            if (ep.y16) ep.y16[yr * ep.ld_y16 + col] = __float2bfloat16_rn(x);
+            if (ep.y32) ep.y32[yr * ep.ld_y32 + col] = x;
+          } else if constexpr (EPI == kEpiDgrad) {
+            if constexpr (kGate)
+              x *= act_grad_t<ACT>(
+                  __bfloat162float(ep.xin[static_cast<size_t>(row) * ep.ld_xin + col]));
+            ep.d16[static_cast<size_t>(row) * ep.ld_d16 + col] = __float2bfloat16_rn(x);
+          } else {
+            x = ep.w_cur[static_cast<size_t>(row) * ep.ld_w32 + col] - ep.lr * x;
+            ep.w_new[static_cast<size_t>(row) * ep.ld_w32 + col] = x;
+            if (ep.w16) ep.w16[static_cast<size_t>(row) * ep.ld_w16 + col] = __float2bfloat16_rn(x);
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) {
+      win[rr] = wnx[rr];
+      xin[rr] = xnx[rr];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- split-K
+// Split-K for forward GEMMs whose tile count cannot fill the GPU (a
+// 128..256-row micro-batch forward of a 4096-wide layer has 32-64 tiles of
+// 128 x 128 for 148 SMs).  The S CTAs of one output tile form a thread-block
+// cluster (1, 1, S); each accumulates one K chunk in its TMEM.  After the
+// mainloop every CTA parks its fp32 partial in its own (now idle) operand
+// ring, the cluster synchronises, and CTA j finishes column block j of the
+// tile: it reads the S partials of its columns over DSMEM in split order,
+// sums them (deterministic) and runs the fused epilogue.  No global
+// workspace, no atomics, and the finishing work is spread over the S CTAs.
+constexpr int kMaxSplits = 4;
+
+template <int BN>
+struct SplitSmem {
+  static constexpr int kLd = BN + 4;  // +16 B per row: float4 row accesses are conflict-free
+  static constexpr int kBytes = 128 * kLd * 4;
+};
+
+// TMEM accumulator row (this thread's row) -> own smem partial.
+template <int BN>
+__device__ __forceinline__ void splitk_park(float* part, int r_local, uint32_t t_row) {
+  float* dst = part + r_local * SplitSmem<BN>::kLd;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    uint32_t r[16];
+    ptx::tmem_ld16(t_row + c, r);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      reinterpret_cast<float4*>(dst + c)[i] =
+          make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                      __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+  }
+}
+
+// Column block `rank` of the tile: sum the S partials of row r_local over
+// DSMEM (split order) and run the epilogue.
+template <int EPI, int ACT, int BN>
+__device__ __forceinline__ void splitk_reduce(const EpiParams& ep, const GemmShape& sh,
+                                              const float* part, int splits, int rank,
+                                              int row, int r_local, int n0) {
+  const int w = BN / splits;  // multiple of 16 (host: splits in {2, 4}, BN >= 128)
+  const int c0 = rank * w;
+  uint32_t src[kMaxSplits];
+#pragma unroll
+  for (int j = 0; j < kMaxSplits; ++j)
+    src[j] = j < splits ? ptx::map_to_rank(part + r_local * SplitSmem<BN>::kLd, j) : 0u;
+#pragma unroll 1
+  for (int c = c0; c < c0 + w; c += 16) {
+    const int n = n0 + c;
+    if (n >= sh.N) break;
+    float4 q[kMaxSplits][4];
+#pragma unroll
+    for (int j = 0; j < kMaxSplits; ++j)
+      if (j < splits)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[j][i] = ptx::ld_dsmem_f4(src[j] + (c + 4 * i) * 4);
     float v[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-    epilogue_chunk<EPI>(ep, sh, row, n, valid, v);
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxSplits; ++j)
+      if (j < splits)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          v[4 * i] += q[j][i].x;
+          v[4 * i + 1] += q[j][i].y;
+          v[4 * i + 2] += q[j][i].z;
+          v[4 * i + 3] += q[j][i].w;
+        }
+    if (row < sh.M) {
+      const int valid = sh.N - n < 16 ? sh.N - n : 16;
+      epilogue_chunk<EPI, ACT>(ep, sh, row, n, valid, v);
+    }
   }
 }
 
@@ -308,7 +658,11 @@ __global__ void __launch_bounds__(128, 1)
   const int lane = threadIdx.x % 32;
   const int m0 = blockIdx.y * Cfg::kBM;
   const int n0 = blockIdx.x * BN;
-  const int num_kb = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+  const int split = blockIdx.z;
+  const int kb_all = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+  const int kb_lo = sh.splits > 1 ? split * sh.kb_per_split : 0;
+  const int kb_hi = sh.splits > 1 ? min(kb_all, kb_lo + sh.kb_per_split) : kb_all;
+  const int num_kb = kb_hi - kb_lo;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmap_a);
@@ -332,7 +686,7 @@ __global__ void __launch_bounds__(128, 1)
       const int s = kb % S;
       if (kb >= S) ptx::mbar_wait(&empty_bar[s], ((kb / S) - 1) & 1);
       ptx::mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-      const int k0 = kb * Cfg::kBK;
+      const int k0 = (kb_lo + kb) * Cfg::kBK;
       uint8_t* a_dst = sA + s * Cfg::kABytes;
       uint8_t* b_dst = sB + s * Cfg::kBBytes;
       if constexpr (!A_MN) {
@@ -388,16 +742,39 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
 
   if (EPI == kEpiFwd || EPI == kEpiDgrad) {
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && ep.tag_src &&
+    if (blockIdx.x == 0 && blockIdx.y == 0 && split == 0 && threadIdx.x == 0 && ep.tag_src &&
         ep.tag_dst)
       write_tags(ep);
   }
   // the operand ring is idle now: reuse it for the per-warp transpose blocks
-  float* T = reinterpret_cast<float*>(sA) + warp * 32 * 33;
-  if (ep.rowwise)
-    epilogue_warp_rows<EPI>(ep, sh, m0 + warp * 32, n0, BN, t_row);
-  else
-    epilogue_warp_tile<EPI>(ep, sh, m0 + warp * 32, n0, BN, t_row, T);
+  float* T = reinterpret_cast<float*>(sA) + warp * 32 * kVecLd;
+  if (ep.dbg_skip & 1) {
+  } else if (EPI == kEpiFwd && sh.splits > 1) {
+    static_assert(SplitSmem<BN>::kBytes <= S * Cfg::kStageBytes, "partial must fit the ring");
+    float* part = reinterpret_cast<float*>(sA);
+    const int r_local = warp * 32 + lane;
+    splitk_park<BN>(part, r_local, t_row);
+    ptx::cluster_sync();  // every partial of the tile is parked
+    if constexpr (EPI == kEpiFwd)
+      with_act<EPI>(ep, [&](auto A) {
+        splitk_reduce<EPI, decltype(A)::value, BN>(ep, sh, part, sh.splits,
+                                                   static_cast<int>(ptx::cluster_ctarank()),
+                                                   m0 + r_local, r_local, n0);
+      });
+    ptx::cluster_sync();  // peers may still be reading this CTA's partial
+  } else if (ep.rowwise == 2) {
+    with_act<EPI>(ep, [&](auto A) {
+      epilogue_warp_vec<EPI, decltype(A)::value>(ep, sh, m0 + warp * 32, n0, BN, t_row, T);
+    });
+  } else if (ep.rowwise) {
+    with_act<EPI>(ep, [&](auto A) {
+      epilogue_warp_rows<EPI, decltype(A)::value>(ep, sh, m0 + warp * 32, n0, BN, t_row);
+    });
+  } else {
+    with_act<EPI>(ep, [&](auto A) {
+      epilogue_warp_tile<EPI, decltype(A)::value>(ep, sh, m0 + warp * 32, n0, BN, t_row, T);
+    });
+  }
 
   ptx::tc_fence_before();
   __syncthreads();
@@ -427,12 +804,13 @@ struct Gemm2Cfg {
   static constexpr int kAHalf = 128 * kBK * 2;         // this CTA's A rows
   static constexpr int kBHalf = (BN / 2) * kBK * 2;    // this CTA's B rows
   static constexpr int kStageBytes = kAHalf + kBHalf;
-  static constexpr int kStages = BN >= 256 ? 6 : 8;
+  static constexpr int kStages = BN >= 256 ? 5 : 7;
   static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  static constexpr int kEpiBytes = kEpiWarps * 32 * 33 * 4;  // per-warp transpose blocks
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 36 * 4;  // per-warp staging blocks
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 512;
   static constexpr uint32_t kTmemCols = 2 * BN;        // double-buffered accumulator
+  static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -463,7 +841,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
   const int tiles_m = (sh.M + 255) / 256;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
-  const int num_kb = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+  const int kb_all = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
+  constexpr int S_k = 1;  // the pair kernel never splits K
+  const int kbps = kb_all;
+  const int num_units = num_tiles;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmap_a);
@@ -488,11 +869,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs), completion on the leader's barrier
       int it = 0;
-      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+      for (int u = pair; u < num_units; u += num_pairs) {
+        const int tile = u / S_k, split = u % S_k;
         const int tm = tile / tiles_n, tn = tile % tiles_n;
         const int m0 = tm * 256 + static_cast<int>(rank) * 128;
         const int nb0 = tn * BN + static_cast<int>(rank) * (BN / 2);
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int kb_lo = split * kbps, kb_hi = min(kb_all, kb_lo + kbps);
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
           const int s = it % S;
           if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
           const uint32_t fb = ptx::map_to_rank(&full_bar[s], 0);
@@ -524,7 +907,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
       // ---------------- MMA issuer (leader only)
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
       int it = 0, local = 0;
-      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+      for (int u = pair; u < num_units; u += num_pairs, ++local) {
+        const int split = u % S_k;
+        const int num_kb = min(kb_all, (split + 1) * kbps) - split * kbps;
         const int acc = local & 1;
         const int use = local >> 1;
         ptx::mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
@@ -558,26 +943,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
     const int q = warp % 4;  // TMEM lane quarter this warp may access
     constexpr int kColsPerWarp = BN / (Cfg::kEpiWarps / 4);
     const int c_off = (e / 4) * kColsPerWarp;
-    float* T = epi_smem + e * 32 * 33;
+    float* T = epi_smem + e * 32 * kVecLd;
     const uint32_t tempty_leader_0 = ptx::map_to_rank(&tempty_bar[0], 0);
     const uint32_t tempty_leader_1 = ptx::map_to_rank(&tempty_bar[1], 0);
+    // SGD: each lane pulls one fp32 master row segment of this warp's part of
+    // a tile into L2 one tile ahead of its update (the first tile during the
+    // first mainloop), so the HBM-bound update reads at L2 latency.
+    // (dgrad: the stored activations that gate the delta, likewise.)
+    auto prefetch_master = [&](int u) {
+      if (u >= num_units) return;
+      const int t = u / S_k;
+      const int row = (t / tiles_n) * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const int n0 = (t % tiles_n) * BN + c_off;
+      const int cols = min(kColsPerWarp, sh.N - n0);
+      if (row >= sh.M || cols <= 0) return;
+      if constexpr (EPI == kEpiWgradSgd) {
+        const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;
+        if (bytes > 0 && (ep.ld_w32 % 4) == 0)
+          ptx::prefetch_l2(ep.w_cur + static_cast<size_t>(row) * ep.ld_w32 + n0, bytes);
+      } else if constexpr (EPI == kEpiDgrad) {
+        const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
+        if (ep.act_prev != kLinear && bytes > 0 && (ep.ld_xin % 8) == 0)
+          ptx::prefetch_l2(ep.xin + static_cast<size_t>(row) * ep.ld_xin + n0, bytes);
+      }
+    };
+    prefetch_master(pair);
     int local = 0;
-    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++local) {
+    for (int u = pair; u < num_units; u += num_pairs, ++local) {
+      const int tile = u / S_k, split = u % S_k;
       const int acc = local & 1;
       const int use = local >> 1;
       const int tm = tile / tiles_n, tn = tile % tiles_n;
+      prefetch_master(u + num_pairs);
       ptx::mbar_wait(&tfull_bar[acc], use & 1);
       ptx::tc_fence_after();
       const int row_base = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
       const uint32_t t_row =
           tmem_base + acc * BN + c_off + (static_cast<uint32_t>(q * 32) << 16);
-      if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && rank == 0 && e == 0 &&
-          lane == 0 && ep.tag_src && ep.tag_dst)
+      if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && split == 0 && rank == 0 &&
+          e == 0 && lane == 0 && ep.tag_src && ep.tag_dst)
         write_tags(ep);
-      if (ep.rowwise)
-        epilogue_warp_rows<EPI>(ep, sh, row_base, tn * BN + c_off, kColsPerWarp, t_row);
-      else
-        epilogue_warp_tile<EPI>(ep, sh, row_base, tn * BN + c_off, kColsPerWarp, t_row, T);
+      if (ep.dbg_skip & 1) {
+      } else if (ep.rowwise == 2) {
+        with_act<EPI>(ep, [&](auto A) {
+          epilogue_warp_vec<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+                                                     kColsPerWarp, t_row, T);
+        });
+      } else if (ep.rowwise) {
+        with_act<EPI>(ep, [&](auto A) {
+          epilogue_warp_rows<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+                                                      kColsPerWarp, t_row);
+        });
+      } else {
+        with_act<EPI>(ep, [&](auto A) {
+          epilogue_warp_tile<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+                                                      kColsPerWarp, t_row, T);
+        });
+      }
       ptx::tc_fence_before();
       ptx::named_bar_sync(1, 32 * Cfg::kEpiWarps);
       if (e == 0 && lane == 0)

@@ -14,6 +14,10 @@ struct GemmShape {
   int M, N, K;
   int a_mn_off, a_k_off;
   int b_mn_off, b_k_off;
+  // split-K (forward, single-CTA kernel): the K range is cut into `splits`
+  // chunks of kb_per_split 64-wide k-blocks, one CTA of a (1,1,splits)
+  // cluster each (0/1 = no split); see gemm_sm100.cuh.
+  int splits, kb_per_split;
 };
 
 struct EpiParams {
@@ -45,8 +49,10 @@ struct EpiParams {
   int tag_count;   // entries written (a coalesced forward covers several micro-batches)
   int tag_stride;  // element stride between entries
   // epilogue access pattern: 0 = transposed (coalesced rows, lane = column),
-  // 1 = row-per-thread vectors
+  // 1 = row-per-thread vectors, 2 = staged transpose with 16/8-byte vectors
   int rowwise;
+  // timing experiments: nonzero skips the epilogue's global traffic
+  int dbg_skip;
 };
 
 }  // namespace pb

@@ -96,13 +96,32 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>;
     constexpr int smem = Gemm2Cfg<BN>::kSmem;
     const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
-    const int pairs = std::min(tiles, std::max(1, sm_count() / 2));
+    int cap = sm_count() / 2;
+    if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
+    const int pairs = std::min(tiles, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
   } else {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
     constexpr int smem = GemmCfg<BN>::kSmem;
-    dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128);
-    kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+    const int splits = std::max(1, g.sh.splits);
+    dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128, splits);
+    if (splits > 1) {  // the splits of a tile are one cluster (DSMEM reduction)
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(128);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = splits;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep));
+    } else {
+      kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+    }
   }
   PB_CUDA(cudaGetLastError());
 }
@@ -136,13 +155,15 @@ void init_gemm_attributes() {
     set_attr<256, false, true, kEpiDgrad>();
     set_attr<128, true, true, kEpiWgradSgd>();
     set_attr<256, true, true, kEpiWgradSgd>();
+    set_attr<128, false, false, kEpiWgradSgd>();
+    set_attr<256, false, false, kEpiWgradSgd>();
   });
 }
 
 namespace {
 
-// PIPESIM_EPI=rows|tile|auto (default auto: row-per-thread vectors for the
-// bf16 epilogues, transposed coalesced rows for the fp32 SGD update).
+// PIPESIM_EPI=rows|tile|vec (default vec: staged transpose, 16/8-byte
+// vectors, 4 row segments per warp instruction; see gemm_sm100.cuh).
 int epi_mode() {
   static const int m = [] {
     const char* e = std::getenv("PIPESIM_EPI");
@@ -153,11 +174,43 @@ int epi_mode() {
   return m;
 }
 
+// PIPESIM_DBG_EPI=1: epilogues skip all global traffic (timing experiments
+// only: results are garbage).
+int dbg_skip() {
+  static const int v = [] {
+    const char* e = std::getenv("PIPESIM_DBG_EPI");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 EpiParams empty_epi(int kind) {
   EpiParams e{};
   const int m = epi_mode();
-  e.rowwise = m == 2 ? (kind == kEpiWgradSgd ? 0 : 1) : m;
+  e.rowwise = m;
+  e.dbg_skip = dbg_skip();
   return e;
+}
+
+// The vector epilogue (mode 2) needs 16-byte fp32 rows and 8-byte bf16 rows;
+// other layouts fall back to the scalar transposed (SGD) / row-per-thread
+// (bf16 outputs) epilogues.
+bool al(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+void vec_or_fallback(EpiParams& e, int kind) {
+  if (e.rowwise != 2) return;
+  bool ok = true;
+  if (kind == kEpiFwd) {
+    if (e.y16) ok = ok && e.ld_y16 % 4 == 0 && al(e.y16, 8);
+    if (e.y32) ok = ok && e.ld_y32 % 4 == 0 && al(e.y32, 16);
+    if (e.bias) ok = ok && al(e.bias, 16);
+  } else if (kind == kEpiDgrad) {
+    ok = e.ld_d16 % 4 == 0 && al(e.d16, 8);
+    if (e.act_prev != kLinear) ok = ok && e.ld_xin % 4 == 0 && al(e.xin, 8);
+  } else {
+    ok = e.ld_w32 % 4 == 0 && al(e.w_cur, 16) && al(e.w_new, 16);
+    if (e.w16) ok = ok && e.ld_w16 % 4 == 0 && al(e.w16, 8);
+  }
+  if (!ok) e.rowwise = kind == kEpiWgradSgd ? 0 : 1;
 }
 
 // B-operand box rows for a K-major B: the pair kernel loads half a tile.
@@ -165,15 +218,51 @@ int b_box(const GemmLaunch& g) { return g.pair ? g.bn / 2 : g.bn; }
 
 }  // namespace
 
+// PIPESIM_SPLITK=0 disables split-K, =<n> forces n splits (A/B runs).
+namespace {
+int splitk_env() {
+  static const int v = [] {
+    const char* e = std::getenv("PIPESIM_SPLITK");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+}  // namespace
+
+// Split-K for skinny forwards (<= 256 rows): enough 128 x 128 tiles x splits
+// to cover the SMs, >= 8 k-blocks per split, at most kMaxSplits (4).
+// PIPESIM_SPLITK=0 disables it, =<n> forces n (A/B runs).
+int fwd_splits(int rows, int N, int K) {
+  if (rows > 256 || splitk_env() == 0 || !pair_allowed()) return 1;
+  const int kb = (K + 63) / 64;
+  const int tiles = ((rows + 127) / 128) * ((N + 127) / 128);
+  int s = std::max(1, sm_count() / tiles);
+  if (splitk_env() > 0) s = splitk_env();
+  s = std::min(s, std::min(4, kb / 8));
+  if (s == 3) s = 2;  // column blocks of the reduction: 128 / s, a multiple of 16
+  return std::max(1, s);
+}
+
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
-                    float* y32, int ld_y32, int y_row_off) {
+                    float* y32, int ld_y32, int y_row_off, bool allow_split) {
   GemmLaunch g;
-  g.bn = pick_bn(rows, w.rows);
-  g.pair = use_pair(rows);
+  const int splits = allow_split || splitk_env() > 0 ? fwd_splits(rows, w.rows, x.cols) : 1;
+  if (splits > 1) {  // single-CTA 128 x 128 tiles, one cluster of `splits` per tile
+    g.bn = 128;
+    g.pair = false;
+  } else {
+    g.bn = pick_bn(rows, w.rows);
+    g.pair = use_pair(rows);
+  }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
-  g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0};
+  g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0, 1, 0};
+  if (splits > 1) {
+    const int kb = (x.cols + 63) / 64;
+    g.sh.kb_per_split = (kb + splits - 1) / splits;
+    g.sh.splits = (kb + g.sh.kb_per_split - 1) / g.sh.kb_per_split;
+  }
   g.ep = empty_epi(kEpiFwd);
   g.ep.bias = bias;
   g.ep.act = act;
@@ -182,6 +271,7 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
   g.ep.y32 = y32;
   g.ep.ld_y32 = ld_y32;
   g.ep.y_row_off = y_row_off;
+  vec_or_fallback(g.ep, kEpiFwd);
   return g;
 }
 
@@ -199,6 +289,7 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
   g.ep.act_prev = act_prev;
   g.ep.d16 = d;
   g.ep.ld_d16 = ld_d;
+  vec_or_fallback(g.ep, kEpiDgrad);
   return g;
 }
 
@@ -211,6 +302,14 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
   g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};
+  if (const char* e = std::getenv("PIPESIM_EXP_WG"); e && std::string(e) == "kk" &&
+      dz.ld == dz.cols && x.ld == x.cols && x_row_off == 0) {
+    // same bytes reinterpreted as K-major [features][rows] (garbage math)
+    g.exp_kk = true;
+    g.ta = make_operand_tmap(Mat16{dz.ptr, dz.cols, dz.rows, dz.rows}, true, 128);
+    g.tb = make_operand_tmap(Mat16{x.ptr, x.cols, x.rows, x.rows}, true, b_box(g));
+    g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, 0};
+  }
   g.ep = empty_epi(kEpiWgradSgd);
   g.ep.w_cur = w_cur;
   g.ep.w_new = w_new;
@@ -218,6 +317,7 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
   g.ep.w16 = w16;
   g.ep.ld_w16 = ld_w16;
   g.ep.lr = lr;
+  vec_or_fallback(g.ep, kEpiWgradSgd);
   return g;
 }
 
@@ -228,6 +328,10 @@ void launch_dgrad(const GemmLaunch& g, cudaStream_t st) {
   launch_bn<false, true, kEpiDgrad>(g, st);
 }
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
+  if (g.exp_kk) {  // timing experiment (PIPESIM_EXP_WG=kk): K-major operands
+    launch_bn<false, false, kEpiWgradSgd>(g, st);
+    return;
+  }
   launch_bn<true, true, kEpiWgradSgd>(g, st);
 }
 

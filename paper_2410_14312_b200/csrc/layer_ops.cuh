@@ -33,12 +33,19 @@ struct GemmLaunch {
   EpiParams ep;
   int bn;
   bool pair = false;  // persistent CTA-pair kernel
+  bool exp_kk = false;  // timing experiment only
 };
+
+// Split count of a forward GEMM of rows x N x K (1 = no split).  Splitting
+// cuts a skinny forward's latency but spends more SM-time per flop, so an
+// executor that keeps many stages in flight on one GPU turns it off
+// (plan_fwd's allow_split).
+int fwd_splits(int rows, int N, int K);
 
 // forward: out = act(x[rows, in] * w[out, in]^T + b)
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
-                    float* y32, int ld_y32, int y_row_off);
+                    float* y32, int ld_y32, int y_row_off, bool allow_split = true);
 // dgrad: d[rows, in] = (dz[rows,out] * w[out,in]) .* act'(xin)
 GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
                       int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d);

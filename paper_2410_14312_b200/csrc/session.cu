@@ -98,7 +98,7 @@ struct Session::Impl {
   };
 
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
-                      send, recv };
+                      send, recv, mark };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
@@ -167,6 +167,10 @@ struct Session::Impl {
   int W_lo = 1, W_hi = 0;  // local stage range (1-based, inclusive)
   int rank = 0, world = 1;
   std::vector<int> owner;  // [stage 0-based] -> rank
+  // profiling: node metadata (issue order) and its begin/end timing events
+  std::vector<NodeTiming> node_meta;
+  std::vector<cudaEvent_t> mark_ev;  // [2 * nodes], created on first profile
+  bool profiling = false;
   std::unique_ptr<P2P> p2p;
   cudaStream_t comm[4] = {nullptr, nullptr, nullptr, nullptr};  // fwd send/recv, bwd send/recv
   bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
@@ -190,6 +194,8 @@ struct Session::Impl {
   }
 
   ~Impl() {
+    for (cudaEvent_t e : mark_ev)
+      if (e) cudaEventDestroy(e);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (!plan_only)
@@ -735,6 +741,15 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         wait_on(s, record_on(Impl::kBwdRecv));
       }
     }
+    const int node_idx = static_cast<int>(I.node_meta.size());
+    I.node_meta.push_back(NodeTiming{s + 1, node.fwd ? 1 : 0, node.k, node.fwd ? node.jj0 : 0,
+                                     node.fwd ? node.jj1 : 0, 0.f, 0.f});
+    {
+      Impl::Op mk{OK::mark};
+      mk.stream = s;
+      mk.value = 2 * node_idx;
+      push(mk);
+    }
     if (node.fwd) {
       const Impl::PoolSlot& ps = st.pool[st.version_colour[tk.version]];
       const int r0 = node.jj0 * I.Rm;
@@ -755,7 +770,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         if (!c.plan_only)
         o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
-                       logits ? as.out32 : nullptr, I.n_out, r0);
+                       logits ? as.out32 : nullptr, I.n_out, r0,
+                       /*allow_split=*/I.W_hi - I.W_lo + 1 <= 2);
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
           o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
@@ -892,6 +908,12 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     r.ev = I.new_event();
     node.done = r.ev;
     push(r);
+    {
+      Impl::Op mk{OK::mark};
+      mk.stream = s;
+      mk.value = 2 * node_idx + 1;
+      push(mk);
+    }
     // outgoing cross-GPU edges of this node
     if (node.fwd && s + 1 < W && !I.local(s + 1)) {
       const auto& ll = st.layers.back();
@@ -1129,6 +1151,9 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::recv:
         I.p2p->recv(o.dst, o.bytes, o.peer, o.dir, s);
         break;
+      case OK::mark:
+        if (I.profiling) PB_CUDA(cudaEventRecord(I.mark_ev[o.value], s));
+        break;
     }
   }
   for (size_t i = 0; i < streams.size(); ++i) {
@@ -1162,7 +1187,46 @@ EpochResult Session::run_epoch() {
   }
   PB_CUDA(cudaEventRecord(I.t1, I.origin));
   PB_CUDA(cudaEventSynchronize(I.t1));
+  return collect_result();
+}
 
+EpochResult Session::profile_epoch(EpochProfile* prof) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  if (I.mark_ev.empty()) {
+    I.mark_ev.assign(2 * I.node_meta.size(), nullptr);
+    for (cudaEvent_t& e : I.mark_ev) PB_CUDA(cudaEventCreate(&e));
+  }
+  PB_CUDA(cudaEventRecord(I.t0, I.origin));
+  I.profiling = true;
+  try {
+    issue(I, I.origin);
+  } catch (...) {
+    I.profiling = false;
+    throw;
+  }
+  I.profiling = false;
+  PB_CUDA(cudaEventRecord(I.t1, I.origin));
+  PB_CUDA(cudaEventSynchronize(I.t1));
+  EpochResult r = collect_result();
+  if (prof) {
+    prof->makespan_ms = r.device_ms;
+    prof->busy_ms.assign(cfg_.W, -1.f);
+    for (int s = 0; s < cfg_.W; ++s)
+      if (I.local(s)) prof->busy_ms[s] = 0.f;
+    prof->nodes = I.node_meta;
+    for (size_t i = 0; i < prof->nodes.size(); ++i) {
+      NodeTiming& n = prof->nodes[i];
+      PB_CUDA(cudaEventElapsedTime(&n.start_ms, I.t0, I.mark_ev[2 * i]));
+      PB_CUDA(cudaEventElapsedTime(&n.end_ms, I.t0, I.mark_ev[2 * i + 1]));
+      prof->busy_ms[n.stage - 1] += n.end_ms - n.start_ms;
+    }
+  }
+  return r;
+}
+
+EpochResult Session::collect_result() {
+  Impl& I = *impl_;
   EpochResult r;
   PB_CUDA(cudaEventElapsedTime(&r.device_ms, I.t0, I.t1));
   const int M = cfg_.M, U = I.U, W = cfg_.W, B = cfg_.B;

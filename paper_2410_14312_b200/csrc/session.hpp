@@ -79,6 +79,22 @@ struct EpochResult {
   float device_ms = 0.f;          // graph/stream time of the epoch
 };
 
+// Per-node device timeline of one epoch (profile_epoch): a node is one
+// backward task or one coalesced run of forward tasks of a stage.
+struct NodeTiming {
+  int stage;           // 1-based
+  int fwd;             // 1 forward run, 0 backward
+  int mini;            // k
+  int micro_lo, micro_hi;  // forward micro-batch range (0-based), 0/0 for backward
+  float start_ms, end_ms;  // from the epoch start, after the node's cross-stage waits
+};
+
+struct EpochProfile {
+  float makespan_ms = 0.f;
+  std::vector<float> busy_ms;  // [W]: sum of node spans per stage (-1: other GPU)
+  std::vector<NodeTiming> nodes;
+};
+
 class Session {
  public:
   explicit Session(const SessionConfig& cfg);
@@ -108,6 +124,10 @@ class Session {
               cudaStream_t st = nullptr);
   // Runs one epoch on the uploaded data.  `epoch` only tags the result.
   EpochResult run_epoch();
+  // Runs one epoch without the CUDA graph, with timing events around every
+  // node on its stage stream: per-stage busy time, the epoch makespan and
+  // the node timeline (pipeline bubble = 1 - sum(busy) / (W * makespan)).
+  EpochResult profile_epoch(EpochProfile* prof);
 
   // Ledger / plan of the session (for logs and checks).
   const pipesim::version_ledger& ledger() const { return ledger_; }
@@ -122,6 +142,7 @@ class Session {
   struct Impl;  // public so the program-issue helpers can see it
 
  private:
+  EpochResult collect_result();
   SessionConfig cfg_;
   std::unique_ptr<Impl> impl_;
   std::unique_ptr<pipesim::schedule_grid> grid_;

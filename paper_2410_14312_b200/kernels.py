@@ -71,3 +71,33 @@ def loss_fwd_bwd(y, t, loss, act_last, denom, dz, row_loss):
     _native.check(_native.lib().pb_loss_fwd_bwd(
         _stream(), _ptr(y), rows, cols, _ld(y), _ptr(t), _ld(t), LOSS[loss],
         ACT[act_last], float(denom), _ptr(dz), _ld(dz), _ptr(row_loss)))
+
+
+def graph_time_us(fns, reps: int = 60) -> float:
+    """Device time per call of a kernel launch, cycling through `fns` (e.g.
+    closures over several operand copies, so that operands larger than L2 are
+    re-read from HBM as inside the pipeline).  The calls are captured in one
+    CUDA graph, so the per-call host cost of the C ABI path is excluded, then
+    replayed after a warm-up and timed with CUDA events on the stream."""
+    if callable(fns):
+        fns = [fns]
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):  # warm-up on the capture stream (per-stream workspaces)
+        for f in fns:
+            f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(reps):
+            fns[i % len(fns)]()
+    g.replay()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()  # replay (and the events) run here
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    g.replay()
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) * 1000.0 / reps

@@ -656,6 +656,42 @@ class Session:
         N.check(_L().pb_session_upload(self._h, x.ctypes.data, self._dtype(x), y.ctypes.data,
                                        self._dtype(y, y_labels)))
 
+    def profile_epoch(self, max_nodes: int = 1 << 16):
+        """One epoch without the CUDA graph, timed per node on the stage
+        streams (the native path, with timing events).  Returns run_epoch's
+        dict plus `profile`: makespan_ms, per-stage busy_ms, the node timeline
+        and bubble = 1 - sum(busy) / (W * makespan) over this GPU's stages."""
+        from ._session_abi import pb_epoch_profile
+        M, U, W = self.M, self.units, self.W
+        r = dict(mini_loss=np.zeros(M), pinned=np.zeros(M * U, np.int32),
+                 consumed=np.zeros(M, np.int32), dev_fwd=np.zeros(M * U * W, np.int32),
+                 dev_bwd=np.zeros(M * W, np.int32), dev_current=np.zeros(W, np.int32))
+        out = pb_epoch_out(_dp(r["mini_loss"]), _ip(r["pinned"]), _ip(r["consumed"]),
+                           _ip(r["dev_fwd"]), _ip(r["dev_bwd"]), _ip(r["dev_current"]), 0.0)
+        busy = np.zeros(W, np.float32)
+        cols = {k: np.zeros(max_nodes, np.int32) for k in ("stage", "fwd", "mini", "lo", "hi")}
+        t0 = np.zeros(max_nodes, np.float32)
+        t1 = np.zeros(max_nodes, np.float32)
+        fp = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+        prof = pb_epoch_profile(0.0, fp(busy), max_nodes, 0, _ip(cols["stage"]),
+                                _ip(cols["fwd"]), _ip(cols["mini"]), _ip(cols["lo"]),
+                                _ip(cols["hi"]), fp(t0), fp(t1))
+        N.check(_L().pb_session_profile_epoch(self._h, C.byref(out), C.byref(prof)))
+        r["device_ms"] = out.device_ms
+        r["pinned"] = r["pinned"].reshape(M, U)
+        r["dev_fwd"] = r["dev_fwd"].reshape(M, U, W)
+        r["dev_bwd"] = r["dev_bwd"].reshape(M, W)
+        n = min(prof.n_nodes, max_nodes)
+        local = busy >= 0
+        mk = float(prof.makespan_ms)
+        r["profile"] = dict(
+            makespan_ms=mk, busy_ms=busy.tolist(),
+            bubble=float(1.0 - busy[local].sum() / (local.sum() * mk)) if mk > 0 else None,
+            nodes=[dict(stage=int(cols["stage"][i]), fwd=bool(cols["fwd"][i]),
+                        mini=int(cols["mini"][i]), micro=(int(cols["lo"][i]), int(cols["hi"][i])),
+                        start_ms=float(t0[i]), end_ms=float(t1[i])) for i in range(n)])
+        return r
+
     def run_epoch(self):
         M, U, W = self.M, self.units, self.W
         r = dict(mini_loss=np.zeros(M), pinned=np.zeros(M * U, np.int32),

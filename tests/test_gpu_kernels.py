@@ -36,6 +36,8 @@ def _rel(got, want):
 FWD_SHAPES = [
     (128, 256, 128), (64, 784, 512), (64, 512, 256), (64, 256, 10), (5, 2, 8),
     (200, 100, 10), (256, 4096, 4096), (128, 4096, 4096), (1000, 136, 392),
+    # split-K shapes (K >= 1024): ragged N, ragged last split, partial M tiles
+    (1024, 4096, 4096), (512, 1024, 1536), (384, 2048, 1000), (100, 3000, 700),
 ]
 
 
@@ -150,3 +152,25 @@ def test_loss(loss, rows, cols):
         ref_g = (torch.softmax(yd, 1) - td) / denom
     assert torch.allclose(rl.double(), ref_rl, rtol=1e-5, atol=1e-5)
     assert _rel(dz, ref_g) < 2 ** -8
+
+
+@pytest.mark.parametrize("rows,inn,out", [(128, 4096, 4096), (256, 4096, 4096), (64, 3000, 700),
+                                          (200, 2048, 1000), (128, 1024, 136)])
+def test_split_k_cluster_forward_deterministic(rows, inn, out):
+    """Split-K forwards (one thread-block cluster per tile, DSMEM reduction in
+    split order): repeated launches give identical bits, and the result
+    matches the fp32 reference at the GEMM tolerance."""
+    x = K.padded_bf16(rows, inn)
+    x.copy_(torch.rand(rows, inn, device="cuda"))
+    w = K.padded_bf16(out, inn)
+    w.copy_((torch.rand(out, inn, device="cuda") * 2 - 1) / inn ** 0.5)
+    b = (torch.rand(out, device="cuda") - 0.5)
+    ys = []
+    for _ in range(3):
+        y = torch.zeros(rows, out, device="cuda")
+        K.linear_fwd(x, w, b, "relu", y32=y)
+        ys.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    ref = torch.relu(x.float() @ w.float().T + b)
+    assert _rel(ys[0], ref) < 2e-5

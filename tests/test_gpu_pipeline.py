@@ -233,7 +233,8 @@ def test_session_resident_epochs_and_labels():
 @pytest.mark.parametrize("mode", ["timeprest", "pipedream"])
 def test_forward_coalescing_is_bit_identical(mode):
     """Coalesced forwards (one GEMM over consecutive micro-batches with the same
-    pinned version) must reproduce per-micro-batch launches bit for bit."""
+    pinned version) must reproduce per-micro-batch launches bit for bit when
+    no layer splits K (K < 512 here: GEMM rows are independent)."""
     net = P.NetworkSpec([256] * 9, ["relu"] * 7 + ["linear"], "softmax_cross_entropy")
     p0 = P.init_network_params(net, 1)
     x, lab = P.make_classification_task(6 * 512, 256, 256, seed=7, as_labels=True,
@@ -249,3 +250,26 @@ def test_forward_coalescing_is_bit_identical(mode):
     for other in res[1:]:
         for a, b in zip(res[0], other):
             np.testing.assert_array_equal(a, b)
+
+
+def test_forward_coalescing_with_split_k():
+    """At widths where skinny forwards split K (a 128-row forward of a
+    1024-wide layer runs as clusters of K chunks, a 512-row one does not),
+    coalescing only reorders fp32 sums: losses and weights agree to fp32
+    rounding, and version traces stay exact."""
+    net = P.NetworkSpec([1024] * 5, ["relu"] * 3 + ["linear"], "softmax_cross_entropy")
+    p0 = P.init_network_params(net, 1)
+    x, lab = P.make_classification_task(6 * 512, 1024, 1024, seed=7, as_labels=True,
+                                        dtype=np.float32)
+    res = []
+    for merge in (1, 0):
+        s = P.Session(net, 2, 4, 512, 6, 0.05, "timeprest", fwd_merge=merge)
+        s.load_params(p0)
+        s.upload(x, lab, y_labels=True)
+        r = s.run_epoch()
+        res.append((r["mini_loss"], r["dev_fwd"], s.read_params()))
+        s.close()
+    np.testing.assert_allclose(res[0][0], res[1][0], rtol=1e-4)
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    d = np.linalg.norm(res[0][2] - res[1][2]) / np.linalg.norm(res[1][2])
+    assert d < 1e-4
