@@ -640,7 +640,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b, GemmShape sh,
-                      EpiParams ep) {
+                      EpiParams ep, const __grid_constant__ EpiMaps maps) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -784,6 +784,80 @@ __global__ void __launch_bounds__(128, 1)
   }
 }
 
+// TMA epilogue of wgrad + SGD (pair kernel): one warp updates its 32 rows x
+// n_cols of the tile in 32 x 32 chunks.  The fp32 master chunk arrives by
+// TMA (128-byte swizzle) one chunk ahead; each thread updates its own row in
+// place in shared memory (the swizzle makes the row-per-thread 16-byte
+// accesses conflict-free), writes the bf16 copy to a 64-byte-swizzled tile,
+// and one lane stores both tiles with TMA.  Loads and stores are bulk and
+// asynchronous: the update never waits for a global store, and out-of-range
+// rows / columns are clipped by the tensor maps.
+struct SgdTmaState {
+  int g = 0;                  // chunks processed by this warp so far
+  uint32_t phase[2] = {0, 0};
+};
+
+__device__ __forceinline__ void sgd_tma_load(const EpiMaps& maps, uint8_t* buf32, uint64_t* bar,
+                                             int col, int row) {
+  ptx::mbar_arrive_expect_tx(bar, 4096);
+  ptx::tma_load_2d(buf32, &maps.w_cur, bar, col, row);
+}
+
+__device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const EpiMaps& maps,
+                                                      int row_base, int n_base, int n_cols,
+                                                      uint32_t t_row, uint8_t* wbuf,
+                                                      uint64_t* bars, SgdTmaState& st,
+                                                      bool first_tile, int next_row,
+                                                      int next_col) {
+  const int lane = threadIdx.x % 32;
+  uint8_t* b32[2] = {wbuf, wbuf + 4096};
+  uint8_t* b16[2] = {wbuf + 8192, wbuf + 8192 + 2048};
+  if (first_tile && lane == 0) sgd_tma_load(maps, b32[st.g & 1], &bars[st.g & 1], n_base, row_base);
+#pragma unroll 1
+  for (int c = 0; c < n_cols; c += 32) {
+    const int b = st.g & 1;
+    if (lane == 0) {
+      // buffer b^1 was last stored from two chunks ago; once that store has
+      // read it, prefetch the next chunk (this tile's, or the next tile's
+      // first) into it
+      ptx::bulk_wait_group_read<0>();
+      if (c + 32 < n_cols)
+        sgd_tma_load(maps, b32[b ^ 1], &bars[b ^ 1], n_base + c + 32, row_base);
+      else if (next_row >= 0)
+        sgd_tma_load(maps, b32[b ^ 1], &bars[b ^ 1], next_col, next_row);
+    }
+    uint32_t r[32];
+    ptx::tmem_ld32(t_row + c, r);
+    ptx::mbar_wait(&bars[b], st.phase[b]);
+    st.phase[b] ^= 1;
+    ptx::tmem_ld_wait();
+    uint8_t* row32 = b32[b] + lane * 128;
+    uint8_t* row16 = b16[b] + lane * 64;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4* p = reinterpret_cast<float4*>(row32 + ((j ^ (lane & 7)) << 4));
+      float4 w = *p;
+      w.x -= ep.lr * __uint_as_float(r[4 * j]);
+      w.y -= ep.lr * __uint_as_float(r[4 * j + 1]);
+      w.z -= ep.lr * __uint_as_float(r[4 * j + 2]);
+      w.w -= ep.lr * __uint_as_float(r[4 * j + 3]);
+      *p = w;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(w.z, w.w);
+      *reinterpret_cast<uint2*>(row16 + (((j >> 1) ^ ((lane >> 1) & 3)) << 4) + (j & 1) * 8) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+    }
+    ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA store
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(&maps.w_new, b32[b], n_base + c, row_base);
+      if (ep.has_w16) ptx::tma_store_2d(&maps.w16, b16[b], n_base + c, row_base);
+      ptx::bulk_commit_group();
+    }
+    ++st.g;
+  }
+}
+
 // ===========================================================================
 // Persistent CTA-pair kernel (cta_group::2).
 //
@@ -798,27 +872,34 @@ __global__ void __launch_bounds__(128, 1)
 //
 // Warps: 0 TMA producer (both CTAs), 1 MMA issuer (leader) + TMEM owner,
 //        2..5 epilogue (TMEM lanes 32*(warp%4) .. +32).
-template <int BN>
+template <int BN, int EPI>
 struct Gemm2Cfg {
   static constexpr int kBK = 64;
   static constexpr int kAHalf = 128 * kBK * 2;         // this CTA's A rows
   static constexpr int kBHalf = (BN / 2) * kBK * 2;    // this CTA's B rows
   static constexpr int kStageBytes = kAHalf + kBHalf;
-  static constexpr int kStages = BN >= 256 ? 5 : 7;
+  // wgrad tiles are short in K (one mini-batch): 4 stages leave room for the
+  // TMA epilogue's double-buffered master tiles
+  static constexpr int kStages = EPI == kEpiWgradSgd ? 4 : (BN >= 256 ? 5 : 7);
   static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  static constexpr int kEpiBytes = kEpiWarps * 32 * 36 * 4;  // per-warp staging blocks
-  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 512;
+  // per epilogue warp: staging block (vector epilogue) or, for SGD, 2 x (fp32
+  // 32x32 master tile 4 KB + bf16 32x32 tile 2 KB) for the TMA epilogue
+  static constexpr int kSgdWarpBytes = 2 * (4096 + 2048);
+  static constexpr int kEpiBytes = EPI == kEpiWgradSgd ? kEpiWarps * kSgdWarpBytes
+                                                       : kEpiWarps * 32 * 36 * 4;
+  static constexpr int kBarOff = kStages * kStageBytes + kEpiBytes;
+  static constexpr int kSmem = kBarOff + 512 + 1024;
   static constexpr uint32_t kTmemCols = 2 * BN;        // double-buffered accumulator
   static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a,
                            const __grid_constant__ CUtensorMap tmap_b, GemmShape sh,
-                           EpiParams ep) {
-  using Cfg = Gemm2Cfg<BN>;
+                           EpiParams ep, const __grid_constant__ EpiMaps maps) {
+  using Cfg = Gemm2Cfg<BN, EPI>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the shared array
@@ -826,12 +907,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kAHalf;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* epi_base = smem + S * Cfg::kStageBytes;  // 1024-aligned
+  float* epi_smem = reinterpret_cast<float*>(epi_base);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kBarOff);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's are used)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  float* epi_smem = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + 512);
+  uint64_t* sgd_bar = tempty_bar + 2;    // [2 per epilogue warp] (TMA SGD epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 2 * Cfg::kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -857,6 +940,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], 2);  // one arrival per CTA of the pair
     }
+    if constexpr (EPI == kEpiWgradSgd)
+      if (ep.rowwise == 3) {
+        for (int i = 0; i < 2 * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
+        ptx::tma_prefetch_desc(&maps.w_cur);
+        ptx::tma_prefetch_desc(&maps.w_new);
+        if (ep.has_w16) ptx::tma_prefetch_desc(&maps.w16);
+      }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
@@ -968,6 +1058,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
       }
     };
     prefetch_master(pair);
+    SgdTmaState sgd_st;
+    uint8_t* sgd_buf = epi_base + e * Cfg::kSgdWarpBytes;
     int local = 0;
     for (int u = pair; u < num_units; u += num_pairs, ++local) {
       const int tile = u / S_k, split = u % S_k;
@@ -984,6 +1076,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
           e == 0 && lane == 0 && ep.tag_src && ep.tag_dst)
         write_tags(ep);
       if (ep.dbg_skip & 1) {
+      } else if (EPI == kEpiWgradSgd && ep.rowwise == 3) {
+        if constexpr (EPI == kEpiWgradSgd) {
+          int next_row = -1, next_col = 0;
+          if (u + num_pairs < num_units) {
+            const int nt = (u + num_pairs) / S_k;
+            next_row = (nt / tiles_n) * 256 + static_cast<int>(rank) * 128 + q * 32;
+            next_col = (nt % tiles_n) * BN + c_off;
+          }
+          epilogue_warp_tma_sgd(ep, maps, row_base, tn * BN + c_off, kColsPerWarp, t_row,
+                                sgd_buf, sgd_bar + 2 * e, sgd_st, local == 0, next_row,
+                                next_col);
+        }
       } else if (ep.rowwise == 2) {
         with_act<EPI>(ep, [&](auto A) {
           epilogue_warp_vec<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
@@ -1005,6 +1109,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN>::kThrea
       if (e == 0 && lane == 0)
         ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader_0 : tempty_leader_1);
     }
+    if (EPI == kEpiWgradSgd && ep.rowwise == 3 && lane == 0)
+      ptx::bulk_wait_group<0>();  // the last TMA stores have landed
   }
 
   __syncwarp();

@@ -1,6 +1,7 @@
 // Plain (host-compilable) parameter types of the layer GEMMs.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 namespace pb {
@@ -18,6 +19,13 @@ struct GemmShape {
   // chunks of kb_per_split 64-wide k-blocks, one CTA of a (1,1,splits)
   // cluster each (0/1 = no split); see gemm_sm100.cuh.
   int splits, kb_per_split;
+};
+
+// Tensor maps of the TMA epilogue of wgrad+SGD (EpiParams::rowwise == 3):
+// fp32 masters (current / new; box 32 x 32, 128-byte swizzle) and the bf16
+// weights of the new version (box 32 x 32, 64-byte swizzle).
+struct alignas(64) EpiMaps {
+  CUtensorMap w_cur, w_new, w16;
 };
 
 struct EpiParams {
@@ -49,8 +57,10 @@ struct EpiParams {
   int tag_count;   // entries written (a coalesced forward covers several micro-batches)
   int tag_stride;  // element stride between entries
   // epilogue access pattern: 0 = transposed (coalesced rows, lane = column),
-  // 1 = row-per-thread vectors, 2 = staged transpose with 16/8-byte vectors
+  // 1 = row-per-thread vectors, 2 = staged transpose with 16/8-byte vectors,
+  // 3 = (SGD, pair kernel) TMA loads/stores through swizzled smem
   int rowwise;
+  int has_w16;  // TMA SGD epilogue: EpiMaps::w16 is valid
   // timing experiments: nonzero skips the epilogue's global traffic
   int dbg_skip;
 };

@@ -55,6 +55,23 @@ CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn) {
   return map;
 }
 
+// Epilogue tensor maps of the TMA SGD epilogue: 2-D row-major, box 32 x 32.
+CUtensorMap make_epi_tmap(const void* ptr, CUtensorMapDataType dt, int elem_bytes, int rows,
+                          int cols, int ld, CUtensorMapSwizzle swz) {
+  CUtensorMap map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * elem_bytes};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeTiled (epilogue) failed (code " +
+                       std::to_string(static_cast<int>(r)) + ")");
+  return map;
+}
+
 // Kernel choice.  Tall problems (M > 128) use the persistent CTA-pair kernel
 // (256 x BN tiles, overlapped epilogue); M <= 128 (micro-batch forwards of
 // <=128 rows, tiny nets) use the single-CTA 128 x BN kernel.
@@ -94,12 +111,13 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
   init_gemm_attributes();
   if (g.pair) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>;
-    constexpr int smem = Gemm2Cfg<BN>::kSmem;
+    constexpr int smem = Gemm2Cfg<BN, EPI>::kSmem;
     const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
     int cap = sm_count() / 2;
     if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
     const int pairs = std::min(tiles, std::max(1, cap));
-    kern<<<dim3(2 * pairs), Gemm2Cfg<BN>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+    kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
+                                                                      g.maps);
   } else {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
     constexpr int smem = GemmCfg<BN>::kSmem;
@@ -118,9 +136,9 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
       attr[0].val.clusterDim.z = splits;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep));
+      PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
     } else {
-      kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep);
+      kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep, g.maps);
     }
   }
   PB_CUDA(cudaGetLastError());
@@ -133,7 +151,7 @@ void set_attr() {
                                GemmCfg<BN>::kSmem));
   PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               Gemm2Cfg<BN>::kSmem));
+                               Gemm2Cfg<BN, EPI>::kSmem));
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -318,6 +336,25 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
   g.ep.ld_w16 = ld_w16;
   g.ep.lr = lr;
   vec_or_fallback(g.ep, kEpiWgradSgd);
+  // pair kernel: TMA epilogue when the masters / bf16 rows are 16-byte
+  // strided and aligned (PIPESIM_EPI=vec|tile|rows keeps the others)
+  static const bool tma_ok = [] {
+    const char* e = std::getenv("PIPESIM_EPI");
+    return !(e && std::string(e) == "vec");
+  }();
+  if (g.pair && g.ep.rowwise == 2 && tma_ok && !g.exp_kk && ld_w32 % 4 == 0 &&
+      al(w_cur, 16) && al(w_new, 16) && (!w16 || (ld_w16 % 8 == 0 && al(w16, 16)))) {
+    const int M = dz.cols, N = x.cols;
+    g.maps.w_cur = make_epi_tmap(w_cur, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, ld_w32,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+    g.maps.w_new = make_epi_tmap(w_new, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, ld_w32,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+    if (w16)
+      g.maps.w16 = make_epi_tmap(w16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_w16,
+                                 CU_TENSOR_MAP_SWIZZLE_64B);
+    g.ep.has_w16 = w16 ? 1 : 0;
+    g.ep.rowwise = 3;
+  }
   return g;
 }
 

@@ -32,6 +32,7 @@ struct GemmLaunch {
   GemmShape sh;
   EpiParams ep;
   int bn;
+  EpiMaps maps{};      // TMA epilogue tensor maps (wgrad + SGD)
   bool pair = false;  // persistent CTA-pair kernel
   bool exp_kk = false;  // timing experiment only
 };
