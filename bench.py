@@ -58,14 +58,15 @@ class ClockSampler:
 
     def __init__(self, device=0):
         self.device = device
-        self.rows = []
+        self.rows = []  # (host time, fields)
         self.proc = None
+        self.window = None  # (t0, t1) host times of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -75,7 +76,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *a):
         if self.proc:
@@ -88,7 +89,14 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = self.rows
+        if self.window:  # samples taken during the timed region (sampling starts before)
+            t0, t1 = self.window
+            inside = [r for t, r in rows if t0 <= t <= t1 + 0.1]
+            rows = inside or [r for _, r in rows[-2:]]
+        else:
+            rows = [r for _, r in rows]
+        for r in rows:
             try:
                 sm.append(float(r[0]))
                 mx = max(mx, float(r[1]))
@@ -196,6 +204,10 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
+    # the executor runs an 8-stage pipeline on one GPU without split-K
+    # forwards (throughput over latency, session.cu); the standalone per-shape
+    # timings below use the same kernels
+    os.environ.setdefault("PIPESIM_SPLITK", "0")
     import torch
     import torch.distributed as dist
 
@@ -225,10 +237,13 @@ def main():
         sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
                          use_graph=not args.no_graph, rank=rank, world=world, nccl_ids=ids[0])
     else:
+        # the dominant GEMM kind is timed in place: CUDA events around each of
+        # its launches, recorded inside the graph on the launch stream
         sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
-                         use_graph=not args.no_graph)
+                         use_graph=not args.no_graph, timed_kernel=DOMINANT)
     p0 = P.init_network_params(net, CFG["seed"])
     sess.load_params(p0)
+    kernels_per_step = sess.kernels_per_epoch
     rows = M * B
     # pinned host inputs: x (f32) and class labels (int32), same generator as the oracle
     x_np, labels_np = P.make_classification_task(rows, WIDTH, WIDTH, seed=7, as_labels=True,
@@ -256,17 +271,21 @@ def main():
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        resident_step()
-    barrier()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks:  # sampling starts before the warm-up
+        for _ in range(args.warmup):
+            resident_step()
+        barrier()
         t0 = time.perf_counter()
         dev_ms = []
+        kt_ms, kt_fl = [], []
         for _ in range(args.steps):
             resident_step()
             dev_ms.append(out.device_ms)
+            if not split:  # the last timed step's launches
+                kt_ms, kt_fl = sess.kernel_timeline()
         barrier()
         wall = time.perf_counter() - t0
+        clocks.window = (t0, t0 + wall)
     ms_step = float(np.mean(dev_ms))
     if world > 1:
         t = torch.tensor([ms_step], device="cuda")
@@ -301,7 +320,9 @@ def main():
     fps = gemm_flops_per_sample(CFG["widths"])
     step_tflops = fps * rows / (ms_step / 1000.0) / 1e12
 
-    roof = kernel_roofline(peaks)
+    roof = kernel_roofline(peaks, kt_ms if len(kt_ms) else None,
+                           kt_fl if len(kt_fl) else None,
+                           in_step_others(P, net, W, Nm, B, M, local, sess) if not split else {})
     roof["step_gemm_tflops"] = step_tflops
     roof["step_frac_of_sustained"] = step_tflops / peaks["bf16_sus"]
 
@@ -328,7 +349,7 @@ def main():
         "cpu_baseline": cb,
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": M * 4 * B + M * 8, "ms_per_step": e2e_step_ms},
-        "gpu_launches": sess.kernels_per_epoch,
+        "gpu_launches": kernels_per_step,
         "clocks": clocks.summary(),
         "wall_s": wall,
     }
@@ -338,63 +359,92 @@ def main():
     return 0
 
 
-def kernel_roofline(peaks):
-    """Dominant kernel: the tcgen05 GEMM at the workload's dgrad shape
-    (M=1024 rows, N=K=4096; 34.4 GFLOP per launch), timed alone with CUDA
-    events on its launch stream over 50 launches.  The three GEMM shapes of
-    the step are all reported."""
+DOMINANT = "fwd"  # largest share of the step (ncu launch list, profiles/)
+
+
+def in_step_others(P, net, W, Nm, B, M, device, main_sess):
+    """In-step launch statistics of the other two GEMM kinds: one extra
+    session each, timed the same way (events around every launch inside the
+    graph), two epochs, the second kept."""
+    out = {}
+    main_sess.close()  # free HBM for the instrumented sessions
+    for kind in ("dgrad", "wgrad"):
+        s = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=device,
+                      timed_kernel=kind)
+        s.load_params(P.init_network_params(net, CFG["seed"]))
+        x, lab = P.make_classification_task(M * B, WIDTH, WIDTH, seed=7, as_labels=True,
+                                            dtype=np.float32)
+        s.upload(x, lab, y_labels=True)
+        s.run_epoch()
+        s.run_epoch()
+        ms, fl = s.kernel_timeline()
+        out[kind] = (ms, fl)
+        s.close()
+    return out
+
+
+def _stats(ms, fl, hbm_bytes=None):
+    d = {"launches_per_step": int(len(ms)), "mean_us": float(1000.0 * ms.mean()),
+         "tflops": float(fl.sum() / (ms.sum() / 1000.0) / 1e12)}
+    if hbm_bytes is not None:
+        d["hbm_gbs"] = float(hbm_bytes * len(ms) / (ms.sum() / 1000.0) / 1e9)
+    return d
+
+
+def kernel_roofline(peaks, fwd_ms, fwd_fl, others):
+    """Roofline of the dominant kernel, the forward GEMM (bias+ReLU fused):
+    algorithmic flops of every forward launch of the timed step (2*rows*N*K)
+    / its device duration, from CUDA events around each launch inside the
+    graph on its stage stream (kernels overlap other stages' kernels, so this
+    is the in-step rate), against the sustained bf16 peak.  Also: the same
+    in-step statistics for dgrad and wgrad+SGD (the SGD epilogue moves
+    10 B/param + operands: HBM GB/s reported), and each GEMM shape timed alone
+    (graph-captured, weights rotated through 6 copies > L2 so they stream
+    from HBM as in the pipeline)."""
     import torch
     from paper_2410_14312_b200 import kernels as K
     torch.manual_seed(0)
-    res = {}
-    shapes = {"fwd_128x4096x4096": (128, 4096, 4096, "fwd"),
-              "dgrad_1024x4096x4096": (1024, 4096, 4096, "dgrad"),
-              "wgrad_4096x4096x1024": (4096, 4096, 1024, "wgrad")}
-    for name, (m, n, k, kind) in shapes.items():
-        if kind == "fwd":
-            x = K.padded_bf16(m, k); x.normal_()
-            w = K.padded_bf16(n, k); w.normal_()
-            b = torch.zeros(n, device="cuda")
-            y = K.padded_bf16(m, n)
-            fn = lambda: K.linear_fwd(x, w, b, "relu", y16=y)  # noqa: E731
-        elif kind == "dgrad":
-            dz = K.padded_bf16(m, k); dz.normal_()
-            w = K.padded_bf16(k, n); w.normal_()
-            xin = K.padded_bf16(m, n); xin.normal_()
-            d = K.padded_bf16(m, n)
-            fn = lambda: K.linear_bwd_dx(dz, w, xin, "relu", d)  # noqa: E731
-        else:
-            dz = K.padded_bf16(k, m); dz.normal_()
-            xx = K.padded_bf16(k, n); xx.normal_()
-            w32 = torch.zeros(m, n, device="cuda")
-            w16 = K.padded_bf16(m, n)
-            fn = lambda: K.linear_bwd_dw_sgd(dz, xx, w32, w32, w16, 0.0)  # noqa: E731
-        for _ in range(5):
-            fn()
-        st = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(st)
-        reps = 50
-        for _ in range(reps):
-            fn()
-        e1.record(st)
-        e1.synchronize()
-        us = e0.elapsed_time(e1) * 1000.0 / reps
-        flops = 2.0 * m * n * k
-        res[name] = {"us": us, "tflops": flops / us / 1e6}
-    dom = res["dgrad_1024x4096x4096"]
+    n = WIDTH
+    alone = {}
+    ws = [K.padded_bf16(n, n).normal_() for _ in range(6)]
+    for m in (128, 256, 1024):
+        x = K.padded_bf16(m, n).normal_()
+        b = torch.zeros(n, device="cuda")
+        y = K.padded_bf16(m, n)
+        us = K.graph_time_us([lambda w=w: K.linear_fwd(x, w, b, "relu", y16=y) for w in ws])
+        alone[f"fwd_{m}x{n}x{n}"] = {"us": us, "tflops": 2.0 * m * n * n / us / 1e6}
+    dz = K.padded_bf16(1024, n).normal_()
+    xin = K.padded_bf16(1024, n).normal_()
+    d = K.padded_bf16(1024, n)
+    us = K.graph_time_us([lambda w=w: K.linear_bwd_dx(dz, w, xin, "relu", d) for w in ws])
+    alone[f"dgrad_1024x{n}x{n}"] = {"us": us, "tflops": 2.0 * 1024 * n * n / us / 1e6}
+    del ws
+    xx = K.padded_bf16(1024, n).normal_()
+    w32s = [torch.zeros(n, n, device="cuda") for _ in range(2)]
+    w16 = K.padded_bf16(n, n)
+    us = K.graph_time_us([lambda w=w: K.linear_bwd_dw_sgd(dz, xx, w, w, w16, 0.0) for w in w32s])
+    sgd_bytes = n * n * 10 + 2 * 1024 * n * 2  # master r/w + bf16 copy + dZ, X
+    alone[f"wgrad_sgd_{n}x{n}x1024"] = {"us": us, "tflops": 2.0 * 1024 * n * n / us / 1e6,
+                                        "hbm_gbs": sgd_bytes / us / 1e3}
     traffic = None
     try:  # DRAM bytes per launch of the same kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["dgrad_1024x4096x4096"]["bytes"]
+            traffic = json.load(f)["fwd_256x4096x4096"]["bytes"]
     except Exception:
         pass
-    return {"bound": "tensor", "kernel": "gemm_bf16_tcgen05_pair (dgrad shape)",
-            "achieved": dom["tflops"], "peak": peaks["bf16"], "unit": "TFLOP/s",
-            "frac": dom["tflops"] / peaks["bf16"], "peak_source": peaks["src"] + " burst bf16",
-            "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)",
-            "flops_per_launch": 2.0 * 1024 * 4096 * 4096, "per_shape": res}
+    in_step = {}
+    if fwd_ms is not None and len(fwd_ms):
+        in_step["fwd"] = _stats(fwd_ms, fwd_fl)
+    for kind, (ms, fl) in others.items():
+        in_step[kind] = _stats(ms, fl, n * n * 10 + 2 * 1024 * n * 2 if kind == "wgrad" else None)
+    achieved = in_step.get("fwd", {}).get("tflops")
+    return {"bound": "tensor", "kernel": "forward GEMM gemm_bf16_tcgen05_pair/_tcgen05 "
+            "(bias+ReLU epilogue), in-step", "achieved": achieved, "peak": peaks["bf16_sus"],
+            "unit": "TFLOP/s", "frac": achieved / peaks["bf16_sus"] if achieved else None,
+            "peak_source": peaks["src"] + " sustained bf16 (kernel timed inside the step)",
+            "traffic": traffic, "traffic_unit": "bytes/launch at 256x4096x4096 (dram read+write, ncu)",
+            "flops_per_launch": "2*rows*4096*4096 (rows = coalesced micro-batches, 128..1024)",
+            "in_step": in_step, "alone": alone}
 
 
 if __name__ == "__main__":

@@ -216,7 +216,14 @@ typedef struct {
   int use_graph;        /* capture the epoch as one CUDA graph */
   int snapshots;        /* keep fp32 host snapshots of every committed version */
   int fwd_merge;        /* max micro-batches per coalesced forward launch (0 = N) */
+  int timed_kernel;     /* PB_KT_*: CUDA events around every launch of that GEMM
+                           inside the epoch (also inside the graph) */
+  int transport;        /* multi-process split: PB_TRANSPORT_* */
 } pb_train_config;      /* train_config, trainer.hpp:117-126 */
+
+enum { PB_TRANSPORT_NCCL = 0, PB_TRANSPORT_IPC = 1 };
+
+enum { PB_KT_NONE = 0, PB_KT_FWD = 1, PB_KT_DGRAD = 2, PB_KT_WGRAD = 3 };
 
 typedef struct {
   double* mini_loss;  /* [M] loss of each mini-batch before its update */
@@ -276,6 +283,11 @@ typedef struct {
   float* node_end_ms;
 } pb_epoch_profile;
 
+/* Device durations (ms) of the timed GEMM's launches in the last epoch, in
+ * issue order (pb_train_config.timed_kernel), and each launch's algorithmic
+ * flops (2*M*N*K; optional); *n = count (<= max written). */
+int pb_session_kernel_times(pb_session* s, float* ms, double* flops, int max, int* n);
+
 /* One epoch without the CUDA graph, with CUDA timing events around every
  * node (for the bubble report; slower than run_epoch). */
 int pb_session_profile_epoch(pb_session* s, pb_epoch_out* out, pb_epoch_profile* prof);
@@ -294,6 +306,15 @@ int pb_session_read_version(pb_session* s, int stage, int version, double* out,
  * owns stages [r*W/world, (r+1)*W/world)).  Activations (stage s -> s+1) and
  * deltas (s+1 -> s) cross GPU boundaries point to point over NVLink (NCCL
  * send/recv, one 2-rank communicator per boundary and direction). */
+
+/* CUDA IPC peer-memory transport (transport = PB_TRANSPORT_IPC): each rank
+ * exports a blob (IPC handles of its slot arena and handshake flags plus its
+ * transfer list), the caller exchanges them, then every rank connects with
+ * all blobs (concatenated, lens[r] bytes each) before its first epoch.  Works
+ * across NVLink peers and for several processes on one GPU.  Epochs run
+ * without the CUDA graph (the handshake values advance per epoch). */
+int pb_session_ipc_export(pb_session* s, uint8_t* buf, int64_t cap, int64_t* len);
+int pb_session_ipc_connect(pb_session* s, const uint8_t* blobs, const int64_t* lens, int world);
 
 /* Writes one NCCL unique id (128 bytes).  Rank 0 makes 2*(world-1) of them
  * and shares them (e.g. torch.distributed broadcast). */

@@ -10,7 +10,8 @@ class pb_train_config(C.Structure):
                 ("mini_batch_size", C.c_int), ("mini_batches", C.c_int),
                 ("learning_rate", C.c_double), ("mode", C.c_int), ("device", C.c_int),
                 ("use_graph", C.c_int), ("snapshots", C.c_int),
-                ("fwd_merge", C.c_int)]
+                ("fwd_merge", C.c_int), ("timed_kernel", C.c_int),
+                ("transport", C.c_int)]
 
 
 class pb_epoch_out(C.Structure):
@@ -51,9 +52,12 @@ def signatures():
         "pb_session_run_epoch": (i, [p, P(pb_epoch_out)]),
         "pb_session_train_epoch": (i, [p, p, i, p, i, P(pb_epoch_out)]),
         "pb_session_profile_epoch": (i, [p, P(pb_epoch_out), P(pb_epoch_profile)]),
+        "pb_session_kernel_times": (i, [p, P(C.c_float), P(C.c_double), i, P(i)]),
         "pb_session_snapshot": (i, [p, i, i, P(C.c_double), i64]),
         "pb_session_read_version": (i, [p, i, i, P(C.c_double), i64]),
         "pb_nccl_unique_id": (i, [C.c_char_p]),
+        "pb_session_ipc_export": (i, [p, C.c_char_p, i64, P(i64)]),
+        "pb_session_ipc_connect": (i, [p, C.c_char_p, P(i64), i]),
         "pb_session_create_dist": (i, [P(pb_net_spec), P(pb_train_config), i, i, C.c_char_p,
                                        C.c_size_t, P(p)]),
         "pb_plan_transfers": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i), P(i), P(i),

@@ -82,6 +82,8 @@ pb::SessionConfig make_config(const pb_net_spec* net, const pb_train_config* cfg
   c.use_graph = cfg->use_graph != 0;
   c.snapshots = cfg->snapshots != 0;
   c.fwd_merge = cfg->fwd_merge;
+  c.timed_kernel = cfg->timed_kernel;
+  c.transport = cfg->transport;
   if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
   if (const char* e = std::getenv("PIPESIM_SIDE")) c.side_streams = std::atoi(e) != 0;
   return c;
@@ -110,6 +112,26 @@ int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg, i
     throw;
   }
   *out = s;
+  PB_GUARD_END
+}
+
+int pb_session_ipc_export(pb_session* s, uint8_t* buf, int64_t cap, int64_t* len) {
+  PB_GUARD_BEGIN
+  const std::vector<uint8_t> b = S(s).ipc_export();
+  if (len) *len = static_cast<int64_t>(b.size());
+  if (buf) std::memcpy(buf, b.data(), std::min<size_t>(b.size(), static_cast<size_t>(cap)));
+  PB_GUARD_END
+}
+
+int pb_session_ipc_connect(pb_session* s, const uint8_t* blobs, const int64_t* lens, int world) {
+  PB_GUARD_BEGIN
+  std::vector<std::vector<uint8_t>> v;
+  size_t at = 0;
+  for (int r = 0; r < world; ++r) {
+    v.emplace_back(blobs + at, blobs + at + lens[r]);
+    at += static_cast<size_t>(lens[r]);
+  }
+  S(s).ipc_connect(v);
   PB_GUARD_END
 }
 
@@ -212,6 +234,18 @@ int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
   ss.upload(x, dtype(x_dtype), y, dtype(y_dtype));
   const pb::EpochResult r = ss.run_epoch();
   fill(r, ss, out);
+  PB_GUARD_END
+}
+
+int pb_session_kernel_times(pb_session* s, float* ms, double* flops, int max, int* n) {
+  PB_GUARD_BEGIN
+  const std::vector<float> t = S(s).kernel_times_ms();
+  const std::vector<double>& f = S(s).kernel_flops();
+  if (n) *n = static_cast<int>(t.size());
+  for (int i = 0; i < max && i < static_cast<int>(t.size()); ++i) {
+    if (ms) ms[i] = t[i];
+    if (flops) flops[i] = f[i];
+  }
   PB_GUARD_END
 }
 

@@ -115,6 +115,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
     int cap = sm_count() / 2;
     if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
+    if (EPI == kEpiWgradSgd)
+      if (const char* e = std::getenv("PIPESIM_WG_PAIRS")) cap = std::min(cap, std::atoi(e));
     const int pairs = std::min(tiles, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
@@ -316,6 +318,7 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           __nv_bfloat16* w16, int ld_w16, float lr) {
   GemmLaunch g;
   g.bn = pick_bn(dz.cols, x.cols);
+  if (const char* e = std::getenv("PIPESIM_WG_BN")) g.bn = std::atoi(e) == 128 ? 128 : g.bn;
   g.pair = use_pair(dz.cols);
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
   g.tb = make_operand_tmap(x, /*k_major=*/false, 64);

@@ -2,6 +2,7 @@
 #include "session.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -9,6 +10,7 @@
 #include <string>
 #include <tuple>
 
+#include "ipc_p2p.hpp"
 #include "nccl_p2p.hpp"
 #include "status.hpp"
 
@@ -98,7 +100,7 @@ struct Session::Impl {
   };
 
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
-                      send, recv, mark };
+                      send, recv, mark, ktime };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
@@ -171,7 +173,17 @@ struct Session::Impl {
   std::vector<NodeTiming> node_meta;
   std::vector<cudaEvent_t> mark_ev;  // [2 * nodes], created on first profile
   bool profiling = false;
+  std::vector<cudaEvent_t> kt_ev;  // [2 * timed launches]
+  std::vector<double> kt_flops;    // [timed launches] 2*M*N*K
   std::unique_ptr<P2P> p2p;
+  // IPC peer-memory transport (SessionConfig::transport == 1)
+  std::unique_ptr<IpcLink> ipc;
+  std::vector<IpcLink::Msg> msgs;  // this rank's transfers in program order
+  uint32_t epoch_no = 0;
+  int add_msg(bool send, int dir, int peer, size_t bytes, const void* src, void* dst) {
+    msgs.push_back(IpcLink::Msg{send, dir, peer, bytes, src, dst});
+    return static_cast<int>(msgs.size()) - 1;
+  }
   cudaStream_t comm[4] = {nullptr, nullptr, nullptr, nullptr};  // fwd send/recv, bwd send/recv
   bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
   cudaStream_t stream_of(int idx) const {
@@ -195,6 +207,8 @@ struct Session::Impl {
 
   ~Impl() {
     for (cudaEvent_t e : mark_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : kt_ev)
       if (e) cudaEventDestroy(e);
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -486,15 +500,26 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
 
   if (!c.plan_only) {
   PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
+  // Stream priorities (PIPESIM_PRIO): 0 all equal; 1 stage streams (forwards,
+  // loss, the dgrad chain) above the side streams (wgrad + SGD); 2 also
+  // later stages above earlier ones (their backwards start the chain).
+  int prio_mode = 0;
+  if (const char* e = std::getenv("PIPESIM_PRIO")) prio_mode = std::atoi(e);
+  int lo_prio = 0, hi_prio = 0;
+  PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));  // hi is numerically lower
   for (int s = 0; s < W; ++s)
     if (I.local(s)) {
-      PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].stream, cudaStreamNonBlocking));
+      int ps = lo_prio, pside = lo_prio;
+      if (prio_mode >= 1) ps = hi_prio;
+      if (prio_mode >= 2) ps = std::max(hi_prio, lo_prio - 1 - s * (lo_prio - hi_prio) / W);
+      PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].stream, cudaStreamNonBlocking, ps));
       if (c.side_streams)
-        PB_CUDA(cudaStreamCreateWithFlags(&I.stages[s].side, cudaStreamNonBlocking));
+        PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].side, cudaStreamNonBlocking, pside));
     }
   if (c.world > 1) {
     for (cudaStream_t& cs : I.comm) PB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    I.p2p = std::make_unique<P2P>(c.rank, c.world, c.nccl_ids.data(), c.nccl_ids.size());
+    if (c.transport == 0)
+      I.p2p = std::make_unique<P2P>(c.rank, c.world, c.nccl_ids.data(), c.nccl_ids.size());
   }
   PB_CUDA(cudaEventCreate(&I.t0));
   PB_CUDA(cudaEventCreate(&I.t1));
@@ -509,7 +534,27 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
 
   // ---------------- compile the program into ops
   using OK = Impl::OpKind;
-  auto push = [&](Impl::Op op) { I.ops.push_back(op); };
+  auto push = [&](Impl::Op op) {
+    const int kind = op.kind == OK::fwd ? 1 : op.kind == OK::dgrad ? 2 : op.kind == OK::wgrad ? 3 : 0;
+    const bool timed = kind != 0 && kind == c.timed_kernel && !c.plan_only;
+    if (timed) {
+      Impl::Op t{OK::ktime};
+      t.stream = op.stream;
+      t.value = static_cast<int>(I.kt_ev.size());
+      cudaEvent_t e0, e1;
+      PB_CUDA(cudaEventCreate(&e0));
+      PB_CUDA(cudaEventCreate(&e1));
+      I.kt_ev.push_back(e0);
+      I.kt_ev.push_back(e1);
+      I.kt_flops.push_back(2.0 * op.g.sh.M * op.g.sh.N * op.g.sh.K);
+      I.ops.push_back(t);
+      I.ops.push_back(op);
+      t.value += 1;
+      I.ops.push_back(t);
+      return;
+    }
+    I.ops.push_back(op);
+  };
   const int last_s = W - 1;
 
   // Rebase (trainer.cpp:372-379): version 0 of this epoch = the previous
@@ -554,6 +599,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     z.dst = st.cur_version;
     push(z);
   }
+
+  // Skinny forwards split K (lower latency, more SM-time) when this process
+  // keeps few stages in flight; PIPESIM_SESSION_SPLIT=0/1 overrides.
+  bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
+  if (const char* e = std::getenv("PIPESIM_SESSION_SPLIT")) split_fwd = std::atoi(e) != 0;
 
   // ---------------- program: coalesce forwards, order the task DAG
   // A node is one backward task, or a run of consecutive forward tasks of one
@@ -723,6 +773,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ld_in * 2;
           rv.peer = I.owner[up.s];
           rv.dir = 0;
+          rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
           push(rv);
           it = fwd_recv_done.emplace(d, record_on(Impl::kFwdRecv)).first;
         }
@@ -737,6 +788,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         rv.bytes = static_cast<size_t>(c.B) * st.layers.back().ld_out * 2;
         rv.peer = I.owner[up.s];
         rv.dir = 1;
+        rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
         push(rv);
         wait_on(s, record_on(Impl::kBwdRecv));
       }
@@ -771,7 +823,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
                        logits ? as.out32 : nullptr, I.n_out, r0,
-                       /*allow_split=*/I.W_hi - I.W_lo + 1 <= 2);
+                       /*allow_split=*/split_fwd);
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
           o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
@@ -924,6 +976,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.ld_out * 2;
       sd.peer = I.owner[s + 1];
       sd.dir = 0;
+      sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
       push(sd);
     }
     if (!node.fwd && s > 0 && !I.local(s - 1)) {
@@ -934,12 +987,28 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ld_in * 2;
       sd.peer = I.owner[s - 1];
       sd.dir = 1;
+      sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
       push(sd);
     }
   }
+  if (c.world > 1 && c.transport == 1 && !c.plan_only)
+    I.ipc = std::make_unique<IpcLink>(c.rank, c.world, c.device, I.arena, I.msgs);
 }
 
 Session::~Session() = default;
+
+std::vector<uint8_t> Session::ipc_export() {
+  Impl& I = *impl_;
+  if (!I.ipc) throw std::logic_error("session does not use the IPC transport");
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  return I.ipc->export_blob();
+}
+
+void Session::ipc_connect(const std::vector<std::vector<uint8_t>>& blobs) {
+  Impl& I = *impl_;
+  if (!I.ipc) throw std::logic_error("session does not use the IPC transport");
+  I.ipc->connect(blobs);
+}
 
 std::vector<Transfer> Session::transfers() const {
   std::vector<Transfer> out;
@@ -1117,6 +1186,9 @@ void issue(Session::Impl& I, cudaStream_t origin) {
     I.fork_ev = I.new_event();
     for (size_t i = 0; i < streams.size(); ++i) I.join_ev.push_back(I.new_event());
   }
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  PB_CUDA(cudaStreamIsCapturing(origin, &cap_status));
+  const bool capturing = cap_status != cudaStreamCaptureStatusNone;
   cudaEvent_t fork = I.fork_ev;
   PB_CUDA(cudaEventRecord(fork, origin));
   for (cudaStream_t st : streams) PB_CUDA(cudaStreamWaitEvent(st, fork, 0));
@@ -1146,13 +1218,23 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         PB_CUDA(cudaMemsetAsync(o.dst, 0, sizeof(int), s));
         break;
       case OK::send:
-        I.p2p->send(o.src, o.bytes, o.peer, o.dir, s);
+        if (I.ipc)
+          I.ipc->send(o.value, s, I.epoch_no);
+        else
+          I.p2p->send(o.src, o.bytes, o.peer, o.dir, s);
         break;
       case OK::recv:
-        I.p2p->recv(o.dst, o.bytes, o.peer, o.dir, s);
+        if (I.ipc)
+          I.ipc->recv(o.value, s, I.epoch_no);
+        else
+          I.p2p->recv(o.dst, o.bytes, o.peer, o.dir, s);
         break;
       case OK::mark:
         if (I.profiling) PB_CUDA(cudaEventRecord(I.mark_ev[o.value], s));
+        break;
+      case OK::ktime:  // an event record node when captured
+        PB_CUDA(cudaEventRecordWithFlags(I.kt_ev[o.value], s,
+                                         capturing ? cudaEventRecordExternal : 0));
         break;
     }
   }
@@ -1166,8 +1248,12 @@ void issue(Session::Impl& I, cudaStream_t origin) {
 EpochResult Session::run_epoch() {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
+  if (I.ipc) {
+    if (!I.ipc->connected()) throw std::logic_error("IPC transport: call ipc_connect first");
+    ++I.epoch_no;  // the handshake values of this epoch
+  }
   PB_CUDA(cudaEventRecord(I.t0, I.origin));
-  if (cfg_.use_graph) {
+  if (cfg_.use_graph && !I.ipc) {
     if (!I.exec) {
       PB_CUDA(cudaStreamBeginCapture(I.origin, cudaStreamCaptureModeThreadLocal));
       try {
@@ -1190,12 +1276,29 @@ EpochResult Session::run_epoch() {
   return collect_result();
 }
 
+const std::vector<double>& Session::kernel_flops() const { return impl_->kt_flops; }
+
+std::vector<float> Session::kernel_times_ms() {
+  Impl& I = *impl_;
+  std::vector<float> out;
+  for (size_t i = 0; i + 1 < I.kt_ev.size(); i += 2) {
+    float ms = 0.f;
+    PB_CUDA(cudaEventElapsedTime(&ms, I.kt_ev[i], I.kt_ev[i + 1]));
+    out.push_back(ms);
+  }
+  return out;
+}
+
 EpochResult Session::profile_epoch(EpochProfile* prof) {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
   if (I.mark_ev.empty()) {
     I.mark_ev.assign(2 * I.node_meta.size(), nullptr);
     for (cudaEvent_t& e : I.mark_ev) PB_CUDA(cudaEventCreate(&e));
+  }
+  if (I.ipc) {
+    if (!I.ipc->connected()) throw std::logic_error("IPC transport: call ipc_connect first");
+    ++I.epoch_no;
   }
   PB_CUDA(cudaEventRecord(I.t0, I.origin));
   I.profiling = true;

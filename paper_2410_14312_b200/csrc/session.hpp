@@ -59,6 +59,12 @@ struct SessionConfig {
   int fwd_merge = 0;
   // per-stage side stream for wgrad/bias (overlaps the dgrad chain)
   bool side_streams = true;
+  // 0 none, 1 fwd, 2 dgrad, 3 wgrad: CUDA events around every launch of that
+  // GEMM kind, recorded inside the graph (kernel_times_ms)
+  int timed_kernel = 0;
+  // multi-process stage split: 0 NCCL send/recv, 1 CUDA IPC peer memory
+  // (ipc_p2p.hpp; also works for several processes sharing one GPU)
+  int transport = 0;
 };
 
 // One point-to-point transfer of the program, in this process's issue order.
@@ -137,7 +143,14 @@ class Session {
   std::vector<int> act_slot_counts() const;
   int64_t device_bytes() const { return arena_bytes_; }
   int kernels_per_epoch() const { return kernels_per_epoch_; }
+  // durations of the timed GEMM kind's launches in the last epoch (ms)
+  std::vector<float> kernel_times_ms();
+  const std::vector<double>& kernel_flops() const;
   std::vector<Transfer> transfers() const;
+  // IPC transport: this rank's connection blob, and the connect step with
+  // every rank's blob (exchanged by the caller, e.g. over torch.distributed)
+  std::vector<uint8_t> ipc_export();
+  void ipc_connect(const std::vector<std::vector<uint8_t>>& blobs);
 
   struct Impl;  // public so the program-issue helpers can see it
 

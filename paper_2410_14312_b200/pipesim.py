@@ -567,13 +567,18 @@ def format_double(v: float) -> str:
 
 
 # ------------------------------------------------------------ GPU sessions
+TIMED_KERNELS = (None, "fwd", "dgrad", "wgrad")
+TRANSPORTS = ("nccl", "ipc")
+
+
 class Session:
     """Resident pipeline session (C ABI pb_session_*): weights, version pools
     and activation slots of every stage stay in HBM across epochs."""
 
     def __init__(self, net: NetworkSpec, workers, micro_batches, mini_batch_size,
                  mini_batches, learning_rate, mode="timeprest", device=0, use_graph=True,
-                 snapshots=False, fwd_merge=0, rank=0, world=1, nccl_ids=b""):
+                 snapshots=False, fwd_merge=0, rank=0, world=1, nccl_ids=b"",
+                 timed_kernel=None, transport="nccl"):
         if mode not in TRAIN_MODES:
             raise DomainError(f"unknown training mode: {mode}", "mode")
         self.net = net
@@ -582,7 +587,9 @@ class Session:
         self.units = micro_batches if mode == "timeprest" else 1
         cfg = pb_train_config(workers, micro_batches, mini_batch_size, mini_batches,
                               float(learning_rate), TRAIN_MODES.index(mode), device,
-                              int(use_graph), int(snapshots), int(fwd_merge))
+                              int(use_graph), int(snapshots), int(fwd_merge),
+                              TIMED_KERNELS.index(timed_kernel),
+                              TRANSPORTS.index(transport))
         spec = net._c()
         h = C.c_void_p()
         if world > 1:
@@ -655,6 +662,37 @@ class Session:
         self._keep = (x, y)
         N.check(_L().pb_session_upload(self._h, x.ctypes.data, self._dtype(x), y.ctypes.data,
                                        self._dtype(y, y_labels)))
+
+    def ipc_export(self) -> bytes:
+        """This rank's IPC connection blob (transport="ipc")."""
+        n = C.c_int64(0)
+        N.check(_L().pb_session_ipc_export(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        N.check(_L().pb_session_ipc_export(self._h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def ipc_connect(self, blobs):
+        """Connect with every rank's blob (list indexed by rank)."""
+        lens = (C.c_int64 * len(blobs))(*[len(b) for b in blobs])
+        N.check(_L().pb_session_ipc_connect(self._h, b"".join(blobs), lens, len(blobs)))
+
+    def kernel_times_ms(self):
+        """Device durations of the timed GEMM kind's launches in the last
+        epoch (Session(timed_kernel=...)), from CUDA events recorded on the
+        launch stream inside the epoch (inside the graph)."""
+        return self.kernel_timeline()[0]
+
+    def kernel_timeline(self):
+        """(durations ms, algorithmic flops) of the timed GEMM kind's launches
+        in the last epoch, in issue order."""
+        n = C.c_int(0)
+        N.check(_L().pb_session_kernel_times(self._h, None, None, 0, C.byref(n)))
+        ms = np.zeros(max(1, n.value), np.float32)
+        fl = np.zeros(max(1, n.value), np.float64)
+        N.check(_L().pb_session_kernel_times(self._h, ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                             fl.ctypes.data_as(C.POINTER(C.c_double)),
+                                             n.value, C.byref(n)))
+        return ms[:n.value], fl[:n.value]
 
     def profile_epoch(self, max_nodes: int = 1 << 16):
         """One epoch without the CUDA graph, timed per node on the stage
