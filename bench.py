@@ -214,9 +214,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PIPESIM_ONE_GPU=1: every rank on cuda:0 (exercises the multi-process
+    # stage split on a one-GPU box; not a multi-GPU throughput number)
+    one_gpu = os.environ.get("PIPESIM_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2410_14312_b200 import pipesim as P
     from paper_2410_14312_b200 import _native as Nn
@@ -231,11 +239,20 @@ def main():
     # per GPU, activations / deltas cross GPUs point to point over NVLink.
     # PIPESIM_REPLICAS=1 instead runs N independent full pipelines.
     split = world > 1 and not os.environ.get("PIPESIM_REPLICAS")
-    if split:
+    # transport between the GPUs: CUDA IPC peer memory (default; the path the
+    # multi-process GPU tests run) or NCCL send/recv (PIPESIM_TRANSPORT=nccl)
+    transport = os.environ.get("PIPESIM_TRANSPORT", "ipc")
+    if split and transport == "nccl":
         ids = [P.nccl_unique_ids(world)] if rank == 0 else [None]
         dist.broadcast_object_list(ids, src=0)
         sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
                          use_graph=not args.no_graph, rank=rank, world=world, nccl_ids=ids[0])
+    elif split:
+        sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
+                         rank=rank, world=world, transport="ipc")
+        blobs = [None] * world
+        dist.all_gather_object(blobs, sess.ipc_export())
+        sess.ipc_connect(blobs)
     else:
         # the dominant GEMM kind is timed in place: CUDA events around each of
         # its launches, recorded inside the graph on the launch stream
@@ -288,7 +305,7 @@ def main():
         clocks.window = (t0, t0 + wall)
     ms_step = float(np.mean(dev_ms))
     if world > 1:
-        t = torch.tensor([ms_step], device="cuda")
+        t = torch.tensor([ms_step], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     jobs = 1 if split else world  # a split pipeline processes the step's rows once
@@ -306,7 +323,7 @@ def main():
     barrier()
     e2e_step_ms = float(np.mean(e2e_ms))
     if world > 1:
-        t = torch.tensor([e2e_step_ms], device="cuda")
+        t = torch.tensor([e2e_step_ms], device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step_ms = float(t.item())
     e2e_value = jobs * rows / (e2e_step_ms / 1000.0)
@@ -342,7 +359,8 @@ def main():
                    "model": "mlp-16x4096-relu-ce4096", "global_batch": B, "seq_len": None,
                    "micro_batches": Nm, "stages": W, "mini_batches_per_step": M,
                    "samples_per_step": rows,
-                   "parallelism": f"pp{W}-on-{world}gpu" + ("-replicas" if world > 1 and not split else ""),
+                   "parallelism": f"pp{W}-on-{world}gpu" + ("-replicas" if world > 1 and not split else
+                                                            (f"-{transport}" if split else "")),
                    "l2": "working set (bf16 weights 537 MB + fp32 masters 1.07 GB) > L2, no flush",
                    "precision": "bf16 operands, fp32 accumulate, fp32 master weights"},
         "roofline": roof,

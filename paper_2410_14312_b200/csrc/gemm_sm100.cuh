@@ -1048,8 +1048,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       const int cols = min(kColsPerWarp, sh.N - n0);
       if (row >= sh.M || cols <= 0) return;
       if constexpr (EPI == kEpiWgradSgd) {
+        // (the TMA epilogue streams the masters itself, one chunk ahead)
         const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;
-        if (bytes > 0 && (ep.ld_w32 % 4) == 0)
+        if (ep.rowwise != 3 && bytes > 0 && (ep.ld_w32 % 4) == 0)
           ptx::prefetch_l2(ep.w_cur + static_cast<size_t>(row) * ep.ld_w32 + n0, bytes);
       } else if constexpr (EPI == kEpiDgrad) {
         const uint32_t bytes = static_cast<uint32_t>(cols * 2) & ~15u;
