@@ -249,6 +249,16 @@ int splitk_env() {
 }
 }  // namespace
 
+namespace {
+int fwd_bn_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("PIPESIM_FWD_BN_ROWS");
+    return e ? std::atoi(e) : 512;
+  }();
+  return v;
+}
+}  // namespace
+
 // Split-K for skinny forwards (<= 256 rows): enough 128 x 128 tiles x splits
 // to cover the SMs, >= 8 k-blocks per split, at most kMaxSplits (4).
 // PIPESIM_SPLITK=0 disables it, =<n> forces n (A/B runs).
@@ -274,6 +284,12 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
   } else {
     g.bn = pick_bn(rows, w.rows);
     g.pair = use_pair(rows);
+    // PIPESIM_FWD_BN=128: narrower pair tiles for skinny forwards (A/B runs)
+    static const int fwd_bn = [] {
+      const char* e = std::getenv("PIPESIM_FWD_BN");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (fwd_bn == 128 && g.pair && rows <= fwd_bn_rows()) g.bn = 128;
   }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
