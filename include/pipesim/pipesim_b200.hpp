@@ -177,6 +177,10 @@ struct sequence_decomposition {
 sequence_decomposition decompose_sequences(const version_ledger& ledger,
                                            int mini_batches);
 
+// Schedule document JSON (export.hpp; export.cpp:78-139): config, non-idle
+// cells, ledger and v analysis, schema version 1.
+std::string schedule_document_json(const schedule_grid& grid, const version_ledger& ledger);
+
 struct retention_interval {
   int version;
   int retained_from_slot;

@@ -80,6 +80,10 @@ int pb_schedule_build(const pb_sim_config* cfg, int mode, int* horizon,
 /* validate_schedule — schedule.hpp:108-109.  Violations are data: kinds[i]
  * (0 task_invariant, 1 stage_continuity, 2 completeness, 3 backward_priority)
  * and '\n'-separated messages. */
+/* Schedule document JSON of build_*_schedule(cfg) and its ledger
+ * (export.cpp:78-139; reference `pipesim simulate --json`). */
+int pb_schedule_document(const pb_sim_config* cfg, int mode, char* buf, int64_t cap,
+                         int64_t* len);
 int pb_schedule_validate(const pb_sim_config* cfg, int mode,
                          const pb_task* cells, int horizon, int* n_violations,
                          int* kinds, int cap_kinds, char* messages,
@@ -287,6 +291,11 @@ typedef struct {
  * issue order (pb_train_config.timed_kernel), and each launch's algorithmic
  * flops (2*M*N*K; optional); *n = count (<= max written). */
 int pb_session_kernel_times(pb_session* s, float* ms, double* flops, int max, int* n);
+
+/* Schedule document JSON (reference export.cpp:78-139) of the last epoch,
+ * with the version numbers observed on the device (pins; timeprest
+ * consumptions).  *len = bytes (without the terminating NUL). */
+int pb_session_trace_document(pb_session* s, char* buf, int64_t cap, int64_t* len);
 
 /* One epoch without the CUDA graph, with CUDA timing events around every
  * node (for the bubble report; slower than run_epoch). */

@@ -81,6 +81,13 @@ def render_ascii(w, n, m, mode=0):
     return buf.value.decode()
 
 
+def schedule_document(w, n, m, mode=0):
+    """The reference's schedule document JSON (export.cpp:78-139)."""
+    buf = C.create_string_buffer(1 << 24)
+    _check(lib().ref_schedule_document(w, n, m, mode, buf, 1 << 24))
+    return buf.value.decode()
+
+
 def ledger(w, n, m, mode=0):
     units = n if mode == 0 else 1
     commits = np.zeros((m * w, 4), np.int32)

@@ -14,6 +14,7 @@
 
 #include "pipesim/checkpoint.hpp"
 #include "pipesim/errors.hpp"
+#include "pipesim/export.hpp"
 #include "pipesim/ledger.hpp"
 #include "pipesim/metrics.hpp"
 #include "pipesim/render.hpp"
@@ -135,6 +136,18 @@ int ref_validate(int w, int n, int m, int mode, const int* cells, int h, int* n_
 int ref_render_ascii(int w, int n, int m, int mode, char* buf, int cap) {
   try {
     put_str(render_ascii(build(w, n, m, mode)), buf, cap);
+    return 0;
+  } catch (...) {
+    return fail();
+  }
+}
+
+// schedule document JSON (export.cpp:78-139) of a (w, n, m, mode) config
+int ref_schedule_document(int w, int n, int m, int mode, char* buf, int cap) {
+  try {
+    const sim_config c = mk(w, n, m);
+    const schedule_grid g = build(w, n, m, mode);
+    put_str(schedule_document_json(g, assign_versions(g, c)), buf, cap);
     return 0;
   } catch (...) {
     return fail();

@@ -119,6 +119,8 @@ def _declare(L: C.CDLL) -> None:
         "pb_version": (C.c_char_p, []),
         "pb_validate_config": (i, [P(pb_sim_config)]),
         "pb_schedule_build": (i, [P(pb_sim_config), i, P(i), P(pb_task), i]),
+        "pb_schedule_document": (i, [P(pb_sim_config), i, C.c_char_p, C.c_int64,
+                                     P(C.c_int64)]),
         "pb_schedule_validate": (i, [P(pb_sim_config), i, P(pb_task), i, P(i), P(i), i,
                                      C.c_char_p, i]),
         "pb_assign_versions": (i, [P(pb_sim_config), i, P(pb_task), i, P(pb_commit),

@@ -53,6 +53,7 @@ def signatures():
         "pb_session_train_epoch": (i, [p, p, i, p, i, P(pb_epoch_out)]),
         "pb_session_profile_epoch": (i, [p, P(pb_epoch_out), P(pb_epoch_profile)]),
         "pb_session_kernel_times": (i, [p, P(C.c_float), P(C.c_double), i, P(i)]),
+        "pb_session_trace_document": (i, [p, C.c_char_p, i64, P(i64)]),
         "pb_session_snapshot": (i, [p, i, i, P(C.c_double), i64]),
         "pb_session_read_version": (i, [p, i, i, P(C.c_double), i64]),
         "pb_nccl_unique_id": (i, [C.c_char_p]),

@@ -1,5 +1,6 @@
 // C ABI over the host plan layer and model helpers (include/pipesim_b200.h).
 // Marshals flat arrays to / from the pipesim:: value types.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,6 +113,22 @@ int pb_schedule_build(const pb_sim_config* cfg, int mode, int* horizon,
       cells[static_cast<size_t>(w - 1) * cap_slots + (t - 1)] =
           pb_task{from_kind(k.kind), k.mini, k.micro};
     }
+  PB_GUARD_END
+}
+
+int pb_schedule_document(const pb_sim_config* cfg, int mode, char* buf, int64_t cap,
+                         int64_t* len) {
+  PB_GUARD_BEGIN
+  const sim_config c = to_cfg(cfg);
+  const schedule_grid g = to_mode(mode) == schedule_mode::timeprest ? build_nf1b_schedule(c)
+                                                                     : build_1f1b_schedule(c);
+  const std::string d = schedule_document_json(g, assign_versions(g, c));
+  if (len) *len = static_cast<int64_t>(d.size());
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(d.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, d.data(), n);
+    buf[n] = '\0';
+  }
   PB_GUARD_END
 }
 

@@ -237,6 +237,18 @@ int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
   PB_GUARD_END
 }
 
+int pb_session_trace_document(pb_session* s, char* buf, int64_t cap, int64_t* len) {
+  PB_GUARD_BEGIN
+  const std::string d = S(s).trace_document();
+  if (len) *len = static_cast<int64_t>(d.size());
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(d.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, d.data(), n);
+    buf[n] = '\0';
+  }
+  PB_GUARD_END
+}
+
 int pb_session_kernel_times(pb_session* s, float* ms, double* flops, int max, int* n) {
   PB_GUARD_BEGIN
   const std::vector<float> t = S(s).kernel_times_ms();

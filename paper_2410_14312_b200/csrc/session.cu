@@ -1357,7 +1357,24 @@ EpochResult Session::collect_result() {
   }
   for (const auto& p : ledger_.pins) r.pinned.push_back(p.version);
   r.consumed = ledger_.update_source;
+  last_ = r;
   return r;
+}
+
+std::string Session::trace_document() const {
+  if (!grid_) throw std::logic_error("trace_document: the sequential mode has no schedule grid");
+  if (cfg_.world > 1) throw std::logic_error("trace_document: multi-process session");
+  if (last_.dev_fwd.empty()) throw std::logic_error("trace_document: run an epoch first");
+  const int W = cfg_.W, U = units();
+  pipesim::version_ledger L = ledger_;
+  for (auto& p : L.pins) {
+    const int j = U > 1 ? p.micro - 1 : 0;
+    p.version = last_.dev_fwd[(static_cast<size_t>(p.mini - 1) * U + j) * W + 0];
+  }
+  if (cfg_.mode == RunMode::timeprest)
+    for (auto& c : L.consumptions)
+      c.version = last_.dev_bwd[static_cast<size_t>(c.mini - 1) * W + (c.stage - 1)];
+  return pipesim::schedule_document_json(*grid_, L);
 }
 
 }  // namespace pb

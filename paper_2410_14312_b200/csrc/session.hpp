@@ -143,6 +143,11 @@ class Session {
   std::vector<int> act_slot_counts() const;
   int64_t device_bytes() const { return arena_bytes_; }
   int kernels_per_epoch() const { return kernels_per_epoch_; }
+  // Schedule document (export.cpp schema) of the last epoch with the version
+  // numbers the device observed: each pin from the tag its stage-1 forward
+  // read, and (timeprest) each consumption from the tag its backward
+  // propagated through.  Single-process sessions with a schedule grid.
+  std::string trace_document() const;
   // durations of the timed GEMM kind's launches in the last epoch (ms)
   std::vector<float> kernel_times_ms();
   const std::vector<double>& kernel_flops() const;
@@ -156,6 +161,7 @@ class Session {
 
  private:
   EpochResult collect_result();
+  EpochResult last_;  // the last epoch's result (trace_document)
   SessionConfig cfg_;
   std::unique_ptr<Impl> impl_;
   std::unique_ptr<pipesim::schedule_grid> grid_;

@@ -189,6 +189,17 @@ class ValidationReport:
         return not self.violations
 
 
+def schedule_document_json(cfg: SimConfig, mode: str = "timeprest") -> str:
+    """schedule_document_json(build_*_schedule(cfg), assign_versions(...))
+    (export.cpp:78-139): the reference's schedule document, schema 1."""
+    c = cfg._c()
+    n = C.c_int64(0)
+    N.check(_L().pb_schedule_document(C.byref(c), _mode_id(mode), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    N.check(_L().pb_schedule_document(C.byref(c), _mode_id(mode), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def validate_schedule(grid: ScheduleGrid, cfg: SimConfig) -> ValidationReport:
     """validate_schedule (schedule.hpp:108-109)."""
     c = cfg._c()
@@ -675,6 +686,15 @@ class Session:
         """Connect with every rank's blob (list indexed by rank)."""
         lens = (C.c_int64 * len(blobs))(*[len(b) for b in blobs])
         N.check(_L().pb_session_ipc_connect(self._h, b"".join(blobs), lens, len(blobs)))
+
+    def trace_document(self) -> str:
+        """The last epoch's schedule document with device-observed versions
+        (pins; timeprest consumptions), in the reference's JSON schema."""
+        n = C.c_int64(0)
+        N.check(_L().pb_session_trace_document(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        N.check(_L().pb_session_trace_document(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
     def kernel_times_ms(self):
         """Device durations of the timed GEMM kind's launches in the last
