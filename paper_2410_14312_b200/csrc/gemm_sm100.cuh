@@ -812,7 +812,9 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
   const int lane = threadIdx.x % 32;
   uint8_t* b32[2] = {wbuf, wbuf + 4096};
   uint8_t* b16[2] = {wbuf + 8192, wbuf + 8192 + 2048};
-  if (first_tile && lane == 0) sgd_tma_load(maps, b32[st.g & 1], &bars[st.g & 1], n_base, row_base);
+  const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;  // timing experiments
+  if (first_tile && lane == 0 && !skip_ld)
+    sgd_tma_load(maps, b32[st.g & 1], &bars[st.g & 1], n_base, row_base);
 #pragma unroll 1
   for (int c = 0; c < n_cols; c += 32) {
     const int b = st.g & 1;
@@ -821,15 +823,18 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
       // read it, prefetch the next chunk (this tile's, or the next tile's
       // first) into it
       ptx::bulk_wait_group_read<0>();
-      if (c + 32 < n_cols)
+      if (skip_ld) {
+      } else if (c + 32 < n_cols)
         sgd_tma_load(maps, b32[b ^ 1], &bars[b ^ 1], n_base + c + 32, row_base);
       else if (next_row >= 0)
         sgd_tma_load(maps, b32[b ^ 1], &bars[b ^ 1], next_col, next_row);
     }
     uint32_t r[32];
     ptx::tmem_ld32(t_row + c, r);
-    ptx::mbar_wait(&bars[b], st.phase[b]);
-    st.phase[b] ^= 1;
+    if (!skip_ld) {
+      ptx::mbar_wait(&bars[b], st.phase[b]);
+      st.phase[b] ^= 1;
+    }
     ptx::tmem_ld_wait();
     uint8_t* row32 = b32[b] + lane * 128;
     uint8_t* row16 = b16[b] + lane * 64;
@@ -849,7 +854,7 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
     }
     ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA store
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && !skip_st) {
       ptx::tma_store_2d(&maps.w_new, b32[b], n_base + c, row_base);
       if (ep.has_w16) ptx::tma_store_2d(&maps.w16, b16[b], n_base + c, row_base);
       ptx::bulk_commit_group();
