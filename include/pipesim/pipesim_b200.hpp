@@ -353,6 +353,7 @@ struct options {
   bool use_graph = true;                 // capture the epoch as a CUDA graph
   digest_policy digest = digest_policy::automatic;
   long long digest_auto_limit = 4000000; // params; above: final_only
+  bool verify_fp32 = false;              // fp32 FFMA verify precision (no bf16 rounding)
 };
 void set_options(const options& o);
 options get_options();

@@ -223,7 +223,11 @@ typedef struct {
   int timed_kernel;     /* PB_KT_*: CUDA events around every launch of that GEMM
                            inside the epoch (also inside the graph) */
   int transport;        /* multi-process split: PB_TRANSPORT_* */
+  int precision;        /* PB_PRECISION_*: bf16 tensor cores (fp32 accumulate,
+                           fp32 masters) or the fp32 FFMA verify mode */
 } pb_train_config;      /* train_config, trainer.hpp:117-126 */
+
+enum { PB_PRECISION_BF16 = 0, PB_PRECISION_FP32_VERIFY = 1 };
 
 enum { PB_TRANSPORT_NCCL = 0, PB_TRANSPORT_IPC = 1 };
 

@@ -11,7 +11,7 @@ class pb_train_config(C.Structure):
                 ("learning_rate", C.c_double), ("mode", C.c_int), ("device", C.c_int),
                 ("use_graph", C.c_int), ("snapshots", C.c_int),
                 ("fwd_merge", C.c_int), ("timed_kernel", C.c_int),
-                ("transport", C.c_int)]
+                ("transport", C.c_int), ("precision", C.c_int)]
 
 
 class pb_epoch_out(C.Structure):

@@ -84,6 +84,7 @@ pb::SessionConfig make_config(const pb_net_spec* net, const pb_train_config* cfg
   c.fwd_merge = cfg->fwd_merge;
   c.timed_kernel = cfg->timed_kernel;
   c.transport = cfg->transport;
+  c.verify_fp32 = cfg->precision == 1;
   if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
   if (const char* e = std::getenv("PIPESIM_SIDE")) c.side_streams = std::atoi(e) != 0;
   return c;

@@ -76,6 +76,22 @@ __device__ __forceinline__ void with_act(const EpiParams& ep, F&& f) {
   }
 }
 
+// Host-side twin of with_act (kernel selection by activation).
+template <int EPI, typename F>
+inline void with_act_host(const EpiParams& ep, F&& f) {
+  if constexpr (EPI == kEpiWgradSgd) {
+    f(std::integral_constant<int, kLinear>{});
+  } else {
+    const int a = EPI == kEpiFwd ? ep.act : ep.act_prev;
+    switch (a) {
+      case kRelu: f(std::integral_constant<int, kRelu>{}); break;
+      case kTanh: f(std::integral_constant<int, kTanh>{}); break;
+      case kSigmoid: f(std::integral_constant<int, kSigmoid>{}); break;
+      default: f(std::integral_constant<int, kLinear>{}); break;
+    }
+  }
+}
+
 // Derivative expressed through the activation value a = act(z).
 __device__ __forceinline__ float act_grad_from_out(float a, int act) {
   switch (act) {

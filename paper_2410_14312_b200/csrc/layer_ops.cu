@@ -275,8 +275,25 @@ int fwd_splits(int rows, int N, int K) {
 
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
-                    float* y32, int ld_y32, int y_row_off, bool allow_split) {
+                    float* y32, int ld_y32, int y_row_off, bool allow_split, bool verify) {
   GemmLaunch g;
+  if (verify) {
+    g.simt = true;
+    g.simt_a = reinterpret_cast<const float*>(x.ptr);
+    g.simt_lda = x.ld;
+    g.simt_b = reinterpret_cast<const float*>(w.ptr);
+    g.simt_ldb = w.ld;
+    g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0, 1, 0};
+    g.ep = EpiParams{};
+    g.ep.bias = bias;
+    g.ep.act = act;
+    g.ep.y16 = y16;
+    g.ep.ld_y16 = ld_y16;
+    g.ep.y32 = y32;
+    g.ep.ld_y32 = ld_y32;
+    g.ep.y_row_off = y_row_off;
+    return g;
+  }
   const int splits = allow_split || splitk_env() > 0 ? fwd_splits(rows, w.rows, x.cols) : 1;
   if (splits > 1) {  // single-CTA 128 x 128 tiles, one cluster of `splits` per tile
     g.bn = 128;
@@ -312,8 +329,23 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
 }
 
 GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
-                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d) {
+                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d, bool verify) {
   GemmLaunch g;
+  if (verify) {
+    g.simt = true;
+    g.simt_a = reinterpret_cast<const float*>(dz.ptr);
+    g.simt_lda = dz.ld;
+    g.simt_b = reinterpret_cast<const float*>(w.ptr);
+    g.simt_ldb = w.ld;
+    g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0, 1, 0};
+    g.ep = EpiParams{};
+    g.ep.xin = xin;
+    g.ep.ld_xin = ld_xin;
+    g.ep.act_prev = act_prev;
+    g.ep.d16 = d;
+    g.ep.ld_d16 = ld_d;
+    return g;
+  }
   g.bn = pick_bn(dz.rows, w.cols);
   g.pair = use_pair(dz.rows);
   g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
@@ -331,8 +363,24 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
 
 GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           const float* w_cur, float* w_new, int ld_w32,
-                          __nv_bfloat16* w16, int ld_w16, float lr) {
+                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify) {
   GemmLaunch g;
+  if (verify) {
+    g.simt = true;
+    g.simt_a = reinterpret_cast<const float*>(dz.ptr);
+    g.simt_lda = dz.ld;
+    g.simt_b = reinterpret_cast<const float*>(x.ptr);
+    g.simt_ldb = x.ld;
+    g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off, 1, 0};
+    g.ep = EpiParams{};
+    g.ep.w_cur = w_cur;
+    g.ep.w_new = w_new;
+    g.ep.ld_w32 = ld_w32;
+    g.ep.w16 = w16;
+    g.ep.ld_w16 = ld_w16;
+    g.ep.lr = lr;
+    return g;
+  }
   g.bn = pick_bn(dz.cols, x.cols);
   if (const char* e = std::getenv("PIPESIM_WG_BN")) g.bn = std::atoi(e) == 128 ? 128 : g.bn;
   g.pair = use_pair(dz.cols);
@@ -378,12 +426,15 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
 }
 
 void launch_fwd(const GemmLaunch& g, cudaStream_t st) {
+  if (g.simt) return launch_simt_gemm(g, kEpiFwd, st);
   launch_bn<false, false, kEpiFwd>(g, st);
 }
 void launch_dgrad(const GemmLaunch& g, cudaStream_t st) {
+  if (g.simt) return launch_simt_gemm(g, kEpiDgrad, st);
   launch_bn<false, true, kEpiDgrad>(g, st);
 }
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
+  if (g.simt) return launch_simt_gemm(g, kEpiWgradSgd, st);
   if (g.exp_kk) {  // timing experiment (PIPESIM_EXP_WG=kk): K-major operands
     launch_bn<false, false, kEpiWgradSgd>(g, st);
     return;
@@ -399,8 +450,9 @@ void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
 constexpr int kBiasCols = 32;
 constexpr int kBiasRowGroups = 64;
 
+template <typename TZ>
 __global__ void __launch_bounds__(256)
-    bias_sgd_kernel(const __nv_bfloat16* __restrict__ dz, int rows, int out, int ld_dz,
+    bias_sgd_kernel(const TZ* __restrict__ dz, int rows, int out, int ld_dz,
                     const float* b_cur, float* b_new, float* b_copy, float lr,
                     int* tag_slot, int* cur_version, int version, const int* trace_src,
                     int* trace_dst) {
@@ -409,8 +461,8 @@ __global__ void __launch_bounds__(256)
   const int ry = threadIdx.x / 4;
   const int c0 = blockIdx.x * kBiasCols + cx * 8;
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const bool vec = (ld_dz % 8) == 0 && c0 + 8 <= out;
-  if (vec) {
+  const bool vec = sizeof(TZ) == 2 && (ld_dz % 8) == 0 && c0 + 8 <= out;
+  if constexpr (sizeof(TZ) == 2) if (vec) {
     // 8 independent 16-byte row loads in flight per thread, then accumulate
     // in row order (fixed order: deterministic).
     constexpr int kU = 8;
@@ -433,10 +485,11 @@ __global__ void __launch_bounds__(256)
         }
       }
     }
-  } else {
+  }
+  if (!vec) {
     for (int r = ry; r < rows; r += kBiasRowGroups) {
-      const __nv_bfloat16* p = dz + static_cast<size_t>(r) * ld_dz + c0;
-      for (int k = 0; k < 8 && c0 + k < out; ++k) acc[k] += __bfloat162float(p[k]);
+      const TZ* p = dz + static_cast<size_t>(r) * ld_dz + c0;
+      for (int k = 0; k < 8 && c0 + k < out; ++k) acc[k] += static_cast<float>(p[k]);
     }
   }
 #pragma unroll
@@ -462,10 +515,16 @@ __global__ void __launch_bounds__(256)
 void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int out, int ld_dz, const float* b_cur, float* b_new,
                      float* b_copy, float lr, int* tag_slot, int* cur_version,
-                     int version, const int* trace_src, int* trace_dst) {
-  bias_sgd_kernel<<<(out + kBiasCols - 1) / kBiasCols, 256, 0, st>>>(
-      dz, rows, out, ld_dz, b_cur, b_new, b_copy, lr, tag_slot, cur_version, version,
-      trace_src, trace_dst);
+                     int version, const int* trace_src, int* trace_dst, bool dz_f32) {
+  const int grid = (out + kBiasCols - 1) / kBiasCols;
+  if (dz_f32)
+    bias_sgd_kernel<float><<<grid, 256, 0, st>>>(
+        reinterpret_cast<const float*>(dz), rows, out, ld_dz, b_cur, b_new, b_copy, lr,
+        tag_slot, cur_version, version, trace_src, trace_dst);
+  else
+    bias_sgd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        dz, rows, out, ld_dz, b_cur, b_new, b_copy, lr, tag_slot, cur_version, version,
+        trace_src, trace_dst);
   PB_CUDA(cudaGetLastError());
 }
 
@@ -499,17 +558,24 @@ __device__ __forceinline__ float block_max(float v, float* red) {
   return s;
 }
 
+template <typename TZ>
+__device__ __forceinline__ TZ to_dz(float g) {
+  if constexpr (sizeof(TZ) == 2) return __float2bfloat16_rn(g);
+  else return g;
+}
+
+template <typename TZ>
 __global__ void __launch_bounds__(256)
     loss_kernel(const float* __restrict__ y, int rows, int cols, int ld_y,
                 const float* __restrict__ t, int ld_t, int loss, int act_last,
-                float denom, __nv_bfloat16* __restrict__ dz, int ld_dz,
+                float denom, TZ* __restrict__ dz, int ld_dz,
                 float* __restrict__ row_loss) {
   __shared__ float red[8];
   const int row = blockIdx.x;
   if (row >= rows) return;
   const float* yr = y + static_cast<size_t>(row) * ld_y;
   const float* tr = t + static_cast<size_t>(row) * ld_t;
-  __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
+  TZ* dr = dz + static_cast<size_t>(row) * ld_dz;
   float acc = 0.f;
   if (loss == 0) {  // mse
     for (int c = threadIdx.x; c < cols; c += blockDim.x) {
@@ -518,7 +584,7 @@ __global__ void __launch_bounds__(256)
       acc += d * d;
       float g = 2.f * d / denom;
       if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
-      dr[c] = __float2bfloat16_rn(g);
+      dr[c] = to_dz<TZ>(g);
     }
   } else {
     float mx = -INFINITY;
@@ -535,7 +601,7 @@ __global__ void __launch_bounds__(256)
       if (tc > 0.5f) acc += -(z - lse) * tc;
       float g = (expf(z) / se - tc) / denom;
       if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
-      dr[c] = __float2bfloat16_rn(g);
+      dr[c] = to_dz<TZ>(g);
     }
   }
   acc = block_sum(acc, red);
@@ -544,11 +610,16 @@ __global__ void __launch_bounds__(256)
 
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
-                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss) {
+                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss, bool dz_f32) {
   if (rows <= 0) return;
   const int threads = cols >= 256 ? 256 : (cols >= 128 ? 128 : 64);
-  loss_kernel<<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss, act_last,
-                                         denom, dz, ld_dz, row_loss);
+  if (dz_f32)
+    loss_kernel<float><<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss,
+                                                 act_last, denom, reinterpret_cast<float*>(dz),
+                                                 ld_dz, row_loss);
+  else
+    loss_kernel<__nv_bfloat16><<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss,
+                                                         act_last, denom, dz, ld_dz, row_loss);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -33,6 +33,12 @@ struct GemmLaunch {
   EpiParams ep;
   int bn;
   EpiMaps maps{};      // TMA epilogue tensor maps (wgrad + SGD)
+  // fp32 verify precision (verify_fp32.cu): CUDA-core FFMA GEMM on fp32
+  // operands stored in the same buffers (pointers reinterpreted)
+  bool simt = false;
+  const float* simt_a = nullptr;
+  const float* simt_b = nullptr;
+  int simt_lda = 0, simt_ldb = 0;
   bool pair = false;  // persistent CTA-pair kernel
   bool exp_kk = false;  // timing experiment only
 };
@@ -46,15 +52,17 @@ int fwd_splits(int rows, int N, int K);
 // forward: out = act(x[rows, in] * w[out, in]^T + b)
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
-                    float* y32, int ld_y32, int y_row_off, bool allow_split = true);
+                    float* y32, int ld_y32, int y_row_off, bool allow_split = true,
+                    bool verify = false);
 // dgrad: d[rows, in] = (dz[rows,out] * w[out,in]) .* act'(xin)
 GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
-                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d);
+                      int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d,
+                      bool verify = false);
 // wgrad+SGD: w_new[out,in] = w_cur - lr * dz[rows,out]^T x[rows,in]
 // (x rows start at x_row_off inside its buffer)
 GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           const float* w_cur, float* w_new, int ld_w32,
-                          __nv_bfloat16* w16, int ld_w16, float lr);
+                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify = false);
 
 void launch_fwd(const GemmLaunch& g, cudaStream_t st);
 void launch_dgrad(const GemmLaunch& g, cudaStream_t st);
@@ -64,7 +72,13 @@ void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int out, int ld_dz, const float* b_cur, float* b_new,
                      float* b_copy, float lr, int* tag_slot, int* cur_version,
                      int version, const int* trace_src = nullptr,
-                     int* trace_dst = nullptr);
+                     int* trace_dst = nullptr, bool dz_f32 = false);
+
+// fp32 verify precision (verify_fp32.cu)
+void launch_simt_gemm(const GemmLaunch& g, int kind, cudaStream_t st);
+// rows x cols of f64/f32 (src_f64) -> fp32 rows (leading dims in elements)
+void launch_rows_to_f32(cudaStream_t st, const void* src, bool src_f64, int rows, int cols,
+                        int ld_src, float* dst, int ld_dst);
 
 // Sets the dynamic-smem attribute of every GEMM instantiation (call before
 // any stream capture).
@@ -72,7 +86,8 @@ void init_gemm_attributes();
 
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
-                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss);
+                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss,
+                 bool dz_f32 = false);
 
 void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
                              int cols, int ld_src, __nv_bfloat16* dst,

@@ -139,6 +139,10 @@ struct Session::Impl {
 
   const SessionConfig& cfg;
   int W, N, B, M, U, Rm;
+  // fp32 verify precision: activation / delta / weight-copy buffers hold fp32
+  // in the same layout; sc = bf16 slots per stored element (1 or 2)
+  bool v32 = false;
+  int sc = 1;
   std::vector<Stage> stages;
   // data
   __nv_bfloat16* x16 = nullptr;
@@ -258,6 +262,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   impl_ = std::make_unique<Impl>(cfg_);
   Impl& I = *impl_;
   I.plan_only = c.plan_only;
+  I.v32 = c.verify_fp32;
+  I.sc = c.verify_fp32 ? 2 : 1;
   I.W = c.W;
   I.N = c.N;
   I.B = c.B;
@@ -427,20 +433,20 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
       if (!I.local(s)) continue;
       need += 2 * (bytes_of(static_cast<size_t>(d.in) * d.out, 4) + bytes_of(d.out, 4));
-      need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2) + bytes_of(d.out, 4));
-      need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
-      if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2);
+      need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2 * I.sc) + bytes_of(d.out, 4));
+      need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
+      if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
     }
     off += st.param_count;
     if (!I.local(s)) continue;
     if (s > 0 && !I.local(s - 1))  // boundary buffers: received input + outgoing delta
-      need += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2);
+      need += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2 * I.sc);
     need += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
-    need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2);
+    need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2 * I.sc);
     if (s == W - 1) need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
   }
   const size_t rows = static_cast<size_t>(M) * c.B;
-  need += bytes_of(rows * I.ld_x, 2) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4);
+  need += bytes_of(rows * I.ld_x, 2 * I.sc) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4);
   I.stage_bytes = rows * std::max<size_t>(c.widths.front(), I.n_out) * 8;
   need += bytes_of(I.stage_bytes, 1);
   need += bytes_of(static_cast<size_t>(M) * U * W, 4) + bytes_of(static_cast<size_t>(M) * W, 4);
@@ -466,7 +472,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     st.pool.resize(pool_n[s]);
     for (auto& ps : st.pool) {
       for (auto& d : st.layers) {
-        ps.w16.push_back(I.carve<__nv_bfloat16>(static_cast<size_t>(d.out) * d.ld_in));
+        ps.w16.push_back(I.carve<__nv_bfloat16>(static_cast<size_t>(d.out) * d.ld_in * I.sc));
         ps.b32.push_back(I.carve<float>(d.out));
       }
       ps.tag = I.carve<int>(1);
@@ -477,21 +483,21 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       for (int l = 0; l < st.L; ++l) {
         const bool logits = (s == W - 1) && (l == st.L - 1);
         as.out16.push_back(logits ? nullptr
-                                  : I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) *
+                                  : I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * I.sc *
                                                            st.layers[l].ld_out));
       }
       if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out);
-      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().ld_out);
+      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().ld_out * I.sc);
       if (s > 0 && !I.local(s - 1)) {
-        as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in);
-        as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in);
+        as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in * I.sc);
+        as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in * I.sc);
       }
     }
     for (int l = 0; l + 1 < st.L; ++l)
       st.scratch_dz.push_back(
-          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].ld_out));
+          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].ld_out * I.sc));
   }
-  I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x);
+  I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x * I.sc);
   I.y32 = I.carve<float>(rows * I.n_out);
   I.row_loss = I.carve<float>(rows);
   I.stage_buf = I.carve<char>(I.stage_bytes);
@@ -583,7 +589,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         o.stream = s;
         o.dst = st.pool[c0].w16[l];
         o.src = st.pool[cM].w16[l];
-        o.bytes = sizeof(__nv_bfloat16) * d.out * static_cast<size_t>(d.ld_in);
+        o.bytes = sizeof(__nv_bfloat16) * I.sc * d.out * static_cast<size_t>(d.ld_in);
         push(o);
         o.dst = st.pool[c0].b32[l];
         o.src = st.pool[cM].b32[l];
@@ -769,8 +775,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           const auto& fl = st.layers.front();
           Impl::Op rv{OK::recv};
           rv.stream = Impl::kFwdRecv;
-          rv.dst = as.in16 + static_cast<size_t>(up.jj0) * I.Rm * fl.ld_in;
-          rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ld_in * 2;
+          rv.dst = as.in16 + static_cast<size_t>(up.jj0) * I.Rm * fl.ld_in * I.sc;
+          rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ld_in * 2 * I.sc;
           rv.peer = I.owner[up.s];
           rv.dir = 0;
           rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
@@ -785,7 +791,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         Impl::Op rv{OK::recv};
         rv.stream = Impl::kBwdRecv;
         rv.dst = as.dzin;
-        rv.bytes = static_cast<size_t>(c.B) * st.layers.back().ld_out * 2;
+        rv.bytes = static_cast<size_t>(c.B) * st.layers.back().ld_out * 2 * I.sc;
         rv.peer = I.owner[up.s];
         rv.dir = 1;
         rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
@@ -823,7 +829,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
                        logits ? as.out32 : nullptr, I.n_out, r0,
-                       /*allow_split=*/split_fwd);
+                       /*allow_split=*/split_fwd && !I.v32, /*verify=*/I.v32);
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
           o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
@@ -889,12 +895,12 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           }
           // act' of the layer below, recovered from the activation it produced
           // (= this layer's input x).
-          const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld;
+          const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld * I.sc;
           Impl::Op o{OK::dgrad};
           o.stream = s;
           if (!c.plan_only)
           o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
-                           dst, d.ld_in);
+                           dst, d.ld_in, I.v32);
           push(o);
           ++kernels_per_epoch_;
         }
@@ -907,7 +913,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           o.stream = side;
           if (!c.plan_only)
           o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
-                               d.ld_in, static_cast<float>(c.lr));
+                               d.ld_in, static_cast<float>(c.lr), I.v32);
           push(o);
           ++kernels_per_epoch_;
         }
@@ -972,8 +978,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       wait_on(Impl::kFwdSend, node.done);
       Impl::Op sd{OK::send};
       sd.stream = Impl::kFwdSend;
-      sd.src = as.out16.back() + static_cast<size_t>(node.jj0) * I.Rm * ll.ld_out;
-      sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.ld_out * 2;
+      sd.src = as.out16.back() + static_cast<size_t>(node.jj0) * I.Rm * ll.ld_out * I.sc;
+      sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.ld_out * 2 * I.sc;
       sd.peer = I.owner[s + 1];
       sd.dir = 0;
       sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
@@ -984,7 +990,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       Impl::Op sd{OK::send};
       sd.stream = Impl::kBwdSend;
       sd.src = as.dzsend;
-      sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ld_in * 2;
+      sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ld_in * 2 * I.sc;
       sd.peer = I.owner[s - 1];
       sd.dir = 1;
       sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
@@ -1058,8 +1064,12 @@ void Session::load_params(const double* flat) {
       PB_CUDA(cudaMemcpy(d.b32[0], host.data() + nw, d.out * 4, cudaMemcpyHostToDevice));
       PB_CUDA(cudaMemcpy(st.pool[c0].b32[l], host.data() + nw, d.out * 4,
                          cudaMemcpyHostToDevice));
-      launch_f32_to_bf16_rows(I.origin, d.w32[0], d.out, d.in, d.in, st.pool[c0].w16[l],
-                              d.ld_in);
+      if (I.v32)
+        launch_rows_to_f32(I.origin, d.w32[0], false, d.out, d.in, d.in,
+                           reinterpret_cast<float*>(st.pool[c0].w16[l]), d.ld_in);
+      else
+        launch_f32_to_bf16_rows(I.origin, d.w32[0], d.out, d.in, d.in, st.pool[c0].w16[l],
+                                d.ld_in);
       // keep the odd master in sync so an M-odd rebase copy is always valid
       PB_CUDA(cudaMemcpyAsync(d.w32[1], d.w32[0], nw * 4, cudaMemcpyDeviceToDevice, I.origin));
       PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
@@ -1071,7 +1081,7 @@ void Session::load_params(const double* flat) {
       for (int l = 0; l < st.L; ++l) {
         auto& d = st.layers[l];
         PB_CUDA(cudaMemcpyAsync(st.pool[cM].w16[l], st.pool[c0].w16[l],
-                                sizeof(__nv_bfloat16) * d.out * static_cast<size_t>(d.ld_in),
+                                sizeof(__nv_bfloat16) * I.sc * d.out * static_cast<size_t>(d.ld_in),
                                 cudaMemcpyDeviceToDevice, I.origin));
         PB_CUDA(cudaMemcpyAsync(st.pool[cM].b32[l], st.pool[c0].b32[l], 4 * d.out,
                                 cudaMemcpyDeviceToDevice, I.origin));
@@ -1142,12 +1152,20 @@ void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
   const int in = cfg_.widths.front();
   if (xt == HostDType::f64) {
     PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 8, cudaMemcpyHostToDevice, st));
-    launch_convert_f64_bf16(st, static_cast<const double*>(I.stage_buf), static_cast<int>(rows),
-                            in, in, I.x16, I.ld_x);
+    if (I.v32)
+      launch_rows_to_f32(st, I.stage_buf, true, static_cast<int>(rows), in, in,
+                         reinterpret_cast<float*>(I.x16), I.ld_x);
+    else
+      launch_convert_f64_bf16(st, static_cast<const double*>(I.stage_buf), static_cast<int>(rows),
+                              in, in, I.x16, I.ld_x);
   } else if (xt == HostDType::f32) {
     PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 4, cudaMemcpyHostToDevice, st));
-    launch_convert_f32_bf16(st, static_cast<const float*>(I.stage_buf), static_cast<int>(rows),
-                            in, in, I.x16, I.ld_x);
+    if (I.v32)
+      launch_rows_to_f32(st, I.stage_buf, false, static_cast<int>(rows), in, in,
+                         reinterpret_cast<float*>(I.x16), I.ld_x);
+    else
+      launch_convert_f32_bf16(st, static_cast<const float*>(I.stage_buf), static_cast<int>(rows),
+                              in, in, I.x16, I.ld_x);
   } else {
     throw std::invalid_argument("x must be f64 or f32");
   }
@@ -1202,11 +1220,11 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::wgrad: launch_wgrad(o.g, s); break;
       case OK::bias:
         launch_bias_sgd(s, o.dz, o.rows, o.cols, o.ld, o.b_cur, o.b_new, o.b_copy, o.lr,
-                        o.tag_slot, o.cur_version, o.version, o.trace_src, o.trace_dst);
+                        o.tag_slot, o.cur_version, o.version, o.trace_src, o.trace_dst, I.v32);
         break;
       case OK::loss:
         launch_loss(s, o.y, o.rows, o.cols, o.ld, o.t, o.ld_t, o.loss, o.act_last, o.denom,
-                    o.dz_out, o.ld_dz, o.row_loss);
+                    o.dz_out, o.ld_dz, o.row_loss, I.v32);
         break;
       case OK::copy:
         PB_CUDA(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, s));

@@ -65,6 +65,9 @@ struct SessionConfig {
   // multi-process stage split: 0 NCCL send/recv, 1 CUDA IPC peer memory
   // (ipc_p2p.hpp; also works for several processes sharing one GPU)
   int transport = 0;
+  // fp32 verify precision: CUDA-core FFMA GEMMs on fp32 activations, deltas
+  // and weight versions (verify_fp32.cu) instead of bf16 tensor cores
+  bool verify_fp32 = false;
 };
 
 // One point-to-point transfer of the program, in this process's issue order.

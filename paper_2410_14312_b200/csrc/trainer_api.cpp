@@ -109,7 +109,8 @@ std::string cache_key(const train_config& cfg, train_mode mode, bool snaps, int 
 std::shared_ptr<SessionHandle> session_for(const train_config& cfg, train_mode mode, bool snaps,
                                            int* units) {
   const b200::options opt = b200::get_options();
-  const std::string key = cache_key(cfg, mode, snaps, opt.device, opt.use_graph);
+  const std::string key =
+      cache_key(cfg, mode, snaps, opt.device, opt.use_graph) + (opt.verify_fp32 ? "|fp32" : "");
   std::lock_guard<std::mutex> lk(g_cache_mu);
   auto it = g_cache.find(key);
   *units = mode == train_mode::timeprest ? cfg.micro_batches : 1;
@@ -131,6 +132,7 @@ std::shared_ptr<SessionHandle> session_for(const train_config& cfg, train_mode m
   tc.device = opt.device;
   tc.use_graph = opt.use_graph ? 1 : 0;
   tc.snapshots = snaps ? 1 : 0;
+  tc.precision = opt.verify_fp32 ? PB_PRECISION_FP32_VERIFY : PB_PRECISION_BF16;
   auto h = std::make_shared<SessionHandle>();
   ok(pb_session_create(&net, &tc, &h->s));
   g_cache[key] = h;

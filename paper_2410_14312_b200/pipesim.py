@@ -580,6 +580,7 @@ def format_double(v: float) -> str:
 # ------------------------------------------------------------ GPU sessions
 TIMED_KERNELS = (None, "fwd", "dgrad", "wgrad")
 TRANSPORTS = ("nccl", "ipc")
+PRECISIONS = ("bf16", "fp32")  # bf16 tensor cores / fp32 FFMA verify mode
 
 
 class Session:
@@ -589,7 +590,7 @@ class Session:
     def __init__(self, net: NetworkSpec, workers, micro_batches, mini_batch_size,
                  mini_batches, learning_rate, mode="timeprest", device=0, use_graph=True,
                  snapshots=False, fwd_merge=0, rank=0, world=1, nccl_ids=b"",
-                 timed_kernel=None, transport="nccl"):
+                 timed_kernel=None, transport="nccl", precision="bf16"):
         if mode not in TRAIN_MODES:
             raise DomainError(f"unknown training mode: {mode}", "mode")
         self.net = net
@@ -600,7 +601,7 @@ class Session:
                               float(learning_rate), TRAIN_MODES.index(mode), device,
                               int(use_graph), int(snapshots), int(fwd_merge),
                               TIMED_KERNELS.index(timed_kernel),
-                              TRANSPORTS.index(transport))
+                              TRANSPORTS.index(transport), PRECISIONS.index(precision))
         spec = net._c()
         h = C.c_void_p()
         if world > 1:
@@ -806,12 +807,13 @@ class b200:
     use_graph = True
     digest = "automatic"         # "automatic" | "every_mini" | "final_only"
     digest_auto_limit = 4_000_000
+    precision = "bf16"           # "bf16" (tensor cores) | "fp32" (FFMA verify mode)
 
 
 def _session_for(cfg: TrainConfig, mode: str, snapshots: bool) -> Session:
     key = (tuple(cfg.net.widths), tuple(cfg.net.activations), cfg.net.loss, cfg.workers,
            cfg.micro_batches, cfg.mini_batch_size, cfg.mini_batches, float(cfg.learning_rate),
-           mode, snapshots, b200.device, b200.use_graph)
+           mode, snapshots, b200.device, b200.use_graph, b200.precision)
     s = _SESSIONS.get(key)
     if s is None:
         if len(_SESSIONS) > 8:
@@ -820,7 +822,7 @@ def _session_for(cfg: TrainConfig, mode: str, snapshots: bool) -> Session:
             _SESSIONS.clear()
         s = Session(cfg.net, cfg.workers, cfg.micro_batches, cfg.mini_batch_size,
                     cfg.mini_batches, cfg.learning_rate, mode, b200.device, b200.use_graph,
-                    snapshots)
+                    snapshots, precision=b200.precision)
         _SESSIONS[key] = s
     return s
 
