@@ -90,6 +90,7 @@ struct Session::Impl {
     int* cur_version = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // wgrad/bias of a backward run beside the dgrad chain
+    cudaStream_t bstream = nullptr;  // backwards (split mode; forwards keep `stream`)
     int64_t param_offset = 0, param_count = 0;
   };
 
@@ -104,6 +105,7 @@ struct Session::Impl {
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
+  static constexpr int kBwdBase = -1000;  // backward stream of stage s (split mode)
   struct Op {
     OpKind kind;
     int stream = 0;  // stage index (0-based); -1 = origin stream
@@ -143,6 +145,8 @@ struct Session::Impl {
   // in the same layout; sc = bf16 slots per stored element (1 or 2)
   bool v32 = false;
   int sc = 1;
+  // forwards and backwards of a stage on separate streams (split mode)
+  bool split_fb = false;
   std::vector<Stage> stages;
   // data
   __nv_bfloat16* x16 = nullptr;
@@ -192,6 +196,7 @@ struct Session::Impl {
   bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
   cudaStream_t stream_of(int idx) const {
     if (idx >= 0) return stages[idx].stream;
+    if (idx <= kBwdBase) return stages[kBwdBase - idx].bstream;
     if (idx <= kSideBase) return stages[kSideBase - idx].side;
     if (idx == -1) return origin;
     return comm[-idx - 2];
@@ -223,6 +228,7 @@ struct Session::Impl {
     for (Stage& s : stages) {
       if (s.stream) cudaStreamDestroy(s.stream);
       if (s.side) cudaStreamDestroy(s.side);
+      if (s.bstream) cudaStreamDestroy(s.bstream);
     }
     if (origin) cudaStreamDestroy(origin);
     for (cudaStream_t c : comm)
@@ -263,6 +269,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   Impl& I = *impl_;
   I.plan_only = c.plan_only;
   I.v32 = c.verify_fp32;
+  I.split_fb = c.split_fb;
+  if (const char* e = std::getenv("PIPESIM_SPLIT_FB")) I.split_fb = std::atoi(e) != 0;
   I.sc = c.verify_fp32 ? 2 : 1;
   I.W = c.W;
   I.N = c.N;
@@ -521,6 +529,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].stream, cudaStreamNonBlocking, ps));
       if (c.side_streams)
         PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].side, cudaStreamNonBlocking, pside));
+      if (I.split_fb)
+        PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].bstream, cudaStreamNonBlocking, ps));
     }
   if (c.world > 1) {
     for (cudaStream_t& cs : I.comm) PB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -611,6 +621,20 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
   if (const char* e = std::getenv("PIPESIM_SESSION_SPLIT")) split_fwd = std::atoi(e) != 0;
 
+  // per stage: pool colour of every version; previous occupant of each
+  // mini-batch's activation slot (0: none)
+  std::vector<std::vector<int>> stage_version_colour(W), act_prev_occupant(W);
+  for (int s0 = 0; s0 < W; ++s0) {
+    stage_version_colour[s0] = I.stages[s0].version_colour;
+    act_prev_occupant[s0].assign(M + 1, 0);
+    std::map<int, int> last;
+    for (int k = 1; k <= M; ++k) {
+      auto it = last.find(I.stages[s0].mini_act[k]);
+      act_prev_occupant[s0][k] = it == last.end() ? 0 : it->second;
+      last[I.stages[s0].mini_act[k]] = k;
+    }
+  }
+
   // ---------------- program: coalesce forwards, order the task DAG
   // A node is one backward task, or a run of consecutive forward tasks of one
   // stage with the same mini-batch and the same pinned version (coalesced
@@ -627,7 +651,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   std::vector<Node> nodes;
   const int merge = c.fwd_merge > 0 ? c.fwd_merge : U;
   {
-    std::vector<int> open(W, -1), last_on_stage(W, -1);
+    // last_on_stage: stream-order predecessor (split mode: per kind)
+    std::vector<int> open(W, -1), last_on_stage(W, -1), last_fwd(W, -1), last_bwd(W, -1);
     std::map<std::tuple<int, int, int>, int> fwd_node;  // (k, jj, s) -> node
     std::map<std::pair<int, int>, int> bwd_node;         // (k, s) -> node
     int order = 0;
@@ -643,19 +668,67 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           continue;
         }
         Node n{true, s, tk.k, tk.version, tk.jj, tk.jj, order, {}};
-        if (last_on_stage[s] >= 0) n.deps.push_back(last_on_stage[s]);
+        const int pred = I.split_fb ? last_fwd[s] : last_on_stage[s];
+        if (pred >= 0) n.deps.push_back(pred);
         nodes.push_back(n);
         const int id = static_cast<int>(nodes.size()) - 1;
-        open[s] = last_on_stage[s] = id;
+        open[s] = last_on_stage[s] = last_fwd[s] = id;
         fwd_node[{tk.k, tk.jj, s}] = id;
       } else {
-        open[s] = -1;
+        // a backward ends a coalescing run unless forwards have their own
+        // stream (then a run may span it: same mini, same pinned version)
+        if (!I.split_fb) open[s] = -1;
         Node n{false, s, tk.k, tk.version, 0, 0, order, {}};
-        if (last_on_stage[s] >= 0) n.deps.push_back(last_on_stage[s]);
+        const int pred = I.split_fb ? last_bwd[s] : last_on_stage[s];
+        if (pred >= 0) n.deps.push_back(pred);
         nodes.push_back(n);
         const int id = static_cast<int>(nodes.size()) - 1;
-        last_on_stage[s] = id;
+        last_on_stage[s] = last_bwd[s] = id;
         bwd_node[{tk.k, s}] = id;
+      }
+    }
+    if (I.split_fb) {
+      // Split mode: the hazards the single stage stream ordered by slot are
+      // explicit edges (all point forward in slot order, so the DAG stays
+      // acyclic):
+      //  (a) a forward reads its pinned version v: after the commit of v on
+      //      this stage (the backward of mini v);
+      //  (b) the first forward of mini k writes activation slot colour(k):
+      //      after the backward of the slot's previous occupant;
+      //  (c) the backward of mini k reads mini k's activations: after the
+      //      last forward of mini k on this stage;
+      //  (d) the commit of version k overwrites pool colour(k): after the
+      //      last forward that read the colour's previous version.
+      std::map<std::pair<int, int>, int> last_fwd_of_mini, last_reader, first_fwd;
+      for (int i = 0; i < static_cast<int>(nodes.size()); ++i) {
+        const Node& n = nodes[i];
+        if (!n.fwd) continue;
+        last_fwd_of_mini[{n.k, n.s}] = i;
+        last_reader[{n.version, n.s}] = i;
+        if (!first_fwd.count({n.k, n.s})) first_fwd[{n.k, n.s}] = i;
+      }
+      for (int i = 0; i < static_cast<int>(nodes.size()); ++i) {
+        Node& n = nodes[i];
+        const auto& colour = stage_version_colour[n.s];
+        if (n.fwd) {
+          if (n.version >= 1) n.deps.push_back(bwd_node.at({n.version, n.s}));  // (a)
+          if (first_fwd.at({n.k, n.s}) == i) {                                  // (b)
+            const int pk = act_prev_occupant[n.s][n.k];
+            if (pk > 0) n.deps.push_back(bwd_node.at({pk, n.s}));
+          }
+        } else {
+          n.deps.push_back(last_fwd_of_mini.at({n.k, n.s}));  // (c)
+          int prev_v = -1;                                     // (d)
+          for (int v = n.k - 1; v >= 0; --v)
+            if (colour[v] == colour[n.k]) {
+              prev_v = v;
+              break;
+            }
+          if (prev_v >= 0) {
+            auto it = last_reader.find({prev_v, n.s});
+            if (it != last_reader.end()) n.deps.push_back(it->second);
+          }
+        }
       }
     }
     for (Node& n : nodes) {
@@ -746,6 +819,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     tk.version = node.version;
     const int a = st.mini_act[tk.k];
     Impl::ActSlot& as = st.acts[a];
+    // the node's stream: the stage stream, or (split mode) the stage's
+    // backward stream for a backward
+    const int ns = (!node.fwd && I.split_fb) ? Impl::kBwdBase - s : s;
     auto wait_on = [&](int stream, cudaEvent_t ev) {
       Impl::Op w{OK::wait};
       w.stream = stream;
@@ -760,9 +836,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       return r.ev;
     };
     for (int d : node.deps) {
-      if (nodes[d].s == s) continue;  // same-stage order is the stream order
+      // same-stage order is the stream order (same kind, or one stream per stage)
+      if (nodes[d].s == s && (nodes[d].fwd == node.fwd || !I.split_fb)) continue;
       if (I.local(nodes[d].s)) {
-        wait_on(s, nodes[d].done);
+        wait_on(ns, nodes[d].done);
         continue;
       }
       const Node& up = nodes[d];
@@ -783,7 +860,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           push(rv);
           it = fwd_recv_done.emplace(d, record_on(Impl::kFwdRecv)).first;
         }
-        wait_on(s, it->second);
+        wait_on(ns, it->second);
       } else {
         // delta of the remote downstream stage -> this slot's dzin; the slot
         // belongs to mini k since its first forward here
@@ -796,7 +873,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         rv.dir = 1;
         rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
         push(rv);
-        wait_on(s, record_on(Impl::kBwdRecv));
+        wait_on(ns, record_on(Impl::kBwdRecv));
       }
     }
     const int node_idx = static_cast<int>(I.node_meta.size());
@@ -804,7 +881,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                                      node.fwd ? node.jj1 : 0, 0.f, 0.f});
     {
       Impl::Op mk{OK::mark};
-      mk.stream = s;
+      mk.stream = ns;
       mk.value = 2 * node_idx;
       push(mk);
     }
@@ -824,7 +901,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         const bool logits = (s == last_s) && (l == st.L - 1);
         Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
         Impl::Op o{OK::fwd};
-        o.stream = s;
+        o.stream = ns;
         if (!c.plan_only)
         o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                        logits ? nullptr : as.out16[l], d.ld_out,
@@ -844,7 +921,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       if (s == last_s) {
         // fused loss + gradient over the stacked mini-batch (trainer.cpp:461-473)
         Impl::Op o{OK::loss};
-        o.stream = s;
+        o.stream = ns;
         o.y = as.out32;
         o.rows = c.B;
         o.cols = I.n_out;
@@ -867,7 +944,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       // exists, overlapping the dgrad chain of the layers below (which only
       // needs dZ); joined back before the task completes.
       const int side = c.side_streams ? Impl::kSideBase - s : s;
-      if (c.side_streams) wait_on(side, record_on(s));
+      if (c.side_streams) wait_on(side, record_on(ns));
       for (int l = st.L - 1; l >= 0; --l) {
         const auto& d = st.layers[l];
         __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
@@ -897,7 +974,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           // (= this layer's input x).
           const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld * I.sc;
           Impl::Op o{OK::dgrad};
-          o.stream = s;
+          o.stream = ns;
           if (!c.plan_only)
           o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
                            dst, d.ld_in, I.v32);
@@ -941,14 +1018,14 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         }
         // dZ_{l-1} (written by this iteration's dgrad on the main stream) is
         // what the side stream needs next
-        if (c.side_streams && l > 0) wait_on(side, record_on(s));
+        if (c.side_streams && l > 0) wait_on(side, record_on(ns));
       }
-      if (c.side_streams) wait_on(s, record_on(side));  // join
+      if (c.side_streams) wait_on(ns, record_on(side));  // join
       if (c.snapshots && !c.plan_only) {
         for (int l = 0, po = 0; l < st.L; ++l) {
           const auto& d = st.layers[l];
           Impl::Op o{OK::snapshot};
-          o.stream = s;
+          o.stream = ns;
           o.dst = I.snaps[s][tk.k] + po;
           o.src = d.w32[nxt];
           o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
@@ -962,13 +1039,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       }
     }
     Impl::Op r{OK::record};
-    r.stream = s;
+    r.stream = ns;
     r.ev = I.new_event();
     node.done = r.ev;
     push(r);
     {
       Impl::Op mk{OK::mark};
-      mk.stream = s;
+      mk.stream = ns;
       mk.value = 2 * node_idx + 1;
       push(mk);
     }
@@ -1197,6 +1274,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
     if (I.local(static_cast<int>(i))) {
       streams.push_back(I.stages[i].stream);
       if (I.stages[i].side) streams.push_back(I.stages[i].side);
+      if (I.stages[i].bstream) streams.push_back(I.stages[i].bstream);
     }
   for (cudaStream_t c : I.comm)
     if (c) streams.push_back(c);

@@ -68,6 +68,9 @@ struct SessionConfig {
   // fp32 verify precision: CUDA-core FFMA GEMMs on fp32 activations, deltas
   // and weight versions (verify_fp32.cu) instead of bf16 tensor cores
   bool verify_fp32 = false;
+  // forwards and backwards of a stage on separate streams, with the slot
+  // order's hazards as explicit events (PIPESIM_SPLIT_FB overrides)
+  bool split_fb = true;
 };
 
 // One point-to-point transfer of the program, in this process's issue order.
