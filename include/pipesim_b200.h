@@ -207,7 +207,8 @@ int pb_convert_f32_to_bf16(void* stream, const float* src, int rows, int cols,
 typedef struct pb_session pb_session;
 
 enum { PB_TRAIN_TIMEPREST = 0, PB_TRAIN_PIPEDREAM = 1, PB_TRAIN_SEQUENTIAL = 2 };
-enum { PB_DTYPE_F64 = 0, PB_DTYPE_F32 = 1, PB_DTYPE_LABELS_I32 = 2 };
+enum { PB_DTYPE_F64 = 0, PB_DTYPE_F32 = 1, PB_DTYPE_LABELS_I32 = 2,
+       PB_DTYPE_BF16 = 3 /* x only: bf16 rows (RNE-rounded), bf16 precision sessions */ };
 
 typedef struct {
   int workers;          /* W (stages) */

@@ -37,6 +37,7 @@ pb::HostDType dtype(int d) {
     case PB_DTYPE_F64: return pb::HostDType::f64;
     case PB_DTYPE_F32: return pb::HostDType::f32;
     case PB_DTYPE_LABELS_I32: return pb::HostDType::labels_i32;
+    case PB_DTYPE_BF16: return pb::HostDType::bf16;
     default: throw std::invalid_argument("bad dtype " + std::to_string(d));
   }
 }
@@ -232,8 +233,7 @@ int pb_session_train_epoch(pb_session* s, const void* x, int x_dtype,
                            const void* y, int y_dtype, pb_epoch_out* out) {
   PB_GUARD_BEGIN
   pb::Session& ss = S(s);
-  ss.upload(x, dtype(x_dtype), y, dtype(y_dtype));
-  const pb::EpochResult r = ss.run_epoch();
+  const pb::EpochResult r = ss.train_epoch_host(x, dtype(x_dtype), y, dtype(y_dtype));
   fill(r, ss, out);
   PB_GUARD_END
 }

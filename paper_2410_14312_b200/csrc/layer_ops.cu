@@ -569,18 +569,20 @@ __global__ void __launch_bounds__(256)
     loss_kernel(const float* __restrict__ y, int rows, int cols, int ld_y,
                 const float* __restrict__ t, int ld_t, int loss, int act_last,
                 float denom, TZ* __restrict__ dz, int ld_dz,
-                float* __restrict__ row_loss) {
+                float* __restrict__ row_loss, const int* __restrict__ labels) {
   __shared__ float red[8];
   const int row = blockIdx.x;
   if (row >= rows) return;
   const float* yr = y + static_cast<size_t>(row) * ld_y;
-  const float* tr = t + static_cast<size_t>(row) * ld_t;
+  // targets: dense rows, or class labels (one-hot implied, never materialised)
+  const float* tr = labels ? nullptr : t + static_cast<size_t>(row) * ld_t;
+  const int lab = labels ? labels[row] : -1;
   TZ* dr = dz + static_cast<size_t>(row) * ld_dz;
   float acc = 0.f;
   if (loss == 0) {  // mse
     for (int c = threadIdx.x; c < cols; c += blockDim.x) {
       const float yv = yr[c];
-      const float d = yv - tr[c];
+      const float d = yv - (tr ? tr[c] : (c == lab ? 1.f : 0.f));
       acc += d * d;
       float g = 2.f * d / denom;
       if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(256)
     for (int c = threadIdx.x; c < cols; c += blockDim.x) {
       const float yv = yr[c];
       const float z = yv - mx;
-      const float tc = tr[c];
+      const float tc = tr ? tr[c] : (c == lab ? 1.f : 0.f);
       if (tc > 0.5f) acc += -(z - lse) * tc;
       float g = (expf(z) / se - tc) / denom;
       if (act_last != kLinear) g *= act_grad_from_out(yv, act_last);
@@ -610,29 +612,38 @@ __global__ void __launch_bounds__(256)
 
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
-                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss, bool dz_f32) {
+                 float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss, bool dz_f32,
+                 const int* labels) {
   if (rows <= 0) return;
   const int threads = cols >= 256 ? 256 : (cols >= 128 ? 128 : 64);
   if (dz_f32)
     loss_kernel<float><<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss,
                                                  act_last, denom, reinterpret_cast<float*>(dz),
-                                                 ld_dz, row_loss);
+                                                 ld_dz, row_loss, labels);
   else
     loss_kernel<__nv_bfloat16><<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss,
-                                                         act_last, denom, dz, ld_dz, row_loss);
+                                                         act_last, denom, dz, ld_dz, row_loss,
+                                                         labels);
   PB_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------------ conversions
+// Row-major conversion to bf16: blocks stride over rows, threads over
+// columns (no per-element index division; coalesced on both sides).
 template <typename T>
 __global__ void to_bf16_kernel(const T* __restrict__ src, int rows, int cols,
                                int ld_src, __nv_bfloat16* __restrict__ dst,
                                int ld_dst) {
-  const size_t n = static_cast<size_t>(rows) * cols;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-       i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / cols, c = i % cols;
-    dst[r * ld_dst + c] = __float2bfloat16_rn(static_cast<float>(src[r * ld_src + c]));
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const T* s = src + static_cast<size_t>(r) * ld_src;
+    __nv_bfloat16* d = dst + static_cast<size_t>(r) * ld_dst;
+    for (int c = 2 * threadIdx.x; c < cols; c += 2 * blockDim.x) {
+      if (c + 1 < cols)
+        *reinterpret_cast<__nv_bfloat162*>(d + c) =
+            __floats2bfloat162_rn(static_cast<float>(s[c]), static_cast<float>(s[c + 1]));
+      else
+        d[c] = __float2bfloat16_rn(static_cast<float>(s[c]));
+    }
   }
 }
 
@@ -655,16 +666,22 @@ int grid_for(size_t n) {
 void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
                              int cols, int ld_src, __nv_bfloat16* dst,
                              int ld_dst) {
-  to_bf16_kernel<double><<<grid_for(static_cast<size_t>(rows) * cols), 256, 0, st>>>(
-      src, rows, cols, ld_src, dst, ld_dst);
+  if (rows <= 0 || cols <= 0) return;
+  if ((ld_dst % 2) != 0) throw std::invalid_argument("bf16 rows must be 4-byte aligned");
+  to_bf16_kernel<double><<<std::min(rows, 64), 256, 0, st>>>(src, rows, cols, ld_src, dst,
+                                                            ld_dst);
   PB_CUDA(cudaGetLastError());
 }
 
 void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
                              int cols, int ld_src, __nv_bfloat16* dst,
                              int ld_dst) {
-  to_bf16_kernel<float><<<grid_for(static_cast<size_t>(rows) * cols), 256, 0, st>>>(
-      src, rows, cols, ld_src, dst, ld_dst);
+  if (rows <= 0 || cols <= 0) return;
+  if ((ld_dst % 2) != 0) throw std::invalid_argument("bf16 rows must be 4-byte aligned");
+  // a few blocks: the conversion streams beside the pipeline's GEMMs
+  // (a full-GPU grid of short blocks stalled them; measured)
+  to_bf16_kernel<float><<<std::min(rows, 64), 256, 0, st>>>(src, rows, cols, ld_src, dst,
+                                                           ld_dst);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -87,7 +87,7 @@ void init_gemm_attributes();
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
                  float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss,
-                 bool dz_f32 = false);
+                 bool dz_f32 = false, const int* labels = nullptr);
 
 void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
                              int cols, int ld_src, __nv_bfloat16* dst,

@@ -101,7 +101,7 @@ struct Session::Impl {
   };
 
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
-                      send, recv, mark, ktime };
+                      send, recv, mark, ktime, xwait };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
@@ -125,6 +125,7 @@ struct Session::Impl {
     // loss
     const float* y = nullptr;
     const float* t = nullptr;
+    const int* lab = nullptr;
     int ld_t = 0, loss = 0, act_last = 0, ld_dz = 0;
     float lr = 0.f;
     float denom = 1.f;
@@ -152,6 +153,9 @@ struct Session::Impl {
   __nv_bfloat16* x16 = nullptr;
   int ld_x = 0;
   float* y32 = nullptr;
+  int* ylab = nullptr;        // class labels [rows] (labels upload: one-hot never materialised)
+  bool use_labels = false;    // the last upload's targets were labels
+  int graph_labels = -1;      // use_labels the resident graph was captured with
   int n_out = 0;
   void* stage_buf = nullptr;  // upload staging (f64 or f32 or i32)
   size_t stage_bytes = 0;
@@ -182,6 +186,25 @@ struct Session::Impl {
   std::vector<cudaEvent_t> mark_ev;  // [2 * nodes], created on first profile
   bool profiling = false;
   std::vector<cudaEvent_t> kt_ev;  // [2 * timed launches]
+  // streamed input (train_epoch from host buffers): the H2D copy and
+  // conversion of mini-batch k's rows run on their own stream inside the
+  // epoch; stage 1's forwards and the loss of mini k wait for x_ready[k]
+  struct HostInput {
+    const void* x = nullptr;
+    const void* y = nullptr;
+    HostDType xt = HostDType::f32, yt = HostDType::f32;
+    bool operator==(const HostInput& o) const {
+      return x == o.x && y == o.y && xt == o.xt && yt == o.yt;
+    }
+  };
+  bool streaming = false;          // the program being issued uploads its input
+  HostInput host_in;               // of the streamed graph
+  cudaStream_t h2d = nullptr;   // copies (back to back on the copy engine)
+  cudaStream_t h2dc = nullptr;  // conversions (high priority)
+  std::vector<cudaEvent_t> x_ready, copy_ev;  // [M + 1]
+  cudaGraph_t sgraph = nullptr;
+  cudaGraphExec_t sexec = nullptr;
+  HostInput sgraph_key;  // host buffers the streamed graph was captured with
   std::vector<double> kt_flops;    // [timed launches] 2*M*N*K
   std::unique_ptr<P2P> p2p;
   // IPC peer-memory transport (SessionConfig::transport == 1)
@@ -215,6 +238,10 @@ struct Session::Impl {
   }
 
   ~Impl() {
+    if (sexec) cudaGraphExecDestroy(sexec);
+    if (sgraph) cudaGraphDestroy(sgraph);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (h2dc) cudaStreamDestroy(h2dc);
     for (cudaEvent_t e : mark_ev)
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : kt_ev)
@@ -454,8 +481,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     if (s == W - 1) need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
   }
   const size_t rows = static_cast<size_t>(M) * c.B;
-  need += bytes_of(rows * I.ld_x, 2 * I.sc) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4);
-  I.stage_bytes = rows * std::max<size_t>(c.widths.front(), I.n_out) * 8;
+  need += bytes_of(rows * I.ld_x, 2 * I.sc) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4) +
+          bytes_of(rows, 4);
+  // upload staging: x rows (f64 at most) then y rows (f64 at most)
+  I.stage_bytes = rows * (static_cast<size_t>(c.widths.front()) + I.n_out) * 8;
   need += bytes_of(I.stage_bytes, 1);
   need += bytes_of(static_cast<size_t>(M) * U * W, 4) + bytes_of(static_cast<size_t>(M) * W, 4);
   need += 64 * kAlign;
@@ -507,6 +536,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   }
   I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x * I.sc);
   I.y32 = I.carve<float>(rows * I.n_out);
+  I.ylab = I.carve<int>(rows);
   I.row_loss = I.carve<float>(rows);
   I.stage_buf = I.carve<char>(I.stage_bytes);
   I.fwd_trace = I.carve<int>(static_cast<size_t>(M) * U * W);
@@ -876,6 +906,14 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         wait_on(ns, record_on(Impl::kBwdRecv));
       }
     }
+    // streamed input: stage 1's first forward of mini k and the loss of mini
+    // k wait for mini k's rows (no-ops when the input is resident)
+    if ((node.fwd && s == 0 && first_fwd_id.at({tk.k, 0}) == id) || (!node.fwd && s == last_s)) {
+      Impl::Op xw{OK::xwait};
+      xw.stream = ns;
+      xw.value = tk.k;
+      push(xw);
+    }
     const int node_idx = static_cast<int>(I.node_meta.size());
     I.node_meta.push_back(NodeTiming{s + 1, node.fwd ? 1 : 0, node.k, node.fwd ? node.jj0 : 0,
                                      node.fwd ? node.jj1 : 0, 0.f, 0.f});
@@ -927,6 +965,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         o.cols = I.n_out;
         o.ld = I.n_out;
         o.t = I.y32 + static_cast<size_t>(tk.k - 1) * c.B * I.n_out;
+        o.lab = I.ylab + static_cast<size_t>(tk.k - 1) * c.B;
         o.ld_t = I.n_out;
         o.loss = c.loss;
         o.act_last = st.layers.back().act;
@@ -1212,51 +1251,18 @@ void Session::read_stage_master(int stage, int parity, double* out) {
 }
 
 // ------------------------------------------------------------------ data
-__global__ void labels_to_onehot(const int* labels, int rows, int classes, float* y) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-       i < static_cast<size_t>(rows) * classes; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / classes;
-    y[i] = (labels[r] == static_cast<int>(i % classes)) ? 1.f : 0.f;
-  }
-}
+namespace {
+void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType xt,
+                 const void* y, HostDType yt, cudaStream_t st, cudaStream_t conv = nullptr,
+                 cudaEvent_t copied = nullptr);
+}  // namespace
 
 void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
                      cudaStream_t st) {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
   if (!st) st = I.origin;
-  const size_t rows = static_cast<size_t>(cfg_.M) * cfg_.B;
-  const int in = cfg_.widths.front();
-  if (xt == HostDType::f64) {
-    PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 8, cudaMemcpyHostToDevice, st));
-    if (I.v32)
-      launch_rows_to_f32(st, I.stage_buf, true, static_cast<int>(rows), in, in,
-                         reinterpret_cast<float*>(I.x16), I.ld_x);
-    else
-      launch_convert_f64_bf16(st, static_cast<const double*>(I.stage_buf), static_cast<int>(rows),
-                              in, in, I.x16, I.ld_x);
-  } else if (xt == HostDType::f32) {
-    PB_CUDA(cudaMemcpyAsync(I.stage_buf, x, rows * in * 4, cudaMemcpyHostToDevice, st));
-    if (I.v32)
-      launch_rows_to_f32(st, I.stage_buf, false, static_cast<int>(rows), in, in,
-                         reinterpret_cast<float*>(I.x16), I.ld_x);
-    else
-      launch_convert_f32_bf16(st, static_cast<const float*>(I.stage_buf), static_cast<int>(rows),
-                              in, in, I.x16, I.ld_x);
-  } else {
-    throw std::invalid_argument("x must be f64 or f32");
-  }
-  if (yt == HostDType::f64) {
-    PB_CUDA(cudaMemcpyAsync(I.stage_buf, y, rows * I.n_out * 8, cudaMemcpyHostToDevice, st));
-    launch_convert_f64_f32(st, static_cast<const double*>(I.stage_buf), I.y32, rows * I.n_out);
-  } else if (yt == HostDType::f32) {
-    PB_CUDA(cudaMemcpyAsync(I.y32, y, rows * I.n_out * 4, cudaMemcpyHostToDevice, st));
-  } else {
-    PB_CUDA(cudaMemcpyAsync(I.stage_buf, y, rows * 4, cudaMemcpyHostToDevice, st));
-    labels_to_onehot<<<1184, 256, 0, st>>>(static_cast<const int*>(I.stage_buf),
-                                            static_cast<int>(rows), I.n_out, I.y32);
-    PB_CUDA(cudaGetLastError());
-  }
+  upload_rows(I, 0, static_cast<size_t>(cfg_.M) * cfg_.B, x, xt, y, yt, st);
   if (st != I.origin) {
     cudaEvent_t e = I.new_event();
     PB_CUDA(cudaEventRecord(e, st));
@@ -1266,6 +1272,70 @@ void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
 
 // ------------------------------------------------------------------ run
 namespace {
+// Rows [r0, r0 + n) of the epoch's data: H2D into the staging buffer (x
+// region, then y region) on `st`, then conversion into the device layout on
+// `conv` (st if null; with a separate conversion stream the copies run back
+// to back on the copy engine and never wait for SMs).
+void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType xt,
+                 const void* y, HostDType yt, cudaStream_t st, cudaStream_t conv,
+                 cudaEvent_t copied) {
+  const int in = I.cfg.widths.front();
+  const size_t rows = static_cast<size_t>(I.M) * I.B;
+  char* xs = static_cast<char*>(I.stage_buf);
+  char* ys = xs + rows * in * 8;  // y region after the largest x region
+  __nv_bfloat16* xdst = I.x16 + r0 * I.ld_x * I.sc;
+  float* ydst = I.y32 + r0 * I.n_out;
+  const size_t xes = xt == HostDType::f64 ? 8 : xt == HostDType::f32 ? 4 : 2;
+  char* xb = xs + r0 * in * xes;
+  char* yb = ys + r0 * I.n_out * 8;
+  // ---- copies
+  if (xt == HostDType::bf16) {  // already the device operand type: one 2-D copy
+    if (I.v32) throw std::invalid_argument("bf16 input needs a bf16-precision session");
+    PB_CUDA(cudaMemcpy2DAsync(xdst, static_cast<size_t>(I.ld_x) * 2,
+                              static_cast<const __nv_bfloat16*>(x) + r0 * in,
+                              static_cast<size_t>(in) * 2, static_cast<size_t>(in) * 2, n,
+                              cudaMemcpyHostToDevice, st));
+  } else if (xt == HostDType::f64 || xt == HostDType::f32) {
+    PB_CUDA(cudaMemcpyAsync(xb, static_cast<const char*>(x) + r0 * in * xes, n * in * xes,
+                            cudaMemcpyHostToDevice, st));
+  } else {
+    throw std::invalid_argument("x must be f64, f32 or bf16");
+  }
+  if (yt == HostDType::f64) {
+    PB_CUDA(cudaMemcpyAsync(yb, static_cast<const char*>(y) + r0 * I.n_out * 8, n * I.n_out * 8,
+                            cudaMemcpyHostToDevice, st));
+  } else if (yt == HostDType::f32) {
+    PB_CUDA(cudaMemcpyAsync(ydst, static_cast<const float*>(y) + r0 * I.n_out, n * I.n_out * 4,
+                            cudaMemcpyHostToDevice, st));
+  } else if (yt == HostDType::labels_i32) {  // the loss kernel reads labels directly
+    PB_CUDA(cudaMemcpyAsync(I.ylab + r0, static_cast<const int*>(y) + r0, n * 4,
+                            cudaMemcpyHostToDevice, st));
+  } else {
+    throw std::invalid_argument("y must be f64, f32 or int32 labels");
+  }
+  I.use_labels = yt == HostDType::labels_i32;
+  // ---- conversions
+  cudaStream_t cs = st;
+  if (conv && conv != st) {
+    PB_CUDA(cudaEventRecord(copied, st));
+    PB_CUDA(cudaStreamWaitEvent(conv, copied, 0));
+    cs = conv;
+  }
+  if (xt == HostDType::f64 || xt == HostDType::f32) {
+    if (I.v32)
+      launch_rows_to_f32(cs, xb, xt == HostDType::f64, static_cast<int>(n), in, in,
+                         reinterpret_cast<float*>(xdst), I.ld_x);
+    else if (xt == HostDType::f64)
+      launch_convert_f64_bf16(cs, reinterpret_cast<const double*>(xb), static_cast<int>(n), in,
+                              in, xdst, I.ld_x);
+    else
+      launch_convert_f32_bf16(cs, reinterpret_cast<const float*>(xb), static_cast<int>(n), in,
+                              in, xdst, I.ld_x);
+  }
+  if (yt == HostDType::f64)
+    launch_convert_f64_f32(cs, reinterpret_cast<const double*>(yb), ydst, n * I.n_out);
+}
+
 void issue(Session::Impl& I, cudaStream_t origin) {
   using OK = Session::Impl::OpKind;
   // every stream this process drives: local stage streams + P2P streams
@@ -1278,16 +1348,22 @@ void issue(Session::Impl& I, cudaStream_t origin) {
     }
   for (cudaStream_t c : I.comm)
     if (c) streams.push_back(c);
-  if (!I.fork_ev) {
-    I.fork_ev = I.new_event();
-    for (size_t i = 0; i < streams.size(); ++i) I.join_ev.push_back(I.new_event());
-  }
+  if (I.h2d) streams.push_back(I.h2d);
+  if (I.h2dc) streams.push_back(I.h2dc);
+  if (!I.fork_ev) I.fork_ev = I.new_event();
+  while (I.join_ev.size() < streams.size()) I.join_ev.push_back(I.new_event());
   cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
   PB_CUDA(cudaStreamIsCapturing(origin, &cap_status));
   const bool capturing = cap_status != cudaStreamCaptureStatusNone;
   cudaEvent_t fork = I.fork_ev;
   PB_CUDA(cudaEventRecord(fork, origin));
   for (cudaStream_t st : streams) PB_CUDA(cudaStreamWaitEvent(st, fork, 0));
+  if (I.streaming)  // mini-batch k's rows: H2D + conversion, then x_ready[k]
+    for (int k = 1; k <= I.M; ++k) {
+      upload_rows(I, static_cast<size_t>(k - 1) * I.B, I.B, I.host_in.x, I.host_in.xt,
+                  I.host_in.y, I.host_in.yt, I.h2d, I.h2dc, I.copy_ev[k]);
+      PB_CUDA(cudaEventRecord(I.x_ready[k], I.h2dc));
+    }
   for (const auto& o : I.ops) {
     cudaStream_t s = I.stream_of(o.stream);
     switch (o.kind) {
@@ -1302,7 +1378,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         break;
       case OK::loss:
         launch_loss(s, o.y, o.rows, o.cols, o.ld, o.t, o.ld_t, o.loss, o.act_last, o.denom,
-                    o.dz_out, o.ld_dz, o.row_loss, I.v32);
+                    o.dz_out, o.ld_dz, o.row_loss, I.v32, I.use_labels ? o.lab : nullptr);
         break;
       case OK::copy:
         PB_CUDA(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, s));
@@ -1328,6 +1404,9 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::mark:
         if (I.profiling) PB_CUDA(cudaEventRecord(I.mark_ev[o.value], s));
         break;
+      case OK::xwait:
+        if (I.streaming) PB_CUDA(cudaStreamWaitEvent(s, I.x_ready[o.value], 0));
+        break;
       case OK::ktime:  // an event record node when captured
         PB_CUDA(cudaEventRecordWithFlags(I.kt_ev[o.value], s,
                                          capturing ? cudaEventRecordExternal : 0));
@@ -1350,7 +1429,14 @@ EpochResult Session::run_epoch() {
   }
   PB_CUDA(cudaEventRecord(I.t0, I.origin));
   if (cfg_.use_graph && !I.ipc) {
+    if (I.exec && I.graph_labels != static_cast<int>(I.use_labels)) {
+      cudaGraphExecDestroy(I.exec);
+      cudaGraphDestroy(I.graph);
+      I.exec = nullptr;
+      I.graph = nullptr;
+    }
     if (!I.exec) {
+      I.graph_labels = static_cast<int>(I.use_labels);
       PB_CUDA(cudaStreamBeginCapture(I.origin, cudaStreamCaptureModeThreadLocal));
       try {
         issue(I, I.origin);
@@ -1383,6 +1469,73 @@ std::vector<float> Session::kernel_times_ms() {
     out.push_back(ms);
   }
   return out;
+}
+
+EpochResult Session::train_epoch_host(const void* x, HostDType xt, const void* y,
+                                      HostDType yt) {
+  Impl& I = *impl_;
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;  // page-locked (cudaHostAlloc / registered)
+  };
+  // IPC (eager epochs) or pageable buffers (not capturable): upload, then the epoch
+  if (I.ipc || !pinned(x) || !pinned(y)) {
+    upload(x, xt, y, yt);
+    return run_epoch();
+  }
+  if (!I.h2d) {
+    int lo = 0, hi = 0;
+    PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    PB_CUDA(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking));
+    PB_CUDA(cudaStreamCreateWithPriority(&I.h2dc, cudaStreamNonBlocking, hi));
+    I.x_ready.assign(cfg_.M + 1, nullptr);
+    I.copy_ev.assign(cfg_.M + 1, nullptr);
+    for (int k = 1; k <= cfg_.M; ++k) {
+      I.x_ready[k] = I.new_event();
+      I.copy_ev[k] = I.new_event();
+    }
+  }
+  const Impl::HostInput in{x, y, xt, yt};
+  PB_CUDA(cudaEventRecord(I.t0, I.origin));
+  I.streaming = true;
+  I.host_in = in;
+  try {
+    if (cfg_.use_graph) {
+      if (!I.sexec || !(I.sgraph_key == in)) {
+        if (I.sexec) cudaGraphExecDestroy(I.sexec);
+        if (I.sgraph) cudaGraphDestroy(I.sgraph);
+        I.sexec = nullptr;
+        I.sgraph = nullptr;
+        PB_CUDA(cudaStreamBeginCapture(I.origin, cudaStreamCaptureModeThreadLocal));
+        try {
+          issue(I, I.origin);
+        } catch (...) {
+          cudaGraph_t g;
+          cudaStreamEndCapture(I.origin, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        PB_CUDA(cudaStreamEndCapture(I.origin, &I.sgraph));
+        PB_CUDA(cudaGraphInstantiate(&I.sexec, I.sgraph, 0));
+        I.sgraph_key = in;
+      }
+      PB_CUDA(cudaGraphLaunch(I.sexec, I.origin));
+    } else {
+      issue(I, I.origin);
+    }
+  } catch (...) {
+    I.streaming = false;
+    throw;
+  }
+  I.streaming = false;
+  PB_CUDA(cudaEventRecord(I.t1, I.origin));
+  PB_CUDA(cudaEventSynchronize(I.t1));
+  return collect_result();
 }
 
 EpochResult Session::profile_epoch(EpochProfile* prof) {

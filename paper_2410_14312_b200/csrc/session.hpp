@@ -32,7 +32,9 @@
 namespace pb {
 
 enum class RunMode { timeprest = 0, pipedream = 1, sequential = 2 };
-enum class HostDType { f64 = 0, f32 = 1, labels_i32 = 2 };
+// bf16: x already rounded to bf16 on the host (the bf16 path's operand type;
+// copied straight into the device layout, no conversion kernel)
+enum class HostDType { f64 = 0, f32 = 1, labels_i32 = 2, bf16 = 3 };
 
 struct SessionConfig {
   std::vector<int> widths;
@@ -136,6 +138,11 @@ class Session {
               cudaStream_t st = nullptr);
   // Runs one epoch on the uploaded data.  `epoch` only tags the result.
   EpochResult run_epoch();
+  // One epoch from host buffers with the upload streamed inside it: mini-batch
+  // k's rows are copied and converted on their own stream while earlier
+  // mini-batches compute; stage 1's forwards and the loss of mini k wait
+  // only for mini k's rows (the graph is re-captured when the buffers change).
+  EpochResult train_epoch_host(const void* x, HostDType xt, const void* y, HostDType yt);
   // Runs one epoch without the CUDA graph, with timing events around every
   // node on its stage stream: per-stage busy time, the epoch makespan and
   // the node timeline (pipeline bubble = 1 - sum(busy) / (W * makespan)).

@@ -675,6 +675,26 @@ class Session:
         N.check(_L().pb_session_upload(self._h, x.ctypes.data, self._dtype(x), y.ctypes.data,
                                        self._dtype(y, y_labels)))
 
+    def train_epoch_host(self, x_ptr: int, x_dtype: str, y_ptr: int, y_dtype: str):
+        """One epoch from host buffers (pb_session_train_epoch): with
+        page-locked buffers the upload is streamed inside the epoch (mini-batch
+        k's rows copied while earlier ones compute).  x_dtype: "f64"|"f32";
+        y_dtype: "f64"|"f32"|"labels"."""
+        M, U, W = self.M, self.units, self.W
+        r = dict(mini_loss=np.zeros(M), pinned=np.zeros(M * U, np.int32),
+                 consumed=np.zeros(M, np.int32), dev_fwd=np.zeros(M * U * W, np.int32),
+                 dev_bwd=np.zeros(M * W, np.int32), dev_current=np.zeros(W, np.int32))
+        out = pb_epoch_out(_dp(r["mini_loss"]), _ip(r["pinned"]), _ip(r["consumed"]),
+                           _ip(r["dev_fwd"]), _ip(r["dev_bwd"]), _ip(r["dev_current"]), 0.0)
+        codes = {"f64": 0, "f32": 1, "labels": 2, "bf16": 3}
+        N.check(_L().pb_session_train_epoch(self._h, C.c_void_p(x_ptr), codes[x_dtype],
+                                            C.c_void_p(y_ptr), codes[y_dtype], C.byref(out)))
+        r["device_ms"] = out.device_ms
+        r["pinned"] = r["pinned"].reshape(M, U)
+        r["dev_fwd"] = r["dev_fwd"].reshape(M, U, W)
+        r["dev_bwd"] = r["dev_bwd"].reshape(M, W)
+        return r
+
     def ipc_export(self) -> bytes:
         """This rank's IPC connection blob (transport="ipc")."""
         n = C.c_int64(0)

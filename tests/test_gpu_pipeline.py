@@ -273,3 +273,37 @@ def test_forward_coalescing_with_split_k():
     np.testing.assert_array_equal(res[0][1], res[1][1])
     d = np.linalg.norm(res[0][2] - res[1][2]) / np.linalg.norm(res[1][2])
     assert d < 1e-4
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_streamed_host_epoch_matches_resident(precision):
+    """pb_session_train_epoch from page-locked host buffers streams the upload
+    inside the epoch (per-mini-batch H2D + conversion on its own stream,
+    stage 1 and the loss wait per mini-batch); results are bit-identical to
+    upload + resident epoch, over several epochs and a buffer change."""
+    import torch
+    net = P.NetworkSpec([96, 128, 64, 10], ["relu", "tanh", "linear"], "softmax_cross_entropy")
+    W, N, B, M = 3, 4, 64, 7
+    x, lab = P.make_classification_task(M * B, 96, 10, seed=7, as_labels=True, dtype=np.float32)
+    x2 = (x[::-1] * 0.5).copy()
+    res = []
+    for streamed in (False, True):
+        s = P.Session(net, W, N, B, M, 0.05, "timeprest", precision=precision)
+        s.load_params(P.init_network_params(net, 1))
+        xs = [torch.from_numpy(a).pin_memory() for a in (x, x2)]
+        yh = torch.from_numpy(lab).pin_memory()
+        outs = []
+        for e, xh in enumerate((xs[0], xs[0], xs[1])):
+            if streamed:
+                r = s.train_epoch_host(xh.data_ptr(), "f32", yh.data_ptr(), "labels")
+            else:
+                s.upload(xh.numpy(), yh.numpy(), y_labels=True)
+                r = s.run_epoch()
+            outs.append((r["mini_loss"].copy(), r["dev_fwd"].copy()))
+        outs.append(s.read_params())
+        s.close()
+        res.append(outs)
+    for a, b in zip(res[0][:-1], res[1][:-1]):
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(res[0][-1], res[1][-1])
