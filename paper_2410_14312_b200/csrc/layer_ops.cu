@@ -115,8 +115,6 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
     int cap = sm_count() / 2;
     if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
-    if (EPI == kEpiWgradSgd)
-      if (const char* e = std::getenv("PIPESIM_WG_PAIRS")) cap = std::min(cap, std::atoi(e));
     const int pairs = std::min(tiles, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
@@ -175,8 +173,6 @@ void init_gemm_attributes() {
     set_attr<256, false, true, kEpiDgrad>();
     set_attr<128, true, true, kEpiWgradSgd>();
     set_attr<256, true, true, kEpiWgradSgd>();
-    set_attr<128, false, false, kEpiWgradSgd>();
-    set_attr<256, false, false, kEpiWgradSgd>();
   });
 }
 
@@ -249,15 +245,6 @@ int splitk_env() {
 }
 }  // namespace
 
-namespace {
-int fwd_bn_rows() {
-  static const int v = [] {
-    const char* e = std::getenv("PIPESIM_FWD_BN_ROWS");
-    return e ? std::atoi(e) : 512;
-  }();
-  return v;
-}
-}  // namespace
 
 // Split-K for skinny forwards (<= 256 rows): enough 128 x 128 tiles x splits
 // to cover the SMs, >= 8 k-blocks per split, at most kMaxSplits (4).
@@ -301,12 +288,6 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
   } else {
     g.bn = pick_bn(rows, w.rows);
     g.pair = use_pair(rows);
-    // PIPESIM_FWD_BN=128: narrower pair tiles for skinny forwards (A/B runs)
-    static const int fwd_bn = [] {
-      const char* e = std::getenv("PIPESIM_FWD_BN");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (fwd_bn == 128 && g.pair && rows <= fwd_bn_rows()) g.bn = 128;
   }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
@@ -382,19 +363,10 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
     return g;
   }
   g.bn = pick_bn(dz.cols, x.cols);
-  if (const char* e = std::getenv("PIPESIM_WG_BN")) g.bn = std::atoi(e) == 128 ? 128 : g.bn;
   g.pair = use_pair(dz.cols);
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
   g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};
-  if (const char* e = std::getenv("PIPESIM_EXP_WG"); e && std::string(e) == "kk" &&
-      dz.ld == dz.cols && x.ld == x.cols && x_row_off == 0) {
-    // same bytes reinterpreted as K-major [features][rows] (garbage math)
-    g.exp_kk = true;
-    g.ta = make_operand_tmap(Mat16{dz.ptr, dz.cols, dz.rows, dz.rows}, true, 128);
-    g.tb = make_operand_tmap(Mat16{x.ptr, x.cols, x.rows, x.rows}, true, b_box(g));
-    g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, 0};
-  }
   g.ep = empty_epi(kEpiWgradSgd);
   g.ep.w_cur = w_cur;
   g.ep.w_new = w_new;
@@ -409,7 +381,7 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
     const char* e = std::getenv("PIPESIM_EPI");
     return !(e && std::string(e) == "vec");
   }();
-  if (g.pair && g.ep.rowwise == 2 && tma_ok && !g.exp_kk && ld_w32 % 4 == 0 &&
+  if (g.pair && g.ep.rowwise == 2 && tma_ok && ld_w32 % 4 == 0 &&
       al(w_cur, 16) && al(w_new, 16) && (!w16 || (ld_w16 % 8 == 0 && al(w16, 16)))) {
     const int M = dz.cols, N = x.cols;
     g.maps.w_cur = make_epi_tmap(w_cur, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, ld_w32,
@@ -435,10 +407,6 @@ void launch_dgrad(const GemmLaunch& g, cudaStream_t st) {
 }
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
   if (g.simt) return launch_simt_gemm(g, kEpiWgradSgd, st);
-  if (g.exp_kk) {  // timing experiment (PIPESIM_EXP_WG=kk): K-major operands
-    launch_bn<false, false, kEpiWgradSgd>(g, st);
-    return;
-  }
   launch_bn<true, true, kEpiWgradSgd>(g, st);
 }
 
@@ -634,9 +602,22 @@ template <typename T>
 __global__ void to_bf16_kernel(const T* __restrict__ src, int rows, int cols,
                                int ld_src, __nv_bfloat16* __restrict__ dst,
                                int ld_dst) {
+  const bool vec4 = sizeof(T) == 4 && (cols % 4) == 0 && (ld_src % 4) == 0 && (ld_dst % 4) == 0 &&
+                    (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dst) & 7) == 0;
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const T* s = src + static_cast<size_t>(r) * ld_src;
     __nv_bfloat16* d = dst + static_cast<size_t>(r) * ld_dst;
+    if (vec4) {  // 16-byte loads, 8-byte stores
+      for (int c = 4 * threadIdx.x; c < cols; c += 4 * blockDim.x) {
+        const float4 v = *reinterpret_cast<const float4*>(s + c);
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v.z, v.w);
+        *reinterpret_cast<uint2*>(d + c) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+      }
+      continue;
+    }
     for (int c = 2 * threadIdx.x; c < cols; c += 2 * blockDim.x) {
       if (c + 1 < cols)
         *reinterpret_cast<__nv_bfloat162*>(d + c) =
@@ -668,8 +649,8 @@ void launch_convert_f64_bf16(cudaStream_t st, const double* src, int rows,
                              int ld_dst) {
   if (rows <= 0 || cols <= 0) return;
   if ((ld_dst % 2) != 0) throw std::invalid_argument("bf16 rows must be 4-byte aligned");
-  to_bf16_kernel<double><<<std::min(rows, 64), 256, 0, st>>>(src, rows, cols, ld_src, dst,
-                                                            ld_dst);
+  to_bf16_kernel<double><<<std::min(rows, 148 * 4), 256, 0, st>>>(src, rows, cols, ld_src, dst,
+                                                                  ld_dst);
   PB_CUDA(cudaGetLastError());
 }
 
@@ -678,10 +659,8 @@ void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
                              int ld_dst) {
   if (rows <= 0 || cols <= 0) return;
   if ((ld_dst % 2) != 0) throw std::invalid_argument("bf16 rows must be 4-byte aligned");
-  // a few blocks: the conversion streams beside the pipeline's GEMMs
-  // (a full-GPU grid of short blocks stalled them; measured)
-  to_bf16_kernel<float><<<std::min(rows, 64), 256, 0, st>>>(src, rows, cols, ld_src, dst,
-                                                           ld_dst);
+  to_bf16_kernel<float><<<std::min(rows, 148 * 4), 256, 0, st>>>(src, rows, cols, ld_src, dst,
+                                                                 ld_dst);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -40,7 +40,6 @@ struct GemmLaunch {
   const float* simt_b = nullptr;
   int simt_lda = 0, simt_ldb = 0;
   bool pair = false;  // persistent CTA-pair kernel
-  bool exp_kk = false;  // timing experiment only
 };
 
 // Split count of a forward GEMM of rows x N x K (1 = no split).  Splitting

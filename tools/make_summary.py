@@ -1,0 +1,110 @@
+"""Regenerates profiles/round1_summary.md from the committed artefacts:
+profiles/round1_bench.json, the launch summary of
+profiles/round1_launches_step_m4.csv, the ncu summary (argument: a
+--set full report, optional) and profiles/sweep_c5_r1.md."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = lambda *a: os.path.join(ROOT, *a)  # noqa: E731
+
+b = json.load(open(P("profiles", "round1_bench.json")))
+r = b["roofline"]
+inst = r["in_step"]
+launch = subprocess.run([sys.executable, P("tools", "launch_summary.py"),
+                         P("profiles", "round1_launches_step_m4.csv")],
+                        capture_output=True, text=True).stdout
+ncu = ""
+if len(sys.argv) > 1 and os.path.exists(sys.argv[1]):
+    ncu = subprocess.run([sys.executable, P("tools", "ncu_summary.py"), sys.argv[1]],
+                         capture_output=True, text=True).stdout
+else:
+    ncu = open(P("profiles", "ncu_round1_full.md")).read()
+sweep = open(P("profiles", "sweep_c5_r1.md")).read()
+traffic = json.load(open(P("profiles", "ncu_traffic.json")))
+
+alone = "\n".join(
+    f"| {k} | {v['us']:.1f} us | {v['tflops']:.0f} TFLOP/s"
+    + (f", {v['hbm_gbs']:.0f} GB/s" if "hbm_gbs" in v else "") + " |"
+    for k, v in r["alone"].items())
+
+txt = f"""# Round 1 — measurements (B200, 1 GPU)
+
+Sources: `profiles/round1_bench.json` (default `bench.py`: timed steps, e2e,
+CPU reference, in-step kernel timing), `profiles/round1_launches_step_m4.csv`
+(ncu launch list of `tools/prof_step.py 4`: parameter load + upload + two
+4-mini-batch epochs of the benchmark network), `profiles/ncu_round1_full.md` /
+`profiles/ncu_traffic.json` (`ncu --set full` of
+`tools/prof_gemm.py fwd256,dgrad,wgrad 1`, split-K off as in the executor),
+`profiles/sweep_c5_r1.*` (`tools/sweep.py`).  Regenerate with
+`python tools/make_summary.py`.
+
+## Bench line (16x4096 MLP, W=8 stages on 1 GPU, N=8, B=1024, M=32 per step)
+
+| quantity | value |
+|---|---|
+| samples/s (device-timed, data resident) | {b['value']:.0f} |
+| ms / step (32 768 samples, 51.7 TFLOP of GEMMs) | {b['ms_per_step']:.2f} |
+| step GEMM throughput | {r['step_gemm_tflops']:.0f} TFLOP/s = {100*r['step_frac_of_sustained']:.1f}% of measured sustained bf16 (1384) |
+| e2e samples/s (C ABI from pinned host x (bf16) + labels, H2D streamed inside the step, loss D2H) | {b['e2e']['value']:.0f} ({b['e2e']['ms_per_step']:.2f} ms/step, {b['e2e']['h2d_bytes_per_step']/1e6:.0f} MB H2D) |
+| CPU reference (compiled `pipesim`, 1 thread, box host) | {b['cpu_baseline']['value']:.4f} samples/s ({b['cpu_baseline']['sample']}) |
+| GPU / CPU | {b['value']/b['cpu_baseline']['value']:.2e} x (e2e: {b['e2e']['value']/b['cpu_baseline']['value']:.2e} x) |
+| clocks during the timed region | {b['clocks']} |
+| our kernel launches per step | {b['gpu_launches']} |
+
+## Kernels inside the step (CUDA events around every launch, recorded in the graph)
+
+| GEMM | launches / step | mean in-step duration | in-step rate |
+|---|---|---|---|
+| forward (dominant: largest share of the launch list) | {inst['fwd']['launches_per_step']} | {inst['fwd']['mean_us']:.1f} us | {inst['fwd']['tflops']:.0f} TFLOP/s |
+| dgrad | {inst['dgrad']['launches_per_step']} | {inst['dgrad']['mean_us']:.1f} us | {inst['dgrad']['tflops']:.0f} TFLOP/s |
+| wgrad + SGD | {inst['wgrad']['launches_per_step']} | {inst['wgrad']['mean_us']:.1f} us | {inst['wgrad']['tflops']:.0f} TFLOP/s, {inst['wgrad']['hbm_gbs']:.0f} GB/s of update traffic |
+
+Two to three GEMMs of different stages run concurrently on the one GPU, so an
+in-step duration includes waiting for SMs; the whole-step GEMM rate above is
+the efficiency figure.  Alone (graph-captured, weights rotated through 6
+copies so they stream from HBM):
+
+| shape | alone | rate |
+|---|---|---|
+{alone}
+
+cuBLAS (torch.mm bf16, same harness, no fused epilogues): fwd 256 rows 11.1 us,
+1024 rows 25.3 us; dgrad 25.3 us; plain wgrad GEMM 27.3 us.
+
+## Kernel share (ncu launch list; serialised, cold caches: compare shares)
+
+The list covers a short session's setup (parameter load: `to_bf16_kernel`)
+as well as two epochs; the step itself is the three GEMMs, bias and loss.
+
+```
+{launch}```
+
+## Dominant kernels, `ncu --set full`
+
+{ncu}
+Algorithmic versus measured DRAM traffic per launch (`profiles/ncu_traffic.json`):
+- **fwd 256x4096x4096**: W 32 MiB + X 2 MiB + Y 2 MiB = 35.7 MB; measured {traffic['fwd_256x4096x4096']['bytes']/1e6:.2f} MB — no re-reads.
+- **dgrad 1024x4096x4096**: dZ 8 MiB + W 32 MiB + stored activation (act' gate) 8 MiB + out 8 MiB = 58.7 MB; measured {traffic['dgrad_1024x4096x4096']['bytes']/1e6:.1f} MB (the written delta stays in L2).
+- **wgrad+SGD 4096x4096x1024**: dZ 8 MiB + X 8 MiB + fp32 master read 64 MiB + write 64 MiB + bf16 write 32 MiB = 184 MB; measured {traffic['wgrad_sgd_4096x4096x1024']['bytes']/1e6:.1f} MB (the rest of the new masters is still in L2 when the kernel ends).
+
+## C5 sweep: version difference, throughput and bubble per (W, N)
+
+16x4096 MLP, B = 128 N, M = 2(W+N), all W stages on one GPU.  `bubble` is
+stage-stream occupancy on one GPU (1 - sum busy / (W makespan)); the slot
+model's idle fraction is the reference metric (metrics.cpp:71-72).
+
+{sweep}
+## This round's changes (alone timings / step, before -> after)
+
+- activation as a compile-time epilogue parameter (the runtime switch inside unrolled loops doubled the code): fwd 1024 rows 41.5 -> 28.7 us.
+- vector staged-transpose epilogue: wgrad+SGD 68 -> 57.6 us (same ring depth).
+- TMA epilogue for the SGD update: 57.6 -> 48.3 us.
+- separate forward / backward streams per stage (explicit hazard edges), forward runs spanning another mini-batch's backward: 1238 -> 992 forward launches per step, 525k -> 556k samples/s.
+- e2e: per-mini-batch H2D streamed inside the epoch, labels read by the loss kernel (no one-hot), bf16 host x: e2e 449k -> {b['e2e']['value']/1000:.0f}k samples/s.
+- step: 68.5 ms (478k samples/s) at the start of this session -> {b['ms_per_step']:.1f} ms ({b['value']/1000:.0f}k samples/s).
+"""
+open(P("profiles", "round1_summary.md"), "w").write(txt)
+print("written")
