@@ -91,6 +91,7 @@ struct Session::Impl {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // wgrad/bias of a backward run beside the dgrad chain
     cudaStream_t bstream = nullptr;  // backwards (split mode; forwards keep `stream`)
+    cudaStream_t biasstream = nullptr;  // bias gradient + SGD of a backward
     int64_t param_offset = 0, param_count = 0;
   };
 
@@ -106,6 +107,7 @@ struct Session::Impl {
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
   static constexpr int kBwdBase = -1000;  // backward stream of stage s (split mode)
+  static constexpr int kBiasBase = -2000;  // bias-gradient stream of stage s
   struct Op {
     OpKind kind;
     int stream = 0;  // stage index (0-based); -1 = origin stream
@@ -148,6 +150,8 @@ struct Session::Impl {
   int sc = 1;
   // forwards and backwards of a stage on separate streams (split mode)
   bool split_fb = false;
+  // bias gradients on their own stream (else on the wgrad side stream)
+  bool bias_stream = true;
   std::vector<Stage> stages;
   // data
   __nv_bfloat16* x16 = nullptr;
@@ -219,6 +223,7 @@ struct Session::Impl {
   bool local(int s0) const { return s0 >= W_lo - 1 && s0 <= W_hi - 1; }
   cudaStream_t stream_of(int idx) const {
     if (idx >= 0) return stages[idx].stream;
+    if (idx <= kBiasBase) return stages[kBiasBase - idx].biasstream;
     if (idx <= kBwdBase) return stages[kBwdBase - idx].bstream;
     if (idx <= kSideBase) return stages[kSideBase - idx].side;
     if (idx == -1) return origin;
@@ -256,6 +261,7 @@ struct Session::Impl {
       if (s.stream) cudaStreamDestroy(s.stream);
       if (s.side) cudaStreamDestroy(s.side);
       if (s.bstream) cudaStreamDestroy(s.bstream);
+      if (s.biasstream) cudaStreamDestroy(s.biasstream);
     }
     if (origin) cudaStreamDestroy(origin);
     for (cudaStream_t c : comm)
@@ -297,6 +303,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   I.plan_only = c.plan_only;
   I.v32 = c.verify_fp32;
   I.split_fb = c.split_fb;
+  if (const char* e = std::getenv("PIPESIM_BIAS_STREAM")) I.bias_stream = std::atoi(e) != 0;
   if (const char* e = std::getenv("PIPESIM_SPLIT_FB")) I.split_fb = std::atoi(e) != 0;
   I.sc = c.verify_fp32 ? 2 : 1;
   I.W = c.W;
@@ -557,8 +564,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       if (prio_mode >= 1) ps = hi_prio;
       if (prio_mode >= 2) ps = std::max(hi_prio, lo_prio - 1 - s * (lo_prio - hi_prio) / W);
       PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].stream, cudaStreamNonBlocking, ps));
-      if (c.side_streams)
+      if (c.side_streams) {
         PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].side, cudaStreamNonBlocking, pside));
+        PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].biasstream, cudaStreamNonBlocking, pside));
+      }
       if (I.split_fb)
         PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].bstream, cudaStreamNonBlocking, ps));
     }
@@ -979,11 +988,17 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
       Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
       const int cur = (tk.k - 1) % 2, nxt = tk.k % 2;
-      // wgrad+SGD and bias of layer l run on the side stream as soon as dZ_l
-      // exists, overlapping the dgrad chain of the layers below (which only
-      // needs dZ); joined back before the task completes.
+      // wgrad+SGD of layer l runs on the side stream and its bias gradient +
+      // SGD on the bias stream as soon as dZ_l exists, overlapping the dgrad
+      // chain of the layers below (which only needs dZ) and each other;
+      // both are joined back before the task completes.
       const int side = c.side_streams ? Impl::kSideBase - s : s;
-      if (c.side_streams) wait_on(side, record_on(ns));
+      const int bstr = !c.side_streams ? s : (I.bias_stream ? Impl::kBiasBase - s : side);
+      if (c.side_streams) {
+        cudaEvent_t ev = record_on(ns);
+        wait_on(side, ev);
+        if (bstr != side) wait_on(bstr, ev);
+      }
       for (int l = st.L - 1; l >= 0; --l) {
         const auto& d = st.layers[l];
         __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
@@ -1036,7 +1051,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         // bias gradient + SGD; the last one stamps the commit
         {
           Impl::Op o{OK::bias};
-          o.stream = side;
+          o.stream = bstr;
           o.dz = dz;
           o.rows = c.B;
           o.cols = d.out;
@@ -1057,9 +1072,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         }
         // dZ_{l-1} (written by this iteration's dgrad on the main stream) is
         // what the side stream needs next
-        if (c.side_streams && l > 0) wait_on(side, record_on(ns));
+        if (c.side_streams && l > 0) {
+          cudaEvent_t ev = record_on(ns);
+          wait_on(side, ev);
+          if (bstr != side) wait_on(bstr, ev);
+        }
       }
-      if (c.side_streams) wait_on(ns, record_on(side));  // join
+      if (c.side_streams) {  // join
+        wait_on(ns, record_on(side));
+        if (bstr != side) wait_on(ns, record_on(bstr));
+      }
       if (c.snapshots && !c.plan_only) {
         for (int l = 0, po = 0; l < st.L; ++l) {
           const auto& d = st.layers[l];
@@ -1345,6 +1367,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       streams.push_back(I.stages[i].stream);
       if (I.stages[i].side) streams.push_back(I.stages[i].side);
       if (I.stages[i].bstream) streams.push_back(I.stages[i].bstream);
+      if (I.stages[i].biasstream) streams.push_back(I.stages[i].biasstream);
     }
   for (cudaStream_t c : I.comm)
     if (c) streams.push_back(c);
