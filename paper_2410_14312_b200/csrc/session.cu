@@ -562,14 +562,21 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     if (I.local(s)) {
       int ps = lo_prio, pside = lo_prio;
       if (prio_mode >= 1) ps = hi_prio;
-      if (prio_mode >= 2) ps = std::max(hi_prio, lo_prio - 1 - s * (lo_prio - hi_prio) / W);
+      if (prio_mode == 2) ps = std::max(hi_prio, lo_prio - 1 - s * (lo_prio - hi_prio) / W);
+      // PIPESIM_PRIO=3: backward (dgrad chain) streams above forwards above
+      // the wgrad / bias streams
+      int pb = ps;
+      if (prio_mode == 3) {
+        pb = hi_prio;
+        ps = std::min(lo_prio, hi_prio + 1);
+      }
       PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].stream, cudaStreamNonBlocking, ps));
       if (c.side_streams) {
         PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].side, cudaStreamNonBlocking, pside));
         PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].biasstream, cudaStreamNonBlocking, pside));
       }
       if (I.split_fb)
-        PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].bstream, cudaStreamNonBlocking, ps));
+        PB_CUDA(cudaStreamCreateWithPriority(&I.stages[s].bstream, cudaStreamNonBlocking, pb));
     }
   if (c.world > 1) {
     for (cudaStream_t& cs : I.comm) PB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
