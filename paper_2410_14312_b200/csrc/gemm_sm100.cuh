@@ -426,16 +426,21 @@ __device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const Ge
 
 // Vectorised transposed epilogue (the default): one warp's 32 rows x
 // n_cols accumulator, 32 columns per step.  tcgen05.ld hands thread i row i;
-// the 32 x 32 fp32 block is staged row-major in padded smem (row stride 36
-// floats: the float4 stores of 32 rows and the float4 reads of 4 rows x
-// 128 B are both at the 4-wavefront minimum), then lane l serves row
+// the 32 x 32 fp32 block is staged row-major in swizzled smem (below), then
+// lane l serves row
 // 4*rr + l/8, columns 4*(l%8)..+3 of the block for rr = 0..7.  Every global
 // access is a 16-byte (fp32) or 8-byte (bf16) vector and one warp
 // instruction covers 4 full row segments (4 x 128 B fp32 / 4 x 64 B bf16):
 // a quarter of the memory instructions of a lane-per-column layout.  The
 // global inputs of step c+1 (fp32 masters for SGD, stored activations for
 // the dgrad gate) are loaded while step c is processed.
-constexpr int kVecLd = 36;  // staging row stride (floats)
+// Staging block: 32 rows x 32 fp32 (4 KB per warp), 16-byte chunks XOR-
+// swizzled by row (chunk j of row r at slot j ^ (r & 7)): the row-wise float4
+// stores of 32 lanes and the 4-rows-per-instruction float4 reads are both at
+// the 4-wavefront minimum, and no padding is spent (the mainloop ring keeps
+// the shared memory: more bytes in flight per SM).
+constexpr int kVecLd = 32;  // staging row stride (floats)
+__device__ __forceinline__ int vec_slot(int row, int chunk) { return (chunk ^ (row & 7)) * 4; }
 
 template <int EPI, int ACT>
 __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const GemmShape& sh,
@@ -476,7 +481,7 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        *reinterpret_cast<float4*>(T + lane * kVecLd + 4 * j) =
+        *reinterpret_cast<float4*>(T + lane * kVecLd + vec_slot(lane, j)) =
             make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
     }
@@ -494,7 +499,7 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
     for (int rr = 0; rr < 8; ++rr) {
       const int rl = rr * 4 + sub_r;
       const int row = row_base + rl;
-      const float4 a = *reinterpret_cast<const float4*>(T + rl * kVecLd + c4);
+      const float4 a = *reinterpret_cast<const float4*>(T + rl * kVecLd + vec_slot(rl, c4 / 4));
       float v[4] = {a.x, a.y, a.z, a.w};
       if (row >= sh.M) continue;
       if (n + 3 < sh.N) {
@@ -901,14 +906,14 @@ struct Gemm2Cfg {
   static constexpr int kStageBytes = kAHalf + kBHalf;
   // wgrad tiles are short in K (one mini-batch): 4 stages leave room for the
   // TMA epilogue's double-buffered master tiles
-  static constexpr int kStages = EPI == kEpiWgradSgd ? 4 : (BN >= 256 ? 5 : 7);
+  static constexpr int kStages = EPI == kEpiWgradSgd ? 4 : (BN >= 256 ? 6 : 8);
   static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   // per epilogue warp: staging block (vector epilogue) or, for SGD, 2 x (fp32
   // 32x32 master tile 4 KB + bf16 32x32 tile 2 KB) for the TMA epilogue
   static constexpr int kSgdWarpBytes = 2 * (4096 + 2048);
   static constexpr int kEpiBytes = EPI == kEpiWgradSgd ? kEpiWarps * kSgdWarpBytes
-                                                       : kEpiWarps * 32 * 36 * 4;
+                                                       : kEpiWarps * 32 * kVecLd * 4;
   static constexpr int kBarOff = kStages * kStageBytes + kEpiBytes;
   static constexpr int kSmem = kBarOff + 512 + 1024;
   static constexpr uint32_t kTmemCols = 2 * BN;        // double-buffered accumulator
