@@ -372,6 +372,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": M * 4 * B + M * 8, "ms_per_step": e2e_step_ms},
         "gpu_launches": kernels_per_step,
+        "other_configs": other_configs(P) if world == 1 else None,
         "clocks": clocks.summary(),
         "wall_s": wall,
     }
@@ -382,6 +383,30 @@ def main():
 
 
 DOMINANT = "fwd"  # largest share of the step (ncu launch list, profiles/)
+
+
+def other_configs(P):
+    """BASELINE configs[0]/[1] on this GPU (784-512-256-10, N=4, B=256,
+    M=12): W=2 nF1B and W=1 sequential, device-timed epochs with resident
+    data.  Launch-bound (0.6 GFLOP per mini-batch); reported beside the
+    headline, not as it."""
+    out = {}
+    widths, acts = [784, 512, 256, 10], ["relu", "relu", "linear"]
+    net = P.NetworkSpec(widths, acts, "softmax_cross_entropy")
+    for key, W, mode in (("C1_mnist_mlp_W2_nf1b", 2, "timeprest"),
+                         ("C2_mnist_mlp_W1_sequential", 1, "sequential")):
+        B, M = 256, 12
+        s = P.Session(net, W, 4, B, M, CFG["lr"], mode)
+        s.load_params(P.init_network_params(net, CFG["seed"]))
+        x, lab = P.make_classification_task(M * B, 784, 10, seed=7, as_labels=True,
+                                            dtype=np.float32)
+        s.upload(x, lab, y_labels=True)
+        for _ in range(3):
+            s.run_epoch()
+        ms = float(np.median([s.run_epoch()["device_ms"] for _ in range(5)]))
+        s.close()
+        out[key] = {"samples_per_s": M * B / (ms / 1000.0), "us_per_mini_batch": 1000.0 * ms / M}
+    return out
 
 
 def in_step_others(P, net, W, Nm, B, M, device, main_sess):
