@@ -898,15 +898,24 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
 //
 // Warps: 0 TMA producer (both CTAs), 1 MMA issuer (leader) + TMEM owner,
 //        2..5 epilogue (TMEM lanes 32*(warp%4) .. +32).
+// BN = 512: two N=256 MMAs per k-block share the A operand (256 x 512 tile,
+// 48 B of operands per 2 x 4 MFLOP per CTA instead of 32 B per 4 MFLOP: the
+// mainloop's per-SM feed, which is latency-bound, covers the
+// MMA rate); the two accumulators fill TMEM, so tiles are not double-buffered.
 template <int BN, int EPI>
 struct Gemm2Cfg {
   static constexpr int kBK = 64;
+  static constexpr int kMmaN = BN > 256 ? 256 : BN;     // N of one tcgen05.mma
+  static constexpr int kSub = BN / kMmaN;               // MMAs per k-block
+  static constexpr int kAccBufs = BN > 256 ? 1 : 2;     // TMEM accumulator buffers
   static constexpr int kAHalf = 128 * kBK * 2;         // this CTA's A rows
-  static constexpr int kBHalf = (BN / 2) * kBK * 2;    // this CTA's B rows
+  static constexpr int kBSub = (kMmaN / 2) * kBK * 2;  // this CTA's B rows of one MMA
+  static constexpr int kBHalf = kSub * kBSub;          // this CTA's B rows
   static constexpr int kStageBytes = kAHalf + kBHalf;
   // wgrad tiles are short in K (one mini-batch): 4 stages leave room for the
   // TMA epilogue's double-buffered master tiles
-  static constexpr int kStages = EPI == kEpiWgradSgd ? 4 : (BN >= 256 ? 6 : 8);
+  static constexpr int kStages =
+      EPI == kEpiWgradSgd ? 4 : (BN > 256 ? 4 : (BN >= 256 ? 6 : 8));
   static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   // per epilogue warp: staging block (vector epilogue) or, for SGD, 2 x (fp32
@@ -916,7 +925,7 @@ struct Gemm2Cfg {
                                                        : kEpiWarps * 32 * kVecLd * 4;
   static constexpr int kBarOff = kStages * kStageBytes + kEpiBytes;
   static constexpr int kSmem = kBarOff + 512 + 1024;
-  static constexpr uint32_t kTmemCols = 2 * BN;        // double-buffered accumulator
+  static constexpr uint32_t kTmemCols = kAccBufs * BN;  // double-buffered if it fits
   static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
@@ -989,7 +998,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
         const int tile = u / S_k, split = u % S_k;
         const int tm = tile / tiles_n, tn = tile % tiles_n;
         const int m0 = tm * 256 + static_cast<int>(rank) * 128;
-        const int nb0 = tn * BN + static_cast<int>(rank) * (BN / 2);
         const int kb_lo = split * kbps, kb_hi = min(kb_all, kb_lo + kbps);
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
           const int s = it % S;
@@ -1007,13 +1015,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
               ptx::tma_load_2d_pair(a_dst + h * 8192, &tmap_a, fb, m0 + h * 64 + sh.a_mn_off,
                                     k0 + sh.a_k_off);
           }
-          if constexpr (!B_MN) {
-            ptx::tma_load_2d_pair(b_dst, &tmap_b, fb, k0 + sh.b_k_off, nb0 + sh.b_mn_off);
-          } else {
 #pragma unroll
-            for (int h = 0; h < BN / 128; ++h)
-              ptx::tma_load_2d_pair(b_dst + h * 8192, &tmap_b, fb, nb0 + h * 64 + sh.b_mn_off,
-                                    k0 + sh.b_k_off);
+          for (int j = 0; j < Cfg::kSub; ++j) {
+            // MMA j of the k-block: this CTA's B rows of N block j
+            const int nbj = tn * BN + j * Cfg::kMmaN + static_cast<int>(rank) * (Cfg::kMmaN / 2);
+            uint8_t* bj = b_dst + j * Cfg::kBSub;
+            if constexpr (!B_MN) {
+              ptx::tma_load_2d_pair(bj, &tmap_b, fb, k0 + sh.b_k_off, nbj + sh.b_mn_off);
+            } else {
+#pragma unroll
+              for (int h = 0; h < Cfg::kMmaN / 128; ++h)
+                ptx::tma_load_2d_pair(bj + h * 8192, &tmap_b, fb, nbj + h * 64 + sh.b_mn_off,
+                                      k0 + sh.b_k_off);
+            }
           }
         }
       }
@@ -1021,13 +1035,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       // ---------------- MMA issuer (leader only)
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, Cfg::kMmaN, A_MN, B_MN);
       int it = 0, local = 0;
       for (int u = pair; u < num_units; u += num_pairs, ++local) {
         const int split = u % S_k;
         const int num_kb = min(kb_all, (split + 1) * kbps) - split * kbps;
-        const int acc = local & 1;
-        const int use = local >> 1;
+        const int acc = local % Cfg::kAccBufs;
+        const int use = local / Cfg::kAccBufs;
         ptx::mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -1042,10 +1056,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             const uint64_t a_desc =
                 A_MN ? ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024)
                      : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
-            const uint64_t b_desc =
-                B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024)
-                     : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
-            ptx::mma_bf16_pair(d_tmem, a_desc, b_desc, idesc, (kb | kk) != 0);
+#pragma unroll
+            for (int j = 0; j < Cfg::kSub; ++j) {
+              const uint32_t bj = b_addr + j * Cfg::kBSub;
+              const uint64_t b_desc =
+                  B_MN ? ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024)
+                       : ptx::smem_desc_sw128(bj + kk * 32, 16, 1024);
+              ptx::mma_bf16_pair(d_tmem + j * Cfg::kMmaN, a_desc, b_desc, idesc,
+                                 (kb | kk) != 0);
+            }
           }
           ptx::mma_commit_pair(&empty_bar[s], 0x3);
         }
@@ -1090,8 +1109,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
     int local = 0;
     for (int u = pair; u < num_units; u += num_pairs, ++local) {
       const int tile = u / S_k, split = u % S_k;
-      const int acc = local & 1;
-      const int use = local >> 1;
+      const int acc = local % Cfg::kAccBufs;
+      const int use = local / Cfg::kAccBufs;
       const int tm = tile / tiles_n, tn = tile % tiles_n;
       prefetch_master(u + num_pairs);
       ptx::mbar_wait(&tfull_bar[acc], use & 1);

@@ -118,7 +118,7 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     const int pairs = std::min(tiles, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
-  } else {
+  } else if constexpr (BN <= 256) {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
     constexpr int smem = GemmCfg<BN>::kSmem;
     const int splits = std::max(1, g.sh.splits);
@@ -146,9 +146,10 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void set_attr() {
-  PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               GemmCfg<BN>::kSmem));
+  if constexpr (BN <= 256)
+    PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GemmCfg<BN>::kSmem));
   PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                Gemm2Cfg<BN, EPI>::kSmem));
@@ -156,6 +157,8 @@ void set_attr() {
 
 template <bool A_MN, bool B_MN, int EPI>
 void launch_bn(const GemmLaunch& g, cudaStream_t st) {
+  if constexpr (EPI != kEpiWgradSgd)
+    if (g.bn == 512) return launch_one<512, A_MN, B_MN, EPI>(g, st);
   if (g.bn == 256)
     launch_one<256, A_MN, B_MN, EPI>(g, st);
   else
@@ -169,6 +172,8 @@ void init_gemm_attributes() {
   std::call_once(once, [] {
     set_attr<128, false, false, kEpiFwd>();
     set_attr<256, false, false, kEpiFwd>();
+    set_attr<512, false, false, kEpiFwd>();
+    set_attr<512, false, true, kEpiDgrad>();
     set_attr<128, false, true, kEpiDgrad>();
     set_attr<256, false, true, kEpiDgrad>();
     set_attr<128, true, true, kEpiWgradSgd>();
@@ -230,7 +235,17 @@ void vec_or_fallback(EpiParams& e, int kind) {
 }
 
 // B-operand box rows for a K-major B: the pair kernel loads half a tile.
-int b_box(const GemmLaunch& g) { return g.pair ? g.bn / 2 : g.bn; }
+int b_box(const GemmLaunch& g) { return g.pair ? std::min(g.bn, 256) / 2 : g.bn; }
+
+// 256 x 512 pair tiles (two MMAs per k-block sharing A) for wide layers:
+// PIPESIM_BN512=0 turns them off (A/B runs).
+bool wide_tiles(int N) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_BN512");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && N >= 1024 && N % 512 == 0;
+}
 
 }  // namespace
 
@@ -288,6 +303,7 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
   } else {
     g.bn = pick_bn(rows, w.rows);
     g.pair = use_pair(rows);
+    if (g.pair && wide_tiles(w.rows)) g.bn = 512;
   }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
@@ -329,6 +345,7 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
   }
   g.bn = pick_bn(dz.rows, w.cols);
   g.pair = use_pair(dz.rows);
+  if (g.pair && wide_tiles(w.cols)) g.bn = 512;
   g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0};
