@@ -5,7 +5,11 @@
 // A session owns, for one network / train configuration, every device buffer
 // of every pipeline stage and a static program derived from the schedule
 // grid and version ledger (plan.cpp):
-//   * one CUDA stream per stage; a stage executes its grid row in slot order;
+//   * per stage a forward stream, a backward stream (dgrad chain, loss), a
+//     side stream (wgrad + SGD) and a bias stream; forwards and backwards each
+//     run in slot order, and the hazards a single slot-ordered stream would
+//     order (pinned version committed, activation slot free, pool colour
+//     free) are explicit events (session.cu);
 //   * cross-stage edges (activation s -> s+1, delta s+1 -> s) are CUDA events;
 //   * weight versions live in a per-stage bf16 pool sized by the retention
 //     timeline's peak (interval colouring), fp32 masters ping-pong by version
