@@ -144,9 +144,25 @@ def _ref_one_step(_=None):
     return ("port", time.perf_counter() - t)
 
 
+def ref_parallel_runs():
+    """How many single-threaded reference runs the host can hold at once:
+    every core, capped by memory (one run of the 16x4096 f64 network holds
+    ~15 GB max RSS: parameters, versions, gradients)."""
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+        mem = max(1, int(psutil.virtual_memory().available // (16 << 30)))
+    except Exception:  # noqa: BLE001
+        mem = 4
+    return max(1, min(cores, mem))
+
+
 def start_cpu_reference(runs):
-    """Starts `runs` independent reference steps, one per host core, in the
-    background (they overlap the GPU measurement).  Returns a finisher."""
+    """Starts `runs` independent single-threaded reference steps, one per host
+    core, in the background (they may overlap the GPU measurement).  The
+    finisher reports the aggregate samples/s of the concurrent runs (the
+    reference is single-threaded, so independent replicas are how it uses
+    several cores) and `cores` = runs."""
     import concurrent.futures as cf
     import multiprocessing as mp
     runs = max(1, min(runs, os.cpu_count() or 1))
@@ -160,30 +176,27 @@ def start_cpu_reference(runs):
         secs = statistics.median(r[1] for r in res)
         S = REF_SAMPLE
         samples = S["M"] * S["B"]
-        return dict(value=samples / secs, unit="samples/s", cores=1, kind=kind,
+        return dict(value=runs * samples / secs, unit="samples/s", cores=runs, kind=kind,
+                    sec_per_run=secs,
                     sample=(f"16x4096 MLP, W=8 nF1B, N={S['N']}, B={S['B']}, M={S['M']} "
-                            f"({samples} samples) per run; median of {runs} independent "
-                            f"single-threaded runs ({runs} host cores in parallel), "
-                            f"{secs:.1f} s each"))
+                            f"({samples} samples) per run; {runs} concurrent independent "
+                            f"single-threaded runs on {runs} host cores (median "
+                            f"{secs:.1f} s each), value = aggregate samples/s"))
     return finish
-
-
-def cpu_reference(steps, warmup):
-    return start_cpu_reference(steps)()
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cb = cpu_reference(args.steps, args.warmup)
-    secs = (REF_SAMPLE["M"] * REF_SAMPLE["B"]) / cb["value"]
+    runs = ref_parallel_runs()
+    cb = start_cpu_reference(runs)()
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "samples/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * secs, "higher_is_better": True,
+            "ms_per_step": 1000.0 * cb.pop("sec_per_run"), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "deep MLP 16x4096, W=8 nF1B (bounded CPU sample)",
-                       "model": "mlp-16x4096", "parallelism": "cpu-1thread"},
+                       "model": "mlp-16x4096", "parallelism": f"cpu-{runs}x1thread"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -255,10 +268,11 @@ def main():
         dist.all_gather_object(blobs, sess.ipc_export())
         sess.ipc_connect(blobs)
     else:
-        # the dominant GEMM kind is timed in place: CUDA events around each of
-        # its launches, recorded inside the graph on the launch stream
+        # uninstrumented: the per-launch kernel timing runs in separate
+        # sessions afterwards (in_step_kernels), so its event nodes do not
+        # perturb the timed step
         sess = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=local,
-                         use_graph=not args.no_graph, timed_kernel=DOMINANT)
+                         use_graph=not args.no_graph)
     p0 = P.init_network_params(net, CFG["seed"])
     sess.load_params(p0)
     kernels_per_step = sess.kernels_per_epoch
@@ -298,12 +312,9 @@ def main():
         barrier()
         t0 = time.perf_counter()
         dev_ms = []
-        kt_ms, kt_fl = [], []
         for _ in range(args.steps):
             resident_step()
             dev_ms.append(out.device_ms)
-            if not split:  # the last timed step's launches
-                kt_ms, kt_fl = sess.kernel_timeline()
         barrier()
         wall = time.perf_counter() - t0
         clocks.window = (t0, t0 + wall)
@@ -341,9 +352,8 @@ def main():
     fps = gemm_flops_per_sample(CFG["widths"])
     step_tflops = fps * rows / (ms_step / 1000.0) / 1e12
 
-    roof = kernel_roofline(peaks, kt_ms if len(kt_ms) else None,
-                           kt_fl if len(kt_fl) else None,
-                           in_step_others(P, net, W, Nm, B, M, local, sess) if not split else {})
+    roof = kernel_roofline(peaks, in_step_kernels(P, net, W, Nm, B, M, local, sess)
+                           if not split else {})
     roof["step_gemm_tflops"] = step_tflops
     roof["step_frac_of_sustained"] = step_tflops / peaks["bf16_sus"]
 
@@ -351,6 +361,7 @@ def main():
     if cpu_finish is not None:
         try:
             cb = cpu_finish()
+            cb.pop("sec_per_run", None)
         except Exception as e:  # noqa: BLE001
             cb = {"value": None, "error": str(e)}
 
@@ -409,13 +420,14 @@ def other_configs(P):
     return out
 
 
-def in_step_others(P, net, W, Nm, B, M, device, main_sess):
-    """In-step launch statistics of the other two GEMM kinds: one extra
-    session each, timed the same way (events around every launch inside the
-    graph), two epochs, the second kept."""
+def in_step_kernels(P, net, W, Nm, B, M, device, main_sess):
+    """In-step launch statistics of the three GEMM kinds: one instrumented
+    session each (CUDA events around every launch of that kind, recorded
+    inside the graph on the launch stream), same workload as the timed step,
+    two epochs, the second kept."""
     out = {}
     main_sess.close()  # free HBM for the instrumented sessions
-    for kind in ("dgrad", "wgrad"):
+    for kind in (DOMINANT, "dgrad", "wgrad"):
         s = P.Session(net, W, Nm, B, M, CFG["lr"], "timeprest", device=device,
                       timed_kernel=kind)
         s.load_params(P.init_network_params(net, CFG["seed"]))
@@ -438,7 +450,7 @@ def _stats(ms, fl, hbm_bytes=None):
     return d
 
 
-def kernel_roofline(peaks, fwd_ms, fwd_fl, others):
+def kernel_roofline(peaks, runs):
     """Roofline of the dominant kernel, the forward GEMM (bias+ReLU fused):
     algorithmic flops of every forward launch of the timed step (2*rows*N*K)
     / its device duration, from CUDA events around each launch inside the
@@ -480,9 +492,7 @@ def kernel_roofline(peaks, fwd_ms, fwd_fl, others):
     except Exception:
         pass
     in_step = {}
-    if fwd_ms is not None and len(fwd_ms):
-        in_step["fwd"] = _stats(fwd_ms, fwd_fl)
-    for kind, (ms, fl) in others.items():
+    for kind, (ms, fl) in runs.items():
         in_step[kind] = _stats(ms, fl, n * n * 10 + 2 * 1024 * n * 2 if kind == "wgrad" else None)
     achieved = in_step.get("fwd", {}).get("tflops")
     return {"bound": "tensor", "kernel": "forward GEMM gemm_bf16_tcgen05_pair/_tcgen05 "

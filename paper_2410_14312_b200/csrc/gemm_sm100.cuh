@@ -471,7 +471,16 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
       }
     }
   };
+  // fwd bias: this step's float4 and the next step's, loaded one step ahead
+  // like the other inputs (an L2 round trip per step otherwise)
+  auto load_bias = [&](int c) {
+    const int n = n_base + c + c4;
+    if constexpr (EPI == kEpiFwd)
+      if (ep.bias && n + 3 < sh.N) return __ldg(reinterpret_cast<const float4*>(ep.bias + n));
+    return make_float4(0.f, 0.f, 0.f, 0.f);
+  };
   load_inputs(0, win, xin);
+  float4 bias4 = load_bias(0);
 #pragma unroll 1
   for (int c = 0; c < n_cols; c += 32) {
     if (n_base + c >= sh.N) break;  // warp-uniform
@@ -488,15 +497,66 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
     // next step's inputs go in flight once the accumulator registers are free
     float4 wnx[8];
     uint2 xnx[8];
-    if (c + 32 < n_cols && n_base + c + 32 < sh.N) load_inputs(c + 32, wnx, xnx);
+    float4 bnx = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c + 32 < n_cols && n_base + c + 32 < sh.N) {
+      load_inputs(c + 32, wnx, xnx);
+      bnx = load_bias(c + 32);
+    }
     __syncwarp();
     const int n = n_base + c + c4;
-    float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // interior 32 x 32 block with a bf16 destination (the common case): one
+    // pointer, no per-row bounds or destination checks
+    const bool full = row_base + 32 <= sh.M && n_base + c + 32 <= sh.N;
+    bool done = false;
     if constexpr (EPI == kEpiFwd) {
-      if (ep.bias && n + 3 < sh.N) bias4 = __ldg(reinterpret_cast<const float4*>(ep.bias + n));
+      if (full && ep.y16 && !ep.y32) {
+        __nv_bfloat16* dst =
+            ep.y16 + static_cast<size_t>(row_base + ep.y_row_off + sub_r) * ep.ld_y16 + n;
+        const size_t step = static_cast<size_t>(4) * ep.ld_y16;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int rl = rr * 4 + sub_r;
+          const float4 a =
+              *reinterpret_cast<const float4*>(T + rl * kVecLd + vec_slot(rl, c4 / 4));
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(act_fwd_t<ACT>(a.x + bias4.x),
+                                                    act_fwd_t<ACT>(a.y + bias4.y));
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(act_fwd_t<ACT>(a.z + bias4.z),
+                                                    act_fwd_t<ACT>(a.w + bias4.w));
+          *reinterpret_cast<uint2*>(dst + rr * step) =
+              make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        }
+        done = true;
+      }
+    } else if constexpr (EPI == kEpiDgrad) {
+      if (full) {
+        __nv_bfloat16* dst = ep.d16 + static_cast<size_t>(row_base + sub_r) * ep.ld_d16 + n;
+        const size_t step = static_cast<size_t>(4) * ep.ld_d16;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int rl = rr * 4 + sub_r;
+          const float4 a =
+              *reinterpret_cast<const float4*>(T + rl * kVecLd + vec_slot(rl, c4 / 4));
+          float v[4] = {a.x, a.y, a.z, a.w};
+          if constexpr (kGate) {
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xin[rr]);
+            const float2 x01 = __bfloat1622float2(xh[0]);
+            const float2 x23 = __bfloat1622float2(xh[1]);
+            v[0] *= act_grad_t<ACT>(x01.x);
+            v[1] *= act_grad_t<ACT>(x01.y);
+            v[2] *= act_grad_t<ACT>(x23.x);
+            v[3] *= act_grad_t<ACT>(x23.y);
+          }
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+          *reinterpret_cast<uint2*>(dst + rr * step) =
+              make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        }
+        done = true;
+      }
     }
 #pragma unroll
     for (int rr = 0; rr < 8; ++rr) {
+      if (done) break;
       const int rl = rr * 4 + sub_r;
       const int row = row_base + rl;
       const float4 a = *reinterpret_cast<const float4*>(T + rl * kVecLd + vec_slot(rl, c4 / 4));
@@ -577,6 +637,7 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
       win[rr] = wnx[rr];
       xin[rr] = xnx[rr];
     }
+    bias4 = bnx;
   }
 }
 

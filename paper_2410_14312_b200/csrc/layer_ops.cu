@@ -115,6 +115,14 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
     int cap = sm_count() / 2;
     if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
+    // PIPESIM_TILES_PER_PAIR=t (fwd/dgrad): at least t tiles per CTA pair,
+    // so the double-buffered accumulator overlaps one tile's epilogue with
+    // the next one's mainloop (fewer SMs per launch, more launches side by side)
+    static const int tpp = [] {
+      const char* e = std::getenv("PIPESIM_TILES_PER_PAIR");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    if (EPI != kEpiWgradSgd && tpp > 1) cap = std::min(cap, (tiles + tpp - 1) / tpp);
     const int pairs = std::min(tiles, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
@@ -237,14 +245,20 @@ void vec_or_fallback(EpiParams& e, int kind) {
 // B-operand box rows for a K-major B: the pair kernel loads half a tile.
 int b_box(const GemmLaunch& g) { return g.pair ? std::min(g.bn, 256) / 2 : g.bn; }
 
-// 256 x 512 pair tiles (two MMAs per k-block sharing A) for wide layers:
-// PIPESIM_BN512=0 turns them off (A/B runs).
-bool wide_tiles(int N) {
+// 256 x 512 pair tiles (two MMAs per k-block sharing A) for wide layers
+// with at least PIPESIM_BN512_ROWS rows (default 512: below that the halved
+// CTA count costs more latency than the lower feed per flop saves; measured
+// 567k vs 561k samples/s with all rows); PIPESIM_BN512=0 turns them off.
+bool wide_tiles(int rows, int N) {
   static const bool on = [] {
     const char* e = std::getenv("PIPESIM_BN512");
     return !(e && std::string(e) == "0");
   }();
-  return on && N >= 1024 && N % 512 == 0;
+  static const int min_rows = [] {
+    const char* e = std::getenv("PIPESIM_BN512_ROWS");
+    return e ? std::atoi(e) : 512;
+  }();
+  return on && rows >= min_rows && N >= 1024 && N % 512 == 0;
 }
 
 }  // namespace
@@ -303,7 +317,7 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
   } else {
     g.bn = pick_bn(rows, w.rows);
     g.pair = use_pair(rows);
-    if (g.pair && wide_tiles(w.rows)) g.bn = 512;
+    if (g.pair && wide_tiles(rows, w.rows)) g.bn = 512;
   }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
@@ -345,7 +359,7 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
   }
   g.bn = pick_bn(dz.rows, w.cols);
   g.pair = use_pair(dz.rows);
-  if (g.pair && wide_tiles(w.cols)) g.bn = 512;
+  if (g.pair && wide_tiles(dz.rows, w.cols)) g.bn = 512;
   g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0};
@@ -428,34 +442,33 @@ void launch_wgrad(const GemmLaunch& g, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ bias + SGD
-// b_new = b_cur - lr * colsum(dz).  A block owns 32 output columns; 256
-// threads = 4 column groups (8 bf16 columns each, one 16-byte load) x 64 row
-// groups.  Row-group partials are combined in a fixed order in smem, so the
-// result is deterministic.  (trainer.cpp:250-252 and :484-488.)
-constexpr int kBiasCols = 32;
-constexpr int kBiasRowGroups = 64;
+// b_new = b_cur - lr * colsum(dz).  A block owns 8 output columns (one
+// 16-byte bf16 load per row); its 256 threads take rows t, t+256, ... with
+// four loads in flight each, so a 1024 x 4096 dZ is read by 512 blocks in a
+// single round trip (7.1 us cold in the ncu launch list, against 8.7 us for
+// 32-column blocks of 64 row groups and 8.5 us for 32-column blocks of 128).
+// The per-thread partials are combined by a fixed shuffle tree and then in
+// warp order: the result is deterministic.  (trainer.cpp:250-252, :484-488.)
+constexpr int kBiasCols = 8;
+constexpr int kBiasThreads = 256;
 
 template <typename TZ>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kBiasThreads)
     bias_sgd_kernel(const TZ* __restrict__ dz, int rows, int out, int ld_dz,
                     const float* b_cur, float* b_new, float* b_copy, float lr,
                     int* tag_slot, int* cur_version, int version, const int* trace_src,
                     int* trace_dst) {
-  __shared__ float part[kBiasRowGroups][kBiasCols + 1];
-  const int cx = threadIdx.x % 4;
-  const int ry = threadIdx.x / 4;
-  const int c0 = blockIdx.x * kBiasCols + cx * 8;
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const bool vec = sizeof(TZ) == 2 && (ld_dz % 8) == 0 && c0 + 8 <= out;
+  __shared__ float red[kBiasThreads / 32][kBiasCols];
+  const int c0 = blockIdx.x * kBiasCols;
+  float acc[kBiasCols] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool vec = sizeof(TZ) == 2 && (ld_dz % 8) == 0 && c0 + kBiasCols <= out;
   if constexpr (sizeof(TZ) == 2) if (vec) {
-    // 8 independent 16-byte row loads in flight per thread, then accumulate
-    // in row order (fixed order: deterministic).
-    constexpr int kU = 8;
-    for (int r0 = ry; r0 < rows; r0 += kU * kBiasRowGroups) {
+    constexpr int kU = 4;
+    for (int r0 = threadIdx.x; r0 < rows; r0 += kU * kBiasThreads) {
       uint4 q[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int r = r0 + u * kBiasRowGroups;
+        const int r = r0 + u * kBiasThreads;
         q[u] = r < rows ? *reinterpret_cast<const uint4*>(dz + static_cast<size_t>(r) * ld_dz + c0)
                         : make_uint4(0, 0, 0, 0);
       }
@@ -472,19 +485,26 @@ __global__ void __launch_bounds__(256)
     }
   }
   if (!vec) {
-    for (int r = ry; r < rows; r += kBiasRowGroups) {
+    for (int r = threadIdx.x; r < rows; r += kBiasThreads) {
       const TZ* p = dz + static_cast<size_t>(r) * ld_dz + c0;
-      for (int k = 0; k < 8 && c0 + k < out; ++k) acc[k] += static_cast<float>(p[k]);
+      for (int k = 0; k < kBiasCols && c0 + k < out; ++k) acc[k] += static_cast<float>(p[k]);
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) part[ry][cx * 8 + k] = acc[k];
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < kBiasCols; ++k) acc[k] += __shfl_xor_sync(~0u, acc[k], o);
+  const int w = threadIdx.x / 32;
+  if (threadIdx.x % 32 == 0)
+#pragma unroll
+    for (int k = 0; k < kBiasCols; ++k) red[w][k] = acc[k];
   __syncthreads();
   if (threadIdx.x < kBiasCols) {
-    const int col = blockIdx.x * kBiasCols + threadIdx.x;
+    const int col = c0 + threadIdx.x;
     if (col < out) {
       float g = 0.f;
-      for (int i = 0; i < kBiasRowGroups; ++i) g += part[i][threadIdx.x];
+#pragma unroll
+      for (int i = 0; i < kBiasThreads / 32; ++i) g += red[i][threadIdx.x];
       const float b = b_cur[col] - lr * g;
       b_new[col] = b;
       if (b_copy) b_copy[col] = b;
@@ -503,11 +523,11 @@ void launch_bias_sgd(cudaStream_t st, const __nv_bfloat16* dz, int rows,
                      int version, const int* trace_src, int* trace_dst, bool dz_f32) {
   const int grid = (out + kBiasCols - 1) / kBiasCols;
   if (dz_f32)
-    bias_sgd_kernel<float><<<grid, 256, 0, st>>>(
+    bias_sgd_kernel<float><<<grid, kBiasThreads, 0, st>>>(
         reinterpret_cast<const float*>(dz), rows, out, ld_dz, b_cur, b_new, b_copy, lr,
         tag_slot, cur_version, version, trace_src, trace_dst);
   else
-    bias_sgd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+    bias_sgd_kernel<__nv_bfloat16><<<grid, kBiasThreads, 0, st>>>(
         dz, rows, out, ld_dz, b_cur, b_new, b_copy, lr, tag_slot, cur_version, version,
         trace_src, trace_dst);
   PB_CUDA(cudaGetLastError());

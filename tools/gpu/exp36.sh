@@ -1,0 +1,11 @@
+# 3-buffer TMA SGD epilogue (vs PIPESIM_DBG_EPI=16 two-buffer) + bias kernel v3
+mkdir -p gpurun_out; o=gpurun_out/exp36.txt; : > $o
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2 >> $o
+for r in 1 2; do for v in 0 16; do
+  PIPESIM_DBG_EPI=$v PIPESIM_SPLITK=0 python tools/gemm_exp.py 2>&1 | sed "s/^/epi=$v /" >> $o
+  PIPESIM_DBG_EPI=$v timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline > gpurun_out/b36.json 2>/dev/null
+  python -c "import json;d=json.load(open('gpurun_out/b36.json'));print('epi=$v bench', round(d['value']), round(d['ms_per_step'],2), 'e2e', round(d['e2e']['value']), d['clocks']['sm_mhz'])" >> $o
+done; done
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_36.csv python tools/prof_step.py 4 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/launches_36.csv >> $o
+cat $o
