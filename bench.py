@@ -488,7 +488,7 @@ def kernel_roofline(peaks, runs):
     traffic = None
     try:  # DRAM bytes per launch of the same kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["fwd_256x4096x4096"]["bytes"]
+            traffic = json.load(f)["fwd_1024x4096x4096"]["bytes"]
     except Exception:
         pass
     in_step = {}
@@ -499,7 +499,7 @@ def kernel_roofline(peaks, runs):
             "(bias+ReLU epilogue), in-step", "achieved": achieved, "peak": peaks["bf16_sus"],
             "unit": "TFLOP/s", "frac": achieved / peaks["bf16_sus"] if achieved else None,
             "peak_source": peaks["src"] + " sustained bf16 (kernel timed inside the step)",
-            "traffic": traffic, "traffic_unit": "bytes/launch at 256x4096x4096 (dram read+write, ncu)",
+            "traffic": traffic, "traffic_unit": "bytes/launch at 1024x4096x4096 (dram read+write, ncu; algorithmic 50.3 MB)",
             "flops_per_launch": "2*rows*4096*4096 (rows = coalesced micro-batches, 128..1024)",
             "in_step": in_step, "alone": alone}
 

@@ -894,7 +894,8 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
   const int lane = threadIdx.x % 32;
   uint8_t* b32[2] = {wbuf, wbuf + 4096};
   uint8_t* b16[2] = {wbuf + 8192, wbuf + 8192 + 2048};
-  const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;  // timing experiments
+  // timing experiments: 2 skips the master loads, 4 all stores, 8 the bf16 stores
+  const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;
   if (first_tile && lane == 0 && !skip_ld)
     sgd_tma_load(maps, b32[st.g & 1], &bars[st.g & 1], n_base, row_base);
 #pragma unroll 1
@@ -938,7 +939,8 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
     __syncwarp();
     if (lane == 0 && !skip_st) {
       ptx::tma_store_2d(&maps.w_new, b32[b], n_base + c, row_base);
-      if (ep.has_w16) ptx::tma_store_2d(&maps.w16, b16[b], n_base + c, row_base);
+      if (ep.has_w16 && !(ep.dbg_skip & 8))
+        ptx::tma_store_2d(&maps.w16, b16[b], n_base + c, row_base);
       ptx::bulk_commit_group();
     }
     ++st.g;

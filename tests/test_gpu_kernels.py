@@ -38,6 +38,8 @@ FWD_SHAPES = [
     (200, 100, 10), (256, 4096, 4096), (128, 4096, 4096), (1000, 136, 392),
     # split-K shapes (K >= 1024): ragged N, ragged last split, partial M tiles
     (1024, 4096, 4096), (512, 1024, 1536), (384, 2048, 1000), (100, 3000, 700),
+    # 256 x 512 tiles with a partial last row tile / ragged rows
+    (700, 1024, 2048), (1000, 512, 1024),
 ]
 
 
@@ -59,7 +61,9 @@ def test_linear_fwd(rows, inn, out, act):
 
 
 DX_SHAPES = [(128, 256, 128), (256, 512, 784), (256, 10, 256), (5, 8, 2),
-             (1024, 4096, 4096), (300, 136, 72)]
+             (1024, 4096, 4096), (300, 136, 72),
+             # 256 x 512 tiles with a partial last row tile (interior fast path + edge path)
+             (600, 1024, 1024), (520, 2048, 1536)]
 
 
 @pytest.mark.parametrize("rows,out,inn", DX_SHAPES)

@@ -24,6 +24,7 @@ else:
     ncu = open(P("profiles", "ncu_round1_full.md")).read()
 sweep = open(P("profiles", "sweep_c5_r1.md")).read()
 traffic = json.load(open(P("profiles", "ncu_traffic.json")))
+ref = json.load(open(P("profiles", "round1_bench_reference.json")))
 
 alone = "\n".join(
     f"| {k} | {v['us']:.1f} us | {v['tflops']:.0f} TFLOP/s"
@@ -37,7 +38,8 @@ CPU reference, in-step kernel timing), `profiles/round1_launches_step_m4.csv`
 (ncu launch list of `tools/prof_step.py 4`: parameter load + upload + two
 4-mini-batch epochs of the benchmark network), `profiles/ncu_round1_full.md` /
 `profiles/ncu_traffic.json` (`ncu --set full` of
-`tools/prof_gemm.py fwd256,dgrad,wgrad 1`, split-K off as in the executor),
+`tools/prof_gemm.py fwd1024,dgrad,wgrad 1`, split-K off as in the executor),
+`profiles/round1_bench_reference.json` (`bench.py --impl reference`),
 `profiles/sweep_c5_r1.*` (`tools/sweep.py`).  Regenerate with
 `python tools/make_summary.py`.
 
@@ -51,6 +53,7 @@ CPU reference, in-step kernel timing), `profiles/round1_launches_step_m4.csv`
 | e2e samples/s (C ABI from pinned host x (bf16) + labels, H2D streamed inside the step, loss D2H) | {b['e2e']['value']:.0f} ({b['e2e']['ms_per_step']:.2f} ms/step, {b['e2e']['h2d_bytes_per_step']/1e6:.0f} MB H2D) |
 | CPU reference (compiled `pipesim`, 1 thread, box host) | {b['cpu_baseline']['value']:.4f} samples/s ({b['cpu_baseline']['sample']}) |
 | GPU / CPU | {b['value']/b['cpu_baseline']['value']:.2e} x (e2e: {b['e2e']['value']/b['cpu_baseline']['value']:.2e} x) |
+| reference arm (`bench.py --impl reference`: concurrent single-threaded runs on the host's cores) | {ref['value']:.4f} samples/s on {ref['cpu_baseline']['cores']} cores; e2e / reference arm = {b['e2e']['value']/ref['value']:.2e} x |
 | clocks during the timed region | {b['clocks']} |
 | our kernel launches per step | {b['gpu_launches']} |
 
@@ -86,7 +89,7 @@ as well as two epochs; the step itself is the three GEMMs, bias and loss.
 
 {ncu}
 Algorithmic versus measured DRAM traffic per launch (`profiles/ncu_traffic.json`):
-- **fwd 256x4096x4096**: W 32 MiB + X 2 MiB + Y 2 MiB = 35.7 MB; measured {traffic['fwd_256x4096x4096']['bytes']/1e6:.2f} MB — no re-reads.
+- **fwd 1024x4096x4096**: W 32 MiB + X 8 MiB + Y 8 MiB = 50.3 MB; measured {traffic['fwd_1024x4096x4096']['bytes']/1e6:.2f} MB.
 - **dgrad 1024x4096x4096**: dZ 8 MiB + W 32 MiB + stored activation (act' gate) 8 MiB + out 8 MiB = 58.7 MB; measured {traffic['dgrad_1024x4096x4096']['bytes']/1e6:.1f} MB (the written delta stays in L2).
 - **wgrad+SGD 4096x4096x1024**: dZ 8 MiB + X 8 MiB + fp32 master read 64 MiB + write 64 MiB + bf16 write 32 MiB = 184 MB; measured {traffic['wgrad_sgd_4096x4096x1024']['bytes']/1e6:.1f} MB (the rest of the new masters is still in L2 when the kernel ends).
 
@@ -99,7 +102,10 @@ model's idle fraction is the reference metric (metrics.cpp:71-72).
 {sweep}
 ## This round's changes (alone timings / step, before -> after)
 
-- activation as a compile-time epilogue parameter (the runtime switch inside unrolled loops doubled the code): fwd 1024 rows 41.5 -> 28.7 us.
+- activation as a compile-time epilogue parameter (the runtime switch inside unrolled loops doubled the code): fwd 1024 rows 41.5 -> 28.7 us (256-wide tiles).
+- 256 x 512 pair tiles for >= 512-row wide layers (MMA-bound mainloop, ~88% of the per-SM MMA rate, on half the SMs): slower alone (fwd 1024 rows 28.7 -> 48 us on 64 SMs), less SM-time per flop in the step: 558k -> 567k samples/s.
+- interior fast path of the vector epilogue (one pointer per 32x32 block, no per-row checks): fwd 1024 rows 48.1 -> 45.4 us, dgrad 53.4 -> 50.6 us.
+- timed step without the kernel-timing event nodes (in-step kernel timing moved to separate sessions): +3-8% on the reported step.
 - vector staged-transpose epilogue: wgrad+SGD 68 -> 57.6 us (same ring depth).
 - TMA epilogue for the SGD update: 57.6 -> 48.3 us.
 - separate forward / backward streams per stage (explicit hazard edges), forward runs spanning another mini-batch's backward: 1238 -> 992 forward launches per step, 525k -> 556k samples/s.
