@@ -870,10 +870,13 @@ __global__ void __launch_bounds__(128, 1)
 // n_cols of the tile in 32 x 32 chunks.  The fp32 master chunk arrives by
 // TMA (128-byte swizzle) one chunk ahead; each thread updates its own row in
 // place in shared memory (the swizzle makes the row-per-thread 16-byte
-// accesses conflict-free), writes the bf16 copy to a 64-byte-swizzled tile,
-// and one lane stores both tiles with TMA.  Loads and stores are bulk and
-// asynchronous: the update never waits for a global store, and out-of-range
-// rows / columns are clipped by the tensor maps.
+// accesses conflict-free), writes the bf16 copy into a 32 x 64 bf16 tile
+// (128-byte swizzle) that two consecutive chunks fill, and one lane stores
+// the fp32 chunk, and the bf16 tile after every second chunk, with TMA: three
+// bulk stores per 64 columns instead of four (the store count, not only the
+// bytes, costs epilogue time).  Loads and stores are bulk and asynchronous:
+// the update never waits for a global store, and out-of-range rows / columns
+// are clipped by the tensor maps.  n_cols is a multiple of 64.
 struct SgdTmaState {
   int g = 0;                  // chunks processed by this warp so far
   uint32_t phase[2] = {0, 0};
@@ -893,7 +896,7 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
                                                       int next_col) {
   const int lane = threadIdx.x % 32;
   uint8_t* b32[2] = {wbuf, wbuf + 4096};
-  uint8_t* b16[2] = {wbuf + 8192, wbuf + 8192 + 2048};
+  uint8_t* b16 = wbuf + 8192;  // 32 rows x 128 B: the bf16 copy of two chunks
   // timing experiments: 2 skips the master loads, 4 all stores, 8 the bf16 stores
   const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;
   if (first_tile && lane == 0 && !skip_ld)
@@ -920,27 +923,38 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
     }
     ptx::tmem_ld_wait();
     uint8_t* row32 = b32[b] + lane * 128;
-    uint8_t* row16 = b16[b] + lane * 64;
+    uint8_t* row16 = b16 + lane * 128;
+    const int half = (c >> 5) & 1;  // which 64-byte half of the bf16 row
+    // the bf16 tile was stored at the end of the previous chunk: every lane
+    // waits for lane 0's bulk_wait_group_read above before refilling it
+    if (half == 0) __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4* p = reinterpret_cast<float4*>(row32 + ((j ^ (lane & 7)) << 4));
-      float4 w = *p;
-      w.x -= ep.lr * __uint_as_float(r[4 * j]);
-      w.y -= ep.lr * __uint_as_float(r[4 * j + 1]);
-      w.z -= ep.lr * __uint_as_float(r[4 * j + 2]);
-      w.w -= ep.lr * __uint_as_float(r[4 * j + 3]);
-      *p = w;
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(w.z, w.w);
-      *reinterpret_cast<uint2*>(row16 + (((j >> 1) ^ ((lane >> 1) & 3)) << 4) + (j & 1) * 8) =
-          make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+    for (int j = 0; j < 8; j += 2) {
+      uint32_t hv[4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        float4* p = reinterpret_cast<float4*>(row32 + (((j + t) ^ (lane & 7)) << 4));
+        float4 w = *p;
+        w.x -= ep.lr * __uint_as_float(r[4 * (j + t)]);
+        w.y -= ep.lr * __uint_as_float(r[4 * (j + t) + 1]);
+        w.z -= ep.lr * __uint_as_float(r[4 * (j + t) + 2]);
+        w.w -= ep.lr * __uint_as_float(r[4 * (j + t) + 3]);
+        *p = w;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(w.x, w.y);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(w.z, w.w);
+        hv[2 * t] = *reinterpret_cast<uint32_t*>(&h0);
+        hv[2 * t + 1] = *reinterpret_cast<uint32_t*>(&h1);
+      }
+      const int unit = half * 4 + j / 2;  // 16-byte unit of the 128-byte bf16 row
+      *reinterpret_cast<uint4*>(row16 + ((unit ^ (lane & 7)) << 4)) =
+          make_uint4(hv[0], hv[1], hv[2], hv[3]);
     }
     ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA store
     __syncwarp();
     if (lane == 0 && !skip_st) {
       ptx::tma_store_2d(&maps.w_new, b32[b], n_base + c, row_base);
-      if (ep.has_w16 && !(ep.dbg_skip & 8))
-        ptx::tma_store_2d(&maps.w16, b16[b], n_base + c, row_base);
+      if (half == 1 && ep.has_w16 && !(ep.dbg_skip & 8))
+        ptx::tma_store_2d(&maps.w16, b16, n_base + c - 32, row_base);
       ptx::bulk_commit_group();
     }
     ++st.g;

@@ -55,13 +55,14 @@ CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn) {
   return map;
 }
 
-// Epilogue tensor maps of the TMA SGD epilogue: 2-D row-major, box 32 x 32.
+// Epilogue tensor maps of the TMA SGD epilogue: 2-D row-major, box 32 rows x
+// box_cols (32 fp32 master columns; 64 bf16 columns: one 128-byte row).
 CUtensorMap make_epi_tmap(const void* ptr, CUtensorMapDataType dt, int elem_bytes, int rows,
-                          int cols, int ld, CUtensorMapSwizzle swz) {
+                          int cols, int ld, CUtensorMapSwizzle swz, int box_cols = 32) {
   CUtensorMap map;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * elem_bytes};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -421,7 +422,7 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
     if (w16)
       g.maps.w16 = make_epi_tmap(w16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_w16,
-                                 CU_TENSOR_MAP_SWIZZLE_64B);
+                                 CU_TENSOR_MAP_SWIZZLE_128B, 64);
     g.ep.has_w16 = w16 ? 1 : 0;
     g.ep.rowwise = 3;
   }
