@@ -88,6 +88,13 @@ as well as two epochs; the step itself is the three GEMMs, bias and loss.
 ## Dominant kernels, `ncu --set full`
 
 {ncu}
+MMA busy = active cycles of the SM's four tensor sub-units / (4 x elapsed
+cycles) (the bf16 ops-path counters do not count tcgen05).  Under ncu
+(serialised, cold L2, clocks not locked) the 512-wide forward keeps the
+tensor cores of its 64 SMs ~70% busy and dgrad ~63%; wgrad+SGD reaches ~34%
+of all 148 SMs: its SGD epilogue (fp32 master in, fp32 + bf16 out through
+TMA) outlasts the mainloop (DESIGN.md §9).
+
 Algorithmic versus measured DRAM traffic per launch (`profiles/ncu_traffic.json`):
 - **fwd 1024x4096x4096**: W 32 MiB + X 8 MiB + Y 8 MiB = 50.3 MB; measured {traffic['fwd_1024x4096x4096']['bytes']/1e6:.2f} MB.
 - **dgrad 1024x4096x4096**: dZ 8 MiB + W 32 MiB + stored activation (act' gate) 8 MiB + out 8 MiB = 58.7 MB; measured {traffic['dgrad_1024x4096x4096']['bytes']/1e6:.1f} MB (the written delta stays in L2).
