@@ -60,22 +60,23 @@ def test_verify_is_tighter_than_bf16():
     assert errs["fp32"] < errs["bf16"] / 100, errs
 
 
-def test_full_width_bf16_against_fp32_verify():
+@pytest.mark.parametrize("mode,W", [("timeprest", 2), ("pipedream", 2), ("sequential", 1)])
+def test_full_width_bf16_against_fp32_verify(mode, W):
     """The benchmark's layer width and mini-batch (4096-wide layers, B=1024,
     N=8), where the fp64 oracle cannot run in test time: the bf16
     tensor-core path (256 x 512 tiles, TMA SGD epilogue, coalesced forwards)
     against the fp32 FFMA verify path from the same parameters and data.
-    4 layers on 2 stages, M=3.  The bf16 path must stay within the tolerances
+    4 layers on 2 stages (1 for sequential), M=3.  The bf16 path must stay within the tolerances
     it meets against the oracle on the smaller networks; version traces are
     identical."""
     net = P.NetworkSpec([4096] * 5, ["relu"] * 3 + ["linear"], "softmax_cross_entropy")
-    W, N, B, M = 2, 8, 1024, 3
+    N, B, M = 8, 1024, 3
     p0 = P.init_network_params(net, 1)
     x, lab = P.make_classification_task(M * B, 4096, 4096, seed=7, as_labels=True,
                                         dtype=np.float32)
     res = {}
     for prec in ("bf16", "fp32"):
-        s = P.Session(net, W, N, B, M, 0.05, "timeprest", precision=prec)
+        s = P.Session(net, W, N, B, M, 0.05, mode, precision=prec)
         s.load_params(p0)
         s.upload(x, lab, y_labels=True)
         r = s.run_epoch()
