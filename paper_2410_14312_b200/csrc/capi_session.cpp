@@ -307,7 +307,7 @@ int pb_session_read_version(pb_session* s, int stage, int version, double* out,
     const float* p = x.snapshot(stage, version);
     for (int64_t i = 0; i < n; ++i) out[i] = p[i];
   } else if (version == M || version == M - 1) {
-    x.read_stage_master(stage, version & 1, out);
+    x.read_stage_master(stage, version, out);
   } else {
     throw pipesim::structural_error("stage " + std::to_string(stage) + " does not hold version " +
                                     std::to_string(version) + " (no snapshots)");

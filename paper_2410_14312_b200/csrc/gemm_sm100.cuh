@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(128, 1)
 // are clipped by the tensor maps.  n_cols is a multiple of 64.
 struct SgdTmaState {
   int g = 0;                  // chunks processed by this warp so far
-  uint32_t phase[2] = {0, 0};
+  uint32_t phase[3] = {0, 0, 0};
 };
 
 __device__ __forceinline__ void sgd_tma_load(const EpiMaps& maps, uint8_t* buf32, uint64_t* bar,
@@ -961,6 +961,99 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd(const EpiParams& ep, const
   }
 }
 
+// Split fp32 masters.  A version's fp32 master is stored as its bf16 GEMM
+// operand hi (already needed by the forwards and dgrads that read the
+// version) plus a signed 16-bit residual lo: bits(master) = bits(hi) << 16 +
+// lo, exact.  hi is the master rounded to nearest in the bit pattern with
+// ties away from zero ((bits + 0x8000) >> 16; differs from RN-even only on
+// exact ties), so the residual always fits in 16 bits.  Per parameter the
+// update reads 4 bytes (hi, lo of the current version) and writes 4 (hi, lo
+// of the new one) instead of 4 + 6 with an fp32 master and a bf16 copy: a
+// third fewer bytes stored, which the step is sensitive to.
+__device__ __forceinline__ float join_master(uint32_t hi16, uint32_t lo16) {
+  return __int_as_float(static_cast<int>(hi16 << 16) + static_cast<int>(static_cast<int16_t>(lo16)));
+}
+__device__ __forceinline__ void split_master(float w, uint32_t& hi16, uint32_t& lo16) {
+  const uint32_t b = __float_as_uint(w);
+  hi16 = (b + 0x8000u) >> 16;
+  lo16 = (b - (hi16 << 16)) & 0xFFFFu;
+}
+
+// TMA epilogue of wgrad + SGD with split masters: one warp, 32 rows x n_cols,
+// 32 x 32 chunks.  hi and lo of the current version arrive by TMA (64-byte
+// swizzle, 2 KB each) one chunk ahead into one of three 4 KB buffers; each
+// thread rebuilds its row's fp32 masters, applies the update and writes the
+// new hi / lo back in place; one lane stores both with TMA.  Three buffers:
+// the load of chunk c+1 waits only for the store of chunk c-2 to have read
+// its buffer, not for the store just issued.
+__device__ __forceinline__ void epilogue_warp_tma_sgd_split(
+    const EpiParams& ep, const EpiMaps& maps, int row_base, int n_base, int n_cols,
+    uint32_t t_row, uint8_t* wbuf, uint64_t* bars, SgdTmaState& st, bool first_tile,
+    int next_row, int next_col) {
+  constexpr int kBufs = 3;
+  const int lane = threadIdx.x % 32;
+  const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;  // timing experiments
+  auto buf = [&](int g) { return wbuf + (g % kBufs) * 4096; };
+  auto load = [&](int g, int col, int row) {
+    uint64_t* bar = &bars[g % kBufs];
+    ptx::mbar_arrive_expect_tx(bar, 4096);
+    ptx::tma_load_2d(buf(g), &maps.w_cur, bar, col, row);
+    ptx::tma_load_2d(buf(g) + 2048, &maps.w_new, bar, col, row);
+  };
+  if (first_tile && lane == 0 && !skip_ld) load(st.g, n_base, row_base);
+#pragma unroll 1
+  for (int c = 0; c < n_cols; c += 32) {
+    const int g = st.g;
+    const int b = g % kBufs;
+    if (lane == 0) {
+      ptx::bulk_wait_group_read<1>();  // chunk g-2's store has read buffer (g+1) % 3
+      if (skip_ld) {
+      } else if (c + 32 < n_cols)
+        load(g + 1, n_base + c + 32, row_base);
+      else if (next_row >= 0)
+        load(g + 1, next_col, next_row);
+    }
+    uint32_t r[32];
+    ptx::tmem_ld32(t_row + c, r);
+    if (!skip_ld) {
+      ptx::mbar_wait(&bars[b], st.phase[b]);
+      st.phase[b] ^= 1;
+    }
+    ptx::tmem_ld_wait();
+    uint8_t* hrow = buf(g) + lane * 64;
+    uint8_t* lrow = hrow + 2048;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 16-byte units: 8 columns each
+      const int off = (u ^ ((lane >> 1) & 3)) << 4;
+      uint4 h = *reinterpret_cast<const uint4*>(hrow + off);
+      uint4 l = *reinterpret_cast<const uint4*>(lrow + off);
+      uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t h0, l0, h1, l1;
+        const float w0 = join_master(hw[q] & 0xFFFFu, lw[q] & 0xFFFFu) -
+                         ep.lr * __uint_as_float(r[8 * u + 2 * q]);
+        const float w1 = join_master(hw[q] >> 16, lw[q] >> 16) -
+                         ep.lr * __uint_as_float(r[8 * u + 2 * q + 1]);
+        split_master(w0, h0, l0);
+        split_master(w1, h1, l1);
+        hw[q] = h0 | (h1 << 16);
+        lw[q] = l0 | (l1 << 16);
+      }
+      *reinterpret_cast<uint4*>(hrow + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(lrow + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA store
+    __syncwarp();
+    if (lane == 0 && !skip_st) {
+      ptx::tma_store_2d(&maps.w16, buf(g), n_base + c, row_base);
+      ptx::tma_store_2d(&maps.lo_new, buf(g) + 2048, n_base + c, row_base);
+      ptx::bulk_commit_group();
+    }
+    ++st.g;
+  }
+}
+
 // ===========================================================================
 // Persistent CTA-pair kernel (cta_group::2).
 //
@@ -1025,8 +1118,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's are used)
-  uint64_t* sgd_bar = tempty_bar + 2;    // [2 per epilogue warp] (TMA SGD epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 2 * Cfg::kEpiWarps);
+  uint64_t* sgd_bar = tempty_bar + 2;    // [3 per epilogue warp] (TMA SGD epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 3 * Cfg::kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -1054,10 +1147,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
     }
     if constexpr (EPI == kEpiWgradSgd)
       if (ep.rowwise == 3) {
-        for (int i = 0; i < 2 * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
+        for (int i = 0; i < 3 * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
         ptx::tma_prefetch_desc(&maps.w_cur);
         ptx::tma_prefetch_desc(&maps.w_new);
         if (ep.has_w16) ptx::tma_prefetch_desc(&maps.w16);
+        if (ep.split_master) ptx::tma_prefetch_desc(&maps.lo_new);
       }
     ptx::fence_mbar_init();
   }
@@ -1207,9 +1301,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             next_row = (nt / tiles_n) * 256 + static_cast<int>(rank) * 128 + q * 32;
             next_col = (nt % tiles_n) * BN + c_off;
           }
-          epilogue_warp_tma_sgd(ep, maps, row_base, tn * BN + c_off, kColsPerWarp, t_row,
-                                sgd_buf, sgd_bar + 2 * e, sgd_st, local == 0, next_row,
-                                next_col);
+          if (ep.split_master)
+            epilogue_warp_tma_sgd_split(ep, maps, row_base, tn * BN + c_off, kColsPerWarp,
+                                        t_row, sgd_buf, sgd_bar + 3 * e, sgd_st, local == 0,
+                                        next_row, next_col);
+          else
+            epilogue_warp_tma_sgd(ep, maps, row_base, tn * BN + c_off, kColsPerWarp, t_row,
+                                  sgd_buf, sgd_bar + 3 * e, sgd_st, local == 0, next_row,
+                                  next_col);
         }
       } else if (ep.rowwise == 2) {
         with_act<EPI>(ep, [&](auto A) {

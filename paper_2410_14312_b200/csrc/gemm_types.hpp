@@ -21,11 +21,15 @@ struct GemmShape {
   int splits, kb_per_split;
 };
 
-// Tensor maps of the TMA epilogue of wgrad+SGD (EpiParams::rowwise == 3):
-// fp32 masters (current / new; box 32 x 32, 128-byte swizzle) and the bf16
-// weights of the new version (box 32 x 32, 64-byte swizzle).
+// Tensor maps of the TMA epilogue of wgrad+SGD (EpiParams::rowwise == 3).
+// fp32 masters: w_cur / w_new = current / new fp32 master (box 32 x 32,
+// 128-byte swizzle), w16 = bf16 weights of the new version (box 32 x 64).
+// Split masters (EpiParams::split_master): w_cur = hi of the current version
+// (its bf16 weights), w_new = lo residual of the current version, w16 = hi of
+// the new version, lo_new = its lo residual (all 16-bit, box 32 x 32, 64-byte
+// swizzle).
 struct alignas(64) EpiMaps {
-  CUtensorMap w_cur, w_new, w16;
+  CUtensorMap w_cur, w_new, w16, lo_new;
 };
 
 struct EpiParams {
@@ -61,6 +65,10 @@ struct EpiParams {
   // 3 = (SGD, pair kernel) TMA loads/stores through swizzled smem
   int rowwise;
   int has_w16;  // TMA SGD epilogue: EpiMaps::w16 is valid
+  // split fp32 masters: master(v) = bits(hi(v)) << 16 + lo(v), hi(v) the
+  // version's bf16 GEMM operand, lo(v) a signed 16-bit residual (exact fp32;
+  // 4 bytes per parameter in place of fp32 master + bf16 copy)
+  int split_master;
   // timing experiments: nonzero skips the epilogue's global traffic
   int dbg_skip;
 };

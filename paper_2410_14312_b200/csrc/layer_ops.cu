@@ -429,6 +429,99 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
   return g;
 }
 
+namespace {
+bool tma_epilogue_on() {
+  static const bool ok = [] {
+    const char* e = std::getenv("PIPESIM_EPI");
+    return !(e && (std::string(e) == "vec" || std::string(e) == "rows" ||
+                   std::string(e) == "tile"));
+  }();
+  return ok;
+}
+}  // namespace
+
+bool split_master_eligible(int out, int in, int ld) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_SPLIT_MASTER");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && tma_epilogue_on() && use_pair(out) && ld % 8 == 0 && in > 0;
+}
+
+GemmLaunch plan_wgrad_sgd_split(const Mat16& dz, const Mat16& x, int x_row_off,
+                                const __nv_bfloat16* hi_cur, const uint16_t* lo_cur,
+                                __nv_bfloat16* hi_new, uint16_t* lo_new, int ld, float lr) {
+  const int M = dz.cols, N = x.cols;
+  if (!split_master_eligible(M, N, ld) || !al(hi_cur, 16) || !al(lo_cur, 16) ||
+      !al(hi_new, 16) || !al(lo_new, 16))
+    throw std::invalid_argument("plan_wgrad_sgd_split: layer not eligible for split masters");
+  GemmLaunch g;
+  g.bn = pick_bn(M, N);
+  g.pair = true;
+  g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
+  g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
+  g.sh = GemmShape{M, N, dz.rows, 0, 0, 0, x_row_off};
+  g.ep = empty_epi(kEpiWgradSgd);
+  g.ep.w16 = hi_new;
+  g.ep.ld_w16 = ld;
+  g.ep.lr = lr;
+  g.ep.has_w16 = 1;
+  g.ep.split_master = 1;
+  g.ep.rowwise = 3;
+  g.maps.w_cur = make_epi_tmap(hi_cur, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld,
+                               CU_TENSOR_MAP_SWIZZLE_64B);
+  g.maps.w_new = make_epi_tmap(lo_cur, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, M, N, ld,
+                               CU_TENSOR_MAP_SWIZZLE_64B);
+  g.maps.w16 = make_epi_tmap(hi_new, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld,
+                             CU_TENSOR_MAP_SWIZZLE_64B);
+  g.maps.lo_new = make_epi_tmap(lo_new, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, M, N, ld,
+                                CU_TENSOR_MAP_SWIZZLE_64B);
+  return g;
+}
+
+namespace {
+__global__ void split_master_kernel(const float* __restrict__ w, int rows, int cols, int ld_w,
+                                    __nv_bfloat16* __restrict__ hi, uint16_t* __restrict__ lo,
+                                    int ld) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    uint32_t h, l;
+    split_master(w[r * ld_w + c], h, l);
+    reinterpret_cast<uint16_t*>(hi)[r * ld + c] = static_cast<uint16_t>(h);
+    lo[r * ld + c] = static_cast<uint16_t>(l);
+  }
+}
+__global__ void join_master_kernel(const __nv_bfloat16* __restrict__ hi,
+                                   const uint16_t* __restrict__ lo, int rows, int cols, int ld,
+                                   float* __restrict__ w, int ld_w) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    w[r * ld_w + c] = join_master(reinterpret_cast<const uint16_t*>(hi)[r * ld + c],
+                                  lo[r * ld + c]);
+  }
+}
+int conv_grid(size_t n) {
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 16)));
+}
+}  // namespace
+
+void launch_split_master(cudaStream_t st, const float* w, int rows, int cols, int ld_w,
+                         __nv_bfloat16* hi, uint16_t* lo, int ld) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  split_master_kernel<<<conv_grid(n), 256, 0, st>>>(w, rows, cols, ld_w, hi, lo, ld);
+  PB_CUDA(cudaGetLastError());
+}
+void launch_join_master(cudaStream_t st, const __nv_bfloat16* hi, const uint16_t* lo, int rows,
+                        int cols, int ld, float* w, int ld_w) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  join_master_kernel<<<conv_grid(n), 256, 0, st>>>(hi, lo, rows, cols, ld, w, ld_w);
+  PB_CUDA(cudaGetLastError());
+}
+
 void launch_fwd(const GemmLaunch& g, cudaStream_t st) {
   if (g.simt) return launch_simt_gemm(g, kEpiFwd, st);
   launch_bn<false, false, kEpiFwd>(g, st);

@@ -63,6 +63,21 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           const float* w_cur, float* w_new, int ld_w32,
                           __nv_bfloat16* w16, int ld_w16, float lr, bool verify = false);
 
+// wgrad+SGD with split fp32 masters (gemm_sm100.cuh: master = hi << 16 + lo):
+// reads hi/lo of the current version, writes hi (the new version's bf16
+// weights) and lo of the new one.  All four are [out, ld] 16-bit row-major.
+GemmLaunch plan_wgrad_sgd_split(const Mat16& dz, const Mat16& x, int x_row_off,
+                                const __nv_bfloat16* hi_cur, const uint16_t* lo_cur,
+                                __nv_bfloat16* hi_new, uint16_t* lo_new, int ld, float lr);
+// whether a layer's wgrad+SGD can run with split masters (the pair kernel's
+// TMA epilogue: out > 128, 16-byte rows, TMA epilogue not disabled)
+bool split_master_eligible(int out, int in, int ld);
+// fp32 [rows, cols] (ld_w) <-> hi bf16 + lo residual [rows, cols] (ld)
+void launch_split_master(cudaStream_t st, const float* w, int rows, int cols, int ld_w,
+                         __nv_bfloat16* hi, uint16_t* lo, int ld);
+void launch_join_master(cudaStream_t st, const __nv_bfloat16* hi, const uint16_t* lo, int rows,
+                        int cols, int ld, float* w, int ld_w);
+
 void launch_fwd(const GemmLaunch& g, cudaStream_t st);
 void launch_dgrad(const GemmLaunch& g, cudaStream_t st);
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st);

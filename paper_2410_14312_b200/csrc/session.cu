@@ -61,7 +61,8 @@ struct Session::Impl {
   struct LayerDev {
     int in = 0, out = 0, act = 0;
     int ld_in = 0, ld_out = 0;
-    float* w32[2] = {nullptr, nullptr};
+    float* w32[2] = {nullptr, nullptr};  // fp32 masters by version parity
+    uint16_t* lo[2] = {nullptr, nullptr};  // split masters: residuals by parity
     float* b32[2] = {nullptr, nullptr};
   };
   struct PoolSlot {
@@ -148,6 +149,9 @@ struct Session::Impl {
   // in the same layout; sc = bf16 slots per stored element (1 or 2)
   bool v32 = false;
   int sc = 1;
+  // split fp32 masters (gemm_sm100.cuh): version v's master is its pool
+  // slot's bf16 weights (hi) plus lo[v % 2]; no separate fp32 masters
+  bool split = false;
   // forwards and backwards of a stage on separate streams (split mode)
   bool split_fb = false;
   // bias gradients on their own stream (else on the wgrad side stream)
@@ -454,6 +458,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     for (int k = 1; k <= M; ++k) st.mini_act[k] = ac[k - 1];
   }
 
+  // ---------------- split masters: every local layer's wgrad+SGD must run the
+  // pair kernel's TMA epilogue (the verify precision and per-slot snapshots
+  // keep fp32 masters)
+  I.split = !I.v32 && !c.snapshots;
+  for (int s = 0; s < W && I.split; ++s) {
+    if (!I.local(s)) continue;
+    for (int gl = part[s].first_layer;
+         gl < part[s].first_layer + static_cast<int>(part[s].layers.size()); ++gl)
+      if (!split_master_eligible(c.widths[gl + 1], c.widths[gl], ld8(c.widths[gl])))
+        I.split = false;
+  }
+
   // ---------------- sizes
   I.n_out = c.widths.back();
   I.ld_x = ld8(c.widths.front());
@@ -474,7 +490,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       st.layers.push_back(d);
       st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
       if (!I.local(s)) continue;
-      need += 2 * (bytes_of(static_cast<size_t>(d.in) * d.out, 4) + bytes_of(d.out, 4));
+      need += 2 * ((I.split ? bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2)
+                            : bytes_of(static_cast<size_t>(d.in) * d.out, 4)) +
+                   bytes_of(d.out, 4));
       need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2 * I.sc) + bytes_of(d.out, 4));
       need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
       if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
@@ -510,7 +528,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     if (!I.local(s)) continue;
     for (auto& d : st.layers)
       for (int p = 0; p < 2; ++p) {
-        d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out);
+        if (I.split)
+          d.lo[p] = I.carve<uint16_t>(static_cast<size_t>(d.out) * d.ld_in);
+        else
+          d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out);
         d.b32[p] = I.carve<float>(d.out);
       }
     st.pool.resize(pool_n[s]);
@@ -631,9 +652,15 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       if (M % 2 == 1) {
         Impl::Op o{OK::copy};
         o.stream = s;
-        o.dst = d.w32[0];
-        o.src = d.w32[1];
-        o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
+        if (I.split) {
+          o.dst = d.lo[0];
+          o.src = d.lo[1];
+          o.bytes = sizeof(uint16_t) * d.out * static_cast<size_t>(d.ld_in);
+        } else {
+          o.dst = d.w32[0];
+          o.src = d.w32[1];
+          o.bytes = sizeof(float) * d.in * static_cast<size_t>(d.out);
+        }
         push(o);
         o.dst = d.b32[0];
         o.src = d.b32[1];
@@ -1049,9 +1076,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         {
           Impl::Op o{OK::wgrad};
           o.stream = side;
-          if (!c.plan_only)
-          o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
-                               d.ld_in, static_cast<float>(c.lr), I.v32);
+          if (!c.plan_only) {
+            if (I.split)  // master(k-1) = hi in version k-1's pool slot + lo[cur]
+              o.g = plan_wgrad_sgd_split(mdz, x, x_off,
+                                         st.pool[st.version_colour[tk.k - 1]].w16[l], d.lo[cur],
+                                         next.w16[l], d.lo[nxt], d.ld_in,
+                                         static_cast<float>(c.lr));
+            else
+              o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
+                                   d.ld_in, static_cast<float>(c.lr), I.v32);
+          }
           push(o);
           ++kernels_per_epoch_;
         }
@@ -1205,10 +1239,28 @@ void Session::load_params(const double* flat) {
       auto& d = st.layers[l];
       const size_t nw = static_cast<size_t>(d.in) * d.out;
       host.assign(flat + po, flat + po + nw + d.out);
-      PB_CUDA(cudaMemcpy(d.w32[0], host.data(), nw * 4, cudaMemcpyHostToDevice));
-      PB_CUDA(cudaMemcpy(d.b32[0], host.data() + nw, d.out * 4, cudaMemcpyHostToDevice));
-      PB_CUDA(cudaMemcpy(st.pool[c0].b32[l], host.data() + nw, d.out * 4,
-                         cudaMemcpyHostToDevice));
+      // every copy is ordered on the origin stream: a synchronous cudaMemcpy
+      // from pageable memory may return before its DMA lands, and the
+      // non-blocking origin stream's kernels below read the destination
+      PB_CUDA(cudaMemcpyAsync(d.b32[0], host.data() + nw, d.out * 4, cudaMemcpyHostToDevice,
+                              I.origin));
+      PB_CUDA(cudaMemcpyAsync(st.pool[c0].b32[l], host.data() + nw, d.out * 4,
+                              cudaMemcpyHostToDevice, I.origin));
+      PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
+      if (I.split) {  // version 0 = hi in pool colour(0) + lo[0] (lo[1] kept equal)
+        float* tmp = nullptr;
+        PB_CUDA(cudaMalloc(&tmp, nw * 4));
+        PB_CUDA(cudaMemcpyAsync(tmp, host.data(), nw * 4, cudaMemcpyHostToDevice, I.origin));
+        launch_split_master(I.origin, tmp, d.out, d.in, d.in, st.pool[c0].w16[l], d.lo[0],
+                            d.ld_in);
+        PB_CUDA(cudaMemcpyAsync(d.lo[1], d.lo[0], sizeof(uint16_t) * d.out * d.ld_in,
+                                cudaMemcpyDeviceToDevice, I.origin));
+        PB_CUDA(cudaStreamSynchronize(I.origin));
+        PB_CUDA(cudaFree(tmp));
+        po += nw + d.out;
+        continue;
+      }
+      PB_CUDA(cudaMemcpyAsync(d.w32[0], host.data(), nw * 4, cudaMemcpyHostToDevice, I.origin));
       if (I.v32)
         launch_rows_to_f32(I.origin, d.w32[0], false, d.out, d.in, d.in,
                            reinterpret_cast<float*>(st.pool[c0].w16[l]), d.ld_in);
@@ -1217,7 +1269,6 @@ void Session::load_params(const double* flat) {
                                 d.ld_in);
       // keep the odd master in sync so an M-odd rebase copy is always valid
       PB_CUDA(cudaMemcpyAsync(d.w32[1], d.w32[0], nw * 4, cudaMemcpyDeviceToDevice, I.origin));
-      PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
       po += nw + d.out;
     }
     // the rebase copies pool[colour(M)] -> pool[colour(0)]: make it a no-op
@@ -1242,41 +1293,54 @@ void Session::load_params(const double* flat) {
     }
 }
 
+namespace {
+// fp32 master of `version` of one stage's layers -> out (flat, W then b per
+// layer, widened to fp64); split masters are joined on the device first
+void read_master(Session::Impl& I, Session::Impl::Stage& st, int version, double* out) {
+  const int p = version & 1;
+  std::vector<float> host;
+  float* tmp = nullptr;
+  size_t po = 0;
+  for (size_t l = 0; l < st.layers.size(); ++l) {
+    auto& d = st.layers[l];
+    const size_t nw = static_cast<size_t>(d.in) * d.out;
+    host.resize(nw + d.out);
+    if (I.split) {
+      if (!tmp) {
+        size_t mx = 0;
+        for (auto& e : st.layers) mx = std::max(mx, static_cast<size_t>(e.in) * e.out);
+        PB_CUDA(cudaMalloc(&tmp, mx * 4));
+      }
+      launch_join_master(I.origin, st.pool[st.version_colour[version]].w16[l], d.lo[p], d.out,
+                         d.in, d.ld_in, tmp, d.in);
+      PB_CUDA(cudaStreamSynchronize(I.origin));
+      PB_CUDA(cudaMemcpy(host.data(), tmp, nw * 4, cudaMemcpyDeviceToHost));
+    } else {
+      PB_CUDA(cudaMemcpy(host.data(), d.w32[p], nw * 4, cudaMemcpyDeviceToHost));
+    }
+    PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[p], d.out * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < host.size(); ++i) out[po + i] = host[i];
+    po += nw + d.out;
+  }
+  if (tmp) PB_CUDA(cudaFree(tmp));
+}
+}  // namespace
+
 void Session::read_params(double* flat) {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
   PB_CUDA(cudaDeviceSynchronize());
-  const int p = cfg_.M % 2;  // current version M lives in master[M % 2]
-  std::vector<float> host;
   for (auto& st : I.stages) {
     if (!I.local(st.id - 1)) continue;  // other GPUs' stages stay untouched
-    size_t po = static_cast<size_t>(st.param_offset);
-    for (auto& d : st.layers) {
-      const size_t nw = static_cast<size_t>(d.in) * d.out;
-      host.resize(nw + d.out);
-      PB_CUDA(cudaMemcpy(host.data(), d.w32[p], nw * 4, cudaMemcpyDeviceToHost));
-      PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[p], d.out * 4, cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < host.size(); ++i) flat[po + i] = host[i];
-      po += nw + d.out;
-    }
+    read_master(I, st, cfg_.M, flat + st.param_offset);  // current version M
   }
 }
 
-void Session::read_stage_master(int stage, int parity, double* out) {
+void Session::read_stage_master(int stage, int version, double* out) {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
   PB_CUDA(cudaDeviceSynchronize());
-  auto& st = I.stages.at(stage - 1);
-  std::vector<float> host;
-  size_t po = 0;
-  for (auto& d : st.layers) {
-    const size_t nw = static_cast<size_t>(d.in) * d.out;
-    host.resize(nw + d.out);
-    PB_CUDA(cudaMemcpy(host.data(), d.w32[parity & 1], nw * 4, cudaMemcpyDeviceToHost));
-    PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[parity & 1], d.out * 4, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < host.size(); ++i) out[po + i] = host[i];
-    po += nw + d.out;
-  }
+  read_master(I, I.stages.at(stage - 1), version, out);
 }
 
 // ------------------------------------------------------------------ data

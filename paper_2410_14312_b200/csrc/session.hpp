@@ -135,7 +135,8 @@ class Session {
   bool has_snapshots() const { return cfg_.snapshots; }
   // fp32 master buffer `parity` (0/1) of stage s: holds the last committed
   // version with that parity (versions M and M-1 after an epoch).
-  void read_stage_master(int stage, int parity, double* out);
+  // fp32 master of `version` (M or M-1 after an epoch) of one stage
+  void read_stage_master(int stage, int version, double* out);
 
   // Host -> device copy of the epoch's data (rows = M*B), then conversion.
   void upload(const void* x, HostDType xt, const void* y, HostDType yt,
