@@ -450,6 +450,11 @@ def _stats(ms, fl, hbm_bytes=None):
     return d
 
 
+# HBM bytes of one wgrad+SGD launch (4096 x 4096 layer, one mini-batch):
+# split masters read hi + lo and write hi + lo (8 B / parameter) + dZ and X
+SGD_BYTES = WIDTH * WIDTH * 8 + 2 * 1024 * WIDTH * 2
+
+
 def kernel_roofline(peaks, runs):
     """Roofline of the dominant kernel, the forward GEMM (bias+ReLU fused):
     algorithmic flops of every forward launch of the timed step (2*rows*N*K)
@@ -479,12 +484,15 @@ def kernel_roofline(peaks, runs):
     alone[f"dgrad_1024x{n}x{n}"] = {"us": us, "tflops": 2.0 * 1024 * n * n / us / 1e6}
     del ws
     xx = K.padded_bf16(1024, n).normal_()
-    w32s = [torch.zeros(n, n, device="cuda") for _ in range(2)]
-    w16 = K.padded_bf16(n, n)
-    us = K.graph_time_us([lambda w=w: K.linear_bwd_dw_sgd(dz, xx, w, w, w16, 0.0) for w in w32s])
-    sgd_bytes = n * n * 10 + 2 * 1024 * n * 2  # master r/w + bf16 copy + dZ, X
+    # the session's split fp32 masters: read hi/lo of the current version,
+    # write hi/lo of the new one (8 B per parameter), two alternating sets
+    his = [K.padded_bf16(n, n) for _ in range(2)]
+    los = [torch.zeros(n, n, dtype=torch.int16, device="cuda") for _ in range(2)]
+    us = K.graph_time_us([lambda i=i: K.linear_bwd_dw_sgd_split(dz, xx, his[i], los[i], his[i],
+                                                                 los[i], 0.0)
+                          for i in range(2)])
     alone[f"wgrad_sgd_{n}x{n}x1024"] = {"us": us, "tflops": 2.0 * 1024 * n * n / us / 1e6,
-                                        "hbm_gbs": sgd_bytes / us / 1e3}
+                                        "hbm_gbs": SGD_BYTES / us / 1e3}
     traffic = None
     try:  # DRAM bytes per launch of the same kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -493,7 +501,7 @@ def kernel_roofline(peaks, runs):
         pass
     in_step = {}
     for kind, (ms, fl) in runs.items():
-        in_step[kind] = _stats(ms, fl, n * n * 10 + 2 * 1024 * n * 2 if kind == "wgrad" else None)
+        in_step[kind] = _stats(ms, fl, SGD_BYTES if kind == "wgrad" else None)
     achieved = in_step.get("fwd", {}).get("tflops")
     return {"bound": "tensor", "kernel": "forward GEMM gemm_bf16_tcgen05_pair/_tcgen05 "
             "(bias+ReLU epilogue), in-step", "achieved": achieved, "peak": peaks["bf16_sus"],

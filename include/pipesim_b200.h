@@ -179,6 +179,21 @@ int pb_linear_bwd_dw_sgd(void* stream, const uint16_t* dz, int rows, int out,
                          const float* w_cur, float* w_new, int ld_w32,
                          uint16_t* w16, int ld_w16, float lr);
 
+/* Split fp32 masters (the session's default for layers with out > 128):
+ * master = bits(hi) << 16 + lo (exact), hi the version's bf16 weights, lo a
+ * 16-bit residual.  master_new = master_cur - lr * dz^T x, written as
+ * hi_new / lo_new.  All four are out x in, leading dimension ld (multiple of
+ * 8).  Same replacement as pb_linear_bwd_dw_sgd. */
+int pb_linear_bwd_dw_sgd_split(void* stream, const uint16_t* dz, int rows, int out, int ld_dz,
+                               const uint16_t* x, int in, int ld_x, const uint16_t* hi_cur,
+                               const uint16_t* lo_cur, uint16_t* hi_new, uint16_t* lo_new,
+                               int ld, float lr);
+/* fp32 out x in (ld_w) <-> split master (hi, lo; ld). */
+int pb_split_master(void* stream, const float* w, int out, int in, int ld_w, uint16_t* hi,
+                    uint16_t* lo, int ld);
+int pb_join_master(void* stream, const uint16_t* hi, const uint16_t* lo, int out, int in, int ld,
+                   float* w, int ld_w);
+
 /* b_new = b_cur - lr * colsum(dz); b_copy (may be NULL) = b_new.
  * Replaces trainer.cpp:250-252 + :484-488 for the bias. */
 int pb_bias_sgd(void* stream, const uint16_t* dz, int rows, int out, int ld_dz,

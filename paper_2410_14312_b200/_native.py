@@ -145,6 +145,9 @@ def _declare(L: C.CDLL) -> None:
         "pb_linear_fwd": (i, [p, p, i, i, i, p, i, i, p, i, p, i, p, i]),
         "pb_linear_bwd_dx": (i, [p, p, i, i, i, p, i, i, p, i, i, p, i]),
         "pb_linear_bwd_dw_sgd": (i, [p, p, i, i, i, p, i, i, p, p, i, p, i, f]),
+        "pb_linear_bwd_dw_sgd_split": (i, [p, p, i, i, i, p, i, i, p, p, p, p, i, f]),
+        "pb_split_master": (i, [p, p, i, i, i, p, p, i]),
+        "pb_join_master": (i, [p, p, p, i, i, i, p, i]),
         "pb_bias_sgd": (i, [p, p, i, i, i, p, p, p, f]),
         "pb_loss_fwd_bwd": (i, [p, p, i, i, i, p, i, i, i, f, p, i, p]),
         "pb_convert_f64_to_bf16": (i, [p, p, i, i, i, p, i]),

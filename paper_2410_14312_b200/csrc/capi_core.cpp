@@ -157,6 +157,33 @@ int pb_linear_bwd_dw_sgd(void* stream, const uint16_t* dz, int rows, int out,
   PB_GUARD_END
 }
 
+int pb_linear_bwd_dw_sgd_split(void* stream, const uint16_t* dz, int rows, int out, int ld_dz,
+                               const uint16_t* x, int in, int ld_x, const uint16_t* hi_cur,
+                               const uint16_t* lo_cur, uint16_t* hi_new, uint16_t* lo_new,
+                               int ld, float lr) {
+  PB_GUARD_BEGIN
+  pb::Mat16 mdz{bf(dz), rows, out, ld_dz};
+  pb::Mat16 mx{bf(x), rows, in, ld_x};
+  pb::GemmLaunch g =
+      pb::plan_wgrad_sgd_split(mdz, mx, 0, bf(hi_cur), lo_cur, bfm(hi_new), lo_new, ld, lr);
+  pb::launch_wgrad(g, as_stream(stream));
+  PB_GUARD_END
+}
+
+int pb_split_master(void* stream, const float* w, int out, int in, int ld_w, uint16_t* hi,
+                    uint16_t* lo, int ld) {
+  PB_GUARD_BEGIN
+  pb::launch_split_master(as_stream(stream), w, out, in, ld_w, bfm(hi), lo, ld);
+  PB_GUARD_END
+}
+
+int pb_join_master(void* stream, const uint16_t* hi, const uint16_t* lo, int out, int in, int ld,
+                   float* w, int ld_w) {
+  PB_GUARD_BEGIN
+  pb::launch_join_master(as_stream(stream), bf(hi), lo, out, in, ld, w, ld_w);
+  PB_GUARD_END
+}
+
 int pb_bias_sgd(void* stream, const uint16_t* dz, int rows, int out, int ld_dz,
                 const float* b_cur, float* b_new, float* b_copy, float lr) {
   PB_GUARD_BEGIN

@@ -59,6 +59,27 @@ def linear_bwd_dw_sgd(dz, x, w_cur, w_new, w16, lr):
         float(lr)))
 
 
+def linear_bwd_dw_sgd_split(dz, x, hi_cur, lo_cur, hi_new, lo_new, lr):
+    """Split-master wgrad+SGD: hi_* bf16 [out, ld], lo_* int16 [out, ld]."""
+    rows, out = dz.shape
+    inn = x.shape[1]
+    _native.check(_native.lib().pb_linear_bwd_dw_sgd_split(
+        _stream(), _ptr(dz), rows, out, _ld(dz), _ptr(x), inn, _ld(x), _ptr(hi_cur),
+        _ptr(lo_cur), _ptr(hi_new), _ptr(lo_new), _ld(hi_cur), float(lr)))
+
+
+def split_master(w, hi, lo):
+    out, inn = w.shape
+    _native.check(_native.lib().pb_split_master(_stream(), _ptr(w), out, inn, _ld(w), _ptr(hi),
+                                                _ptr(lo), _ld(hi)))
+
+
+def join_master(hi, lo, w):
+    out, inn = w.shape
+    _native.check(_native.lib().pb_join_master(_stream(), _ptr(hi), _ptr(lo), out, inn, _ld(hi),
+                                               _ptr(w), _ld(w)))
+
+
 def bias_sgd(dz, b_cur, b_new, b_copy, lr):
     rows, out = dz.shape
     _native.check(_native.lib().pb_bias_sgd(

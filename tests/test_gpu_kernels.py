@@ -105,6 +105,43 @@ def test_linear_bwd_dw_sgd(rows, out, inn):
     assert _rel(w16, ref) < 2 ** -8
 
 
+def _padded_i16(rows, cols):
+    ld = (cols + 7) // 8 * 8
+    return torch.zeros(rows, ld, dtype=torch.int16, device="cuda")[:, :cols]
+
+
+@pytest.mark.parametrize("rows,out,inn", [(256, 512, 784), (1024, 4096, 4096), (300, 136, 72),
+                                          (512, 1000, 520)])
+def test_linear_bwd_dw_sgd_split_master(rows, out, inn):
+    """Split fp32 masters (hi = bf16 operand, lo = 16-bit residual): the
+    split / join round trip is exact, the update matches the fp32-master
+    kernel bit for bit (same fp32 arithmetic), and hi is the new master
+    rounded to bf16 (nearest; exact ties away from zero)."""
+    dz = K.padded_bf16(rows, out)
+    dz.copy_(torch.randn(rows, out, device="cuda") * 1e-2)
+    x = K.padded_bf16(rows, inn)
+    x.copy_(torch.rand(rows, inn, device="cuda"))
+    w_cur = (torch.rand(out, inn, device="cuda") * 2 - 1)
+    hi, lo = K.padded_bf16(out, inn), _padded_i16(out, inn)
+    K.split_master(w_cur, hi, lo)
+    back = torch.empty_like(w_cur)
+    K.join_master(hi, lo, back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, w_cur)
+    hi2, lo2 = K.padded_bf16(out, inn), _padded_i16(out, inn)
+    lr = 0.5
+    K.linear_bwd_dw_sgd_split(dz, x, hi, lo, hi2, lo2, lr)
+    w_new = torch.empty_like(w_cur)
+    K.join_master(hi2, lo2, w_new)
+    ref_new = torch.empty_like(w_cur)
+    K.linear_bwd_dw_sgd(dz, x, w_cur, ref_new, None, lr)
+    torch.cuda.synchronize()
+    assert torch.equal(w_new, ref_new)
+    assert torch.equal(hi2.float(), w_new.to(torch.bfloat16).float()) or \
+        (hi2.float() - w_new.to(torch.bfloat16).float()).abs().max() <= \
+        w_new.abs().max() * 2 ** -7  # ties only
+
+
 def test_wgrad_in_place():
     rows, out, inn = 128, 256, 256
     dz = K.padded_bf16(rows, out)

@@ -27,7 +27,11 @@ if cub:
 xx = K.padded_bf16(1024, n); xx.normal_()
 w32s = [torch.zeros(n, n, device="cuda") for _ in range(2)]
 w16 = K.padded_bf16(n, n)
-res["wgrad"] = K.graph_time_us([lambda w=w: K.linear_bwd_dw_sgd(dz, xx, w, w, w16, 0.0) for w in w32s])
+res["wgrad32"] = K.graph_time_us([lambda w=w: K.linear_bwd_dw_sgd(dz, xx, w, w, w16, 0.0) for w in w32s])
+his = [K.padded_bf16(n, n) for _ in range(2)]
+los = [torch.zeros(n, n, dtype=torch.int16, device="cuda") for _ in range(2)]
+res["wgrad"] = K.graph_time_us([lambda i=i: K.linear_bwd_dw_sgd_split(dz, xx, his[i], los[i], his[i], los[i], 0.0)
+                                for i in range(2)])
 if cub:
     res["cublas_wgrad"] = K.graph_time_us(lambda: torch.mm(dz.t(), xx))
 env = {k: v for k, v in os.environ.items() if k.startswith("PIPESIM_")}

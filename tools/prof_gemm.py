@@ -24,7 +24,11 @@ if "dgrad" in which:
     dz = K.padded_bf16(m, k); dz.normal_(); w = K.padded_bf16(k, n); w.normal_()
     xin = K.padded_bf16(m, n); xin.normal_(); d = K.padded_bf16(m, n)
     for _ in range(reps): K.linear_bwd_dx(dz, w, xin, "relu", d)
-if "wgrad" in which:
+if "wgrad" in which:  # split fp32 masters, as in the session
+    dz = K.padded_bf16(m, k); dz.normal_(); xx = K.padded_bf16(m, n); xx.normal_()
+    hi = K.padded_bf16(k, n); lo = torch.zeros(k, n, dtype=torch.int16, device="cuda")
+    for _ in range(reps): K.linear_bwd_dw_sgd_split(dz, xx, hi, lo, hi, lo, 0.0)
+if "wgrad32" in which:  # fp32 masters + bf16 copy
     dz = K.padded_bf16(m, k); dz.normal_(); xx = K.padded_bf16(m, n); xx.normal_()
     w32 = torch.zeros(k, n, device="cuda"); w16 = K.padded_bf16(k, n)
     for _ in range(reps): K.linear_bwd_dw_sgd(dz, xx, w32, w32, w16, 0.0)
