@@ -38,7 +38,7 @@ CPU reference, in-step kernel timing), `profiles/round1_launches_step_m4.csv`
 (ncu launch list of `tools/prof_step.py 4`: parameter load + upload + two
 4-mini-batch epochs of the benchmark network), `profiles/ncu_round1_full.md` /
 `profiles/ncu_traffic.json` (`ncu --set full` of
-`tools/prof_gemm.py fwd1024,dgrad,wgrad 1`, split-K off as in the executor),
+`tools/prof_gemm.py fwd1024,dgrad,wgrad 1`, split-K off as in the executor, wgrad with split masters),
 `profiles/round1_bench_reference.json` (`bench.py --impl reference`),
 `profiles/sweep_c5_r1.*` (`tools/sweep.py`).  Regenerate with
 `python tools/make_summary.py`.
