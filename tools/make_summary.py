@@ -98,7 +98,7 @@ TMA) outlasts the mainloop (DESIGN.md §9).
 Algorithmic versus measured DRAM traffic per launch (`profiles/ncu_traffic.json`):
 - **fwd 1024x4096x4096**: W 32 MiB + X 8 MiB + Y 8 MiB = 50.3 MB; measured {traffic['fwd_1024x4096x4096']['bytes']/1e6:.2f} MB.
 - **dgrad 1024x4096x4096**: dZ 8 MiB + W 32 MiB + stored activation (act' gate) 8 MiB + out 8 MiB = 58.7 MB; measured {traffic['dgrad_1024x4096x4096']['bytes']/1e6:.1f} MB (the written delta stays in L2).
-- **wgrad+SGD 4096x4096x1024**: dZ 8 MiB + X 8 MiB + fp32 master read 64 MiB + write 64 MiB + bf16 write 32 MiB = 184 MB; measured {traffic['wgrad_sgd_4096x4096x1024']['bytes']/1e6:.1f} MB (the rest of the new masters is still in L2 when the kernel ends).
+- **wgrad+SGD 4096x4096x1024** (split masters): dZ 8 MiB + X 8 MiB + hi/lo of the current version 64 MiB read + hi/lo of the new version 64 MiB written = 151 MB; measured {traffic['wgrad_sgd_4096x4096x1024']['bytes']/1e6:.1f} MB (most of the new hi/lo is still in L2 when the kernel ends).
 
 ## C5 sweep: version difference, throughput and bubble per (W, N)
 
@@ -113,6 +113,7 @@ model's idle fraction is the reference metric (metrics.cpp:71-72).
 - 256 x 512 pair tiles for >= 512-row wide layers (MMA-bound mainloop, ~88% of the per-SM MMA rate, on half the SMs): slower alone (fwd 1024 rows 28.7 -> 48 us on 64 SMs), less SM-time per flop in the step: 558k -> 567k samples/s.
 - interior fast path of the vector epilogue (one pointer per 32x32 block, no per-row checks): fwd 1024 rows 48.1 -> 45.4 us, dgrad 53.4 -> 50.6 us.
 - timed step without the kernel-timing event nodes (in-step kernel timing moved to separate sessions): +3-8% on the reported step.
+- split fp32 masters (bf16 operand + 16-bit residual, exact): the SGD epilogue stores 4 instead of 6 bytes per parameter; wgrad+SGD 47.3 -> 44.6 us alone, 581k -> 605k samples/s.
 - vector staged-transpose epilogue: wgrad+SGD 68 -> 57.6 us (same ring depth).
 - TMA epilogue for the SGD update: 57.6 -> 48.3 us.
 - separate forward / backward streams per stage (explicit hazard edges), forward runs spanning another mini-batch's backward: 1238 -> 992 forward launches per step, 525k -> 556k samples/s.
