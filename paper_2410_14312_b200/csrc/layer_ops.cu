@@ -480,45 +480,42 @@ GemmLaunch plan_wgrad_sgd_split(const Mat16& dz, const Mat16& x, int x_row_off,
 }
 
 namespace {
+// one row per blockIdx.y step, columns across threads (no per-element
+// division; this runs once per parameter upload / read-back)
 __global__ void split_master_kernel(const float* __restrict__ w, int rows, int cols, int ld_w,
                                     __nv_bfloat16* __restrict__ hi, uint16_t* __restrict__ lo,
                                     int ld) {
-  const size_t n = static_cast<size_t>(rows) * cols;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / cols, c = i % cols;
-    uint32_t h, l;
-    split_master(w[r * ld_w + c], h, l);
-    reinterpret_cast<uint16_t*>(hi)[r * ld + c] = static_cast<uint16_t>(h);
-    lo[r * ld + c] = static_cast<uint16_t>(l);
-  }
+  for (int r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+      uint32_t h, l;
+      split_master(w[static_cast<size_t>(r) * ld_w + c], h, l);
+      reinterpret_cast<uint16_t*>(hi)[static_cast<size_t>(r) * ld + c] = static_cast<uint16_t>(h);
+      lo[static_cast<size_t>(r) * ld + c] = static_cast<uint16_t>(l);
+    }
 }
 __global__ void join_master_kernel(const __nv_bfloat16* __restrict__ hi,
                                    const uint16_t* __restrict__ lo, int rows, int cols, int ld,
                                    float* __restrict__ w, int ld_w) {
-  const size_t n = static_cast<size_t>(rows) * cols;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / cols, c = i % cols;
-    w[r * ld_w + c] = join_master(reinterpret_cast<const uint16_t*>(hi)[r * ld + c],
-                                  lo[r * ld + c]);
-  }
+  for (int r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x)
+      w[static_cast<size_t>(r) * ld_w + c] =
+          join_master(reinterpret_cast<const uint16_t*>(hi)[static_cast<size_t>(r) * ld + c],
+                      lo[static_cast<size_t>(r) * ld + c]);
 }
-int conv_grid(size_t n) {
-  return static_cast<int>(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 16)));
+dim3 conv_grid(int rows, int cols) {
+  return dim3(static_cast<unsigned>(std::max(1, std::min((cols + 255) / 256, 16))),
+              static_cast<unsigned>(std::max(1, std::min(rows, 148 * 8))));
 }
 }  // namespace
 
 void launch_split_master(cudaStream_t st, const float* w, int rows, int cols, int ld_w,
                          __nv_bfloat16* hi, uint16_t* lo, int ld) {
-  const size_t n = static_cast<size_t>(rows) * cols;
-  split_master_kernel<<<conv_grid(n), 256, 0, st>>>(w, rows, cols, ld_w, hi, lo, ld);
+  split_master_kernel<<<conv_grid(rows, cols), 256, 0, st>>>(w, rows, cols, ld_w, hi, lo, ld);
   PB_CUDA(cudaGetLastError());
 }
 void launch_join_master(cudaStream_t st, const __nv_bfloat16* hi, const uint16_t* lo, int rows,
                         int cols, int ld, float* w, int ld_w) {
-  const size_t n = static_cast<size_t>(rows) * cols;
-  join_master_kernel<<<conv_grid(n), 256, 0, st>>>(hi, lo, rows, cols, ld, w, ld_w);
+  join_master_kernel<<<conv_grid(rows, cols), 256, 0, st>>>(hi, lo, rows, cols, ld, w, ld_w);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -79,8 +79,9 @@ cuBLAS (torch.mm bf16, same harness, no fused epilogues): fwd 256 rows 11.1 us,
 
 ## Kernel share (ncu launch list; serialised, cold caches: compare shares)
 
-The list covers a short session's setup (parameter load: `to_bf16_kernel`)
-as well as two epochs; the step itself is the three GEMMs, bias and loss.
+The list covers a short session's setup (parameter load: `split_master_kernel`
+turns the fp32 masters into the pool's hi/lo, `to_bf16_kernel` the data) as
+well as two epochs; the step itself is the three GEMMs, bias and loss.
 
 ```
 {launch}```
