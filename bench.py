@@ -356,6 +356,10 @@ def main():
                            if not split else {})
     roof["step_gemm_tflops"] = step_tflops
     roof["step_frac_of_sustained"] = step_tflops / peaks["bf16_sus"]
+    if split:
+        roof["note"] = ("in-step per-launch timing runs only in the single-process (N=1) "
+                        "configuration; with the stages split over processes the line gives "
+                        "the alone table and the step-level GEMM rate")
 
     cb = None
     if cpu_finish is not None:
