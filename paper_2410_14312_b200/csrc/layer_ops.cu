@@ -706,11 +706,70 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) row_loss[row] = acc;
 }
 
+// Softmax-CE against class labels with a linear output layer (the benchmark
+// head): each thread keeps its <= 16 logits in registers (four float4), so
+// the row is read once and exp is evaluated once per logit; max, sum and the
+// gradient as in loss_kernel, the row loss from the label's logit.
+__global__ void __launch_bounds__(256)
+    loss_ce_labels_kernel(const float* __restrict__ y, int cols, int ld_y, float denom,
+                          __nv_bfloat16* __restrict__ dz, int ld_dz,
+                          float* __restrict__ row_loss, const int* __restrict__ labels) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const float4* yr = reinterpret_cast<const float4*>(y + static_cast<size_t>(row) * ld_y);
+  const int nq = cols / 4;
+  const int lab = labels[row];
+  float4 v[4];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = threadIdx.x + 256 * i;
+    v[i] = q < nq ? yr[q] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    mx = fmaxf(mx, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+  }
+  mx = block_max(mx, red);
+  float se = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = make_float4(expf(v[i].x - mx), expf(v[i].y - mx), expf(v[i].z - mx),
+                       expf(v[i].w - mx));  // exp(-inf) = 0 for the padding
+    se += v[i].x + v[i].y + v[i].z + v[i].w;
+  }
+  se = block_sum(se, red);
+  if (threadIdx.x == 0) {
+    const float lse = logf(se);
+    row_loss[row] = (lab >= 0 && lab < cols)
+                        ? -((y[static_cast<size_t>(row) * ld_y + lab] - mx) - lse) : 0.f;
+  }
+  __nv_bfloat16* dr = dz + static_cast<size_t>(row) * ld_dz;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = threadIdx.x + 256 * i;
+    if (q >= nq) continue;
+    const int c = 4 * q;
+    const float g0 = (v[i].x / se - (c == lab ? 1.f : 0.f)) / denom;
+    const float g1 = (v[i].y / se - (c + 1 == lab ? 1.f : 0.f)) / denom;
+    const float g2 = (v[i].z / se - (c + 2 == lab ? 1.f : 0.f)) / denom;
+    const float g3 = (v[i].w / se - (c + 3 == lab ? 1.f : 0.f)) / denom;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(g0, g1);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(g2, g3);
+    *reinterpret_cast<uint2*>(dr + c) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+  }
+}
+
 void launch_loss(cudaStream_t st, const float* y, int rows, int cols, int ld_y,
                  const float* targets, int ld_t, int loss, int act_last,
                  float denom, __nv_bfloat16* dz, int ld_dz, float* row_loss, bool dz_f32,
                  const int* labels) {
   if (rows <= 0) return;
+  if (loss != 0 && labels && act_last == kLinear && !dz_f32 && cols % 4 == 0 && cols <= 4096 &&
+      cols >= 1024 && ld_y % 4 == 0 && ld_dz % 4 == 0 && al(y, 16) && al(dz, 8)) {
+    loss_ce_labels_kernel<<<rows, 256, 0, st>>>(y, cols, ld_y, denom, dz, ld_dz, row_loss,
+                                                labels);
+    PB_CUDA(cudaGetLastError());
+    return;
+  }
   const int threads = cols >= 256 ? 256 : (cols >= 128 ? 128 : 64);
   if (dz_f32)
     loss_kernel<float><<<rows, threads, 0, st>>>(y, rows, cols, ld_y, targets, ld_t, loss,
