@@ -360,7 +360,12 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
   }
   g.bn = pick_bn(dz.rows, w.cols);
   g.pair = use_pair(dz.rows);
-  if (g.pair && wide_tiles(dz.rows, w.cols)) g.bn = 512;
+  // (PIPESIM_BN512_DGRAD=0: dgrad keeps 256-wide tiles, twice the SMs)
+  static const bool dgrad_wide = [] {
+    const char* e = std::getenv("PIPESIM_BN512_DGRAD");
+    return !(e && std::string(e) == "0");
+  }();
+  if (g.pair && dgrad_wide && wide_tiles(dz.rows, w.cols)) g.bn = 512;
   g.ta = make_operand_tmap(dz, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.rows, w.cols, dz.cols, 0, 0, 0, 0};
