@@ -115,6 +115,7 @@ model's idle fraction is the reference metric (metrics.cpp:71-72).
 - interior fast path of the vector epilogue (one pointer per 32x32 block, no per-row checks): fwd 1024 rows 48.1 -> 45.4 us, dgrad 53.4 -> 50.6 us.
 - timed step without the kernel-timing event nodes (in-step kernel timing moved to separate sessions): +3-8% on the reported step.
 - split fp32 masters (bf16 operand + 16-bit residual, exact): the SGD epilogue stores 4 instead of 6 bytes per parameter; wgrad+SGD 47.3 -> 44.6 us alone, 581k -> 605k samples/s.
+- register-resident softmax-CE for class labels (row read once, one exp per logit; on the critical path): 24.6 -> 11.5 us per mini-batch, ~605k -> ~612-620k samples/s.
 - vector staged-transpose epilogue: wgrad+SGD 68 -> 57.6 us (same ring depth).
 - TMA epilogue for the SGD update: 57.6 -> 48.3 us.
 - separate forward / backward streams per stage (explicit hazard edges), forward runs spanning another mini-batch's backward: 1238 -> 992 forward launches per step, 525k -> 556k samples/s.
