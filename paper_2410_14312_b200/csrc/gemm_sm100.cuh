@@ -526,6 +526,19 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
               make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
         }
         done = true;
+      } else if (full && ep.y32 && !ep.y16) {  // fp32 logits of the output layer
+        float* dst = ep.y32 + static_cast<size_t>(row_base + ep.y_row_off + sub_r) * ep.ld_y32 + n;
+        const size_t step = static_cast<size_t>(4) * ep.ld_y32;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int rl = rr * 4 + sub_r;
+          const float4 a =
+              *reinterpret_cast<const float4*>(T + rl * kVecLd + vec_slot(rl, c4 / 4));
+          *reinterpret_cast<float4*>(dst + rr * step) =
+              make_float4(act_fwd_t<ACT>(a.x + bias4.x), act_fwd_t<ACT>(a.y + bias4.y),
+                          act_fwd_t<ACT>(a.z + bias4.z), act_fwd_t<ACT>(a.w + bias4.w));
+        }
+        done = true;
       }
     } else if constexpr (EPI == kEpiDgrad) {
       if (full) {
