@@ -148,6 +148,23 @@ int pb_make_synthetic_task(int samples, uint64_t seed, double* x, double* y);
  * values[0..n) each followed by '\n'; out receives 16 hex chars + NUL. */
 int pb_params_digest(const double* values, int64_t n, char* out17);
 
+/* checkpoint_stage / restore_stage (checkpoint.hpp:29-44; file format of
+ * checkpoint.cpp:39-153).  A stage is its id, first layer, n_layers
+ * (in, out, PB_ACT_*) triples in `layers`, and the current version's flat
+ * params (per layer W out x in, then b).  Errors: PB_ERR_IO (cannot write),
+ * PB_ERR_INTEGRITY (missing / truncated / tampered / wrong stage or epoch;
+ * pb_last_error_stage_epoch names the expected stage and epoch). */
+int pb_checkpoint_stage(int stage_id, int first_layer, int n_layers, const int* layers,
+                        int version, const double* params, int64_t n, int loss, int epoch,
+                        const char* path);
+typedef struct {
+  int stage_id, first_layer, n_layers, version, loss, epoch;
+  int64_t n_values;
+} pb_restored_stage;
+int pb_restore_stage(const char* path, int expected_stage, int expected_epoch,
+                     pb_restored_stage* info, int* layers, int layers_cap, double* params,
+                     int64_t cap);
+
 /* ------------------------------------------------------------ device layer
  * Per-op kernels on device pointers (bf16 = uint16 storage).  `stream` is a
  * cudaStream_t (NULL = legacy default stream).  Leading dimensions are in

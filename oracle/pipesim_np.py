@@ -199,8 +199,9 @@ def format_double(v: float) -> str:
 
 
 def fnv1a64_hex(data: bytes) -> str:
-    """text.cpp:39-51."""
-    h = 0xCBF29CE484222325
+    """text.cpp:39-51.  The reference's offset basis is 1469598103934665603
+    (not the textbook 14695981039346656037)."""
+    h = 1469598103934665603
     for c in data:
         h ^= c
         h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF

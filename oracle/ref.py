@@ -207,3 +207,20 @@ def network_gradient(widths, acts, loss, params, x, y):
                                       _dp(np.ascontiguousarray(params, np.float64)),
                                       x.shape[0], _dp(x), _dp(y), _dp(out)))
     return out
+
+
+def checkpoint_stage(stage_id, first_layer, layers, version, params, loss, epoch, path):
+    """Reference checkpoint_stage; layers = [(in, out, act_id), ...]."""
+    lay = np.ascontiguousarray(layers, np.int32)
+    p = np.ascontiguousarray(params, np.float64)
+    _check(lib().ref_checkpoint_stage(stage_id, first_layer, len(lay), _ip(lay), version,
+                                      _dp(p), len(p), loss, epoch, str(path).encode()))
+
+
+def restore_stage(path, expected_stage=0, expected_epoch=0, cap=1 << 24):
+    """Reference restore_stage -> (params, version, epoch)."""
+    out = np.zeros(cap)
+    n, v, e = C.c_int(), C.c_int(), C.c_int()
+    _check(lib().ref_restore_stage(str(path).encode(), expected_stage, expected_epoch, _dp(out),
+                                   cap, C.byref(n), C.byref(v), C.byref(e)))
+    return out[:n.value].copy(), v.value, e.value

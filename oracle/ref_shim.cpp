@@ -360,4 +360,48 @@ int ref_network_gradient(int n_layers, const int* widths, const int* acts, int l
   }
 }
 
+// checkpoint_stage of the reference (checkpoint.cpp:39-67) for one stage
+// given as (stage_id, first_layer, layers as in/out/act triples, version,
+// params); used to byte-compare checkpoint files and cross-restore them.
+int ref_checkpoint_stage(int stage_id, int first_layer, int n_layers, const int* layers,
+                         int version, const double* params, int n, int loss, int epoch,
+                         const char* path) {
+  try {
+    stage_model st;
+    st.stage_id = stage_id;
+    st.first_layer = first_layer;
+    for (int i = 0; i < n_layers; ++i) {
+      layer_spec l;
+      l.in = layers[3 * i];
+      l.out = layers[3 * i + 1];
+      l.act = static_cast<activation_kind>(layers[3 * i + 2]);
+      st.layers.push_back(l);
+    }
+    st.version_store[version] = std::vector<double>(params, params + n);
+    st.current_version = version;
+    checkpoint_stage(st, loss == 0 ? loss_kind::mse : loss_kind::softmax_cross_entropy, epoch,
+                     path);
+    return 0;
+  } catch (...) {
+    return fail();
+  }
+}
+
+// restore_stage of the reference; writes the current params (n = count).
+int ref_restore_stage(const char* path, int expected_stage, int expected_epoch, double* params,
+                      int cap, int* n, int* version, int* epoch) {
+  try {
+    const restored_stage r = restore_stage(path, expected_stage, expected_epoch);
+    const auto& p = r.stage.current_params();
+    if (static_cast<int>(p.size()) > cap) return 9;
+    std::memcpy(params, p.data(), p.size() * sizeof(double));
+    *n = static_cast<int>(p.size());
+    *version = r.stage.current_version;
+    *epoch = r.epoch;
+    return 0;
+  } catch (...) {
+    return fail();
+  }
+}
+
 }  // extern "C"

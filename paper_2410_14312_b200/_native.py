@@ -88,6 +88,12 @@ class pb_interval(C.Structure):
                 ("freed_slot", C.c_int)]
 
 
+class pb_restored_stage(C.Structure):
+    _fields_ = [("stage_id", C.c_int), ("first_layer", C.c_int), ("n_layers", C.c_int),
+                ("version", C.c_int), ("loss", C.c_int), ("epoch", C.c_int),
+                ("n_values", C.c_int64)]
+
+
 class pb_net_spec(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("widths", C.POINTER(C.c_int)),
                 ("activations", C.POINTER(C.c_int)), ("loss", C.c_int)]
@@ -139,6 +145,8 @@ def _declare(L: C.CDLL) -> None:
         "pb_init_network_params": (i, [P(pb_net_spec), u64, P(d), i64]),
         "pb_make_synthetic_task": (i, [i, u64, P(d), P(d)]),
         "pb_params_digest": (i, [P(d), i64, C.c_char_p]),
+        "pb_checkpoint_stage": (i, [i, i, i, P(i), i, P(d), i64, i, i, C.c_char_p]),
+        "pb_restore_stage": (i, [C.c_char_p, i, i, P(pb_restored_stage), P(i), i, P(d), i64]),
         "pb_device_count": (i, [P(i)]),
         "pb_set_device": (i, [i]),
         "pb_synchronize": (i, []),

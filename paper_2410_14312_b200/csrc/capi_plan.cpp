@@ -308,14 +308,56 @@ int pb_make_synthetic_task(int samples, uint64_t seed, double* x, double* y) {
 
 int pb_params_digest(const double* values, int64_t n, char* out17) {
   PB_GUARD_BEGIN
-  std::string text;
-  text.reserve(static_cast<size_t>(n) * 20);
-  for (int64_t i = 0; i < n; ++i) {
-    text += format_double(values[i]);
-    text.push_back('\n');
-  }
-  const std::string h = fnv1a64_hex(text);
+  const std::string h = pb::digest_spans({{values, n}});
   std::memcpy(out17, h.c_str(), 17);
+  PB_GUARD_END
+}
+
+int pb_checkpoint_stage(int stage_id, int first_layer, int n_layers, const int* layers,
+                        int version, const double* params, int64_t n, int loss, int epoch,
+                        const char* path) {
+  PB_GUARD_BEGIN
+  if (!path || (n > 0 && !params) || n_layers < 1 || !layers)
+    throw std::invalid_argument("pb_checkpoint_stage: null argument");
+  stage_model st;
+  st.stage_id = stage_id;
+  st.first_layer = first_layer;
+  for (int i = 0; i < n_layers; ++i)
+    st.layers.push_back({layers[3 * i], layers[3 * i + 1],
+                         static_cast<activation_kind>(layers[3 * i + 2])});
+  if (st.param_count() != n)
+    throw pipesim::structural_error("stage holds " + std::to_string(st.param_count()) +
+                                    " params, got " + std::to_string(n));
+  st.version_store[version].assign(params, params + n);
+  st.current_version = version;
+  checkpoint_stage(st, loss == PB_LOSS_MSE ? loss_kind::mse : loss_kind::softmax_cross_entropy,
+                   epoch, path);
+  PB_GUARD_END
+}
+
+int pb_restore_stage(const char* path, int expected_stage, int expected_epoch,
+                     pb_restored_stage* info, int* layers, int layers_cap, double* params,
+                     int64_t cap) {
+  PB_GUARD_BEGIN
+  if (!path || !info) throw std::invalid_argument("pb_restore_stage: null argument");
+  const restored_stage r = restore_stage(path, expected_stage, expected_epoch);
+  const std::vector<double>& p = r.stage.current_params();
+  info->stage_id = r.stage.stage_id;
+  info->first_layer = r.stage.first_layer;
+  info->n_layers = static_cast<int>(r.stage.layers.size());
+  info->version = r.stage.current_version;
+  info->loss = r.loss == loss_kind::mse ? PB_LOSS_MSE : PB_LOSS_SOFTMAX_CE;
+  info->epoch = r.epoch;
+  info->n_values = static_cast<int64_t>(p.size());
+  if (info->n_layers > layers_cap || info->n_values > cap)
+    throw pb::capacity_error("checkpoint holds " + std::to_string(info->n_layers) +
+                             " layers / " + std::to_string(info->n_values) + " values");
+  for (int i = 0; i < info->n_layers; ++i) {
+    layers[3 * i] = r.stage.layers[i].in;
+    layers[3 * i + 1] = r.stage.layers[i].out;
+    layers[3 * i + 2] = static_cast<int>(r.stage.layers[i].act);
+  }
+  std::memcpy(params, p.data(), p.size() * sizeof(double));
   PB_GUARD_END
 }
 

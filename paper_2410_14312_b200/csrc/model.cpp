@@ -30,15 +30,9 @@ double parse_double(const std::string& text) {
 }
 
 std::string fnv1a64_hex(const std::string& data) {
-  std::uint64_t h = 0xcbf29ce484222325ull;
-  for (unsigned char c : data) {
-    h ^= c;
-    h *= 0x100000001b3ull;
-  }
-  std::string hex(16, '0');
-  static const char kHex[] = "0123456789abcdef";
-  for (int i = 15; i >= 0; --i, h >>= 4) hex[i] = kHex[h & 0xF];
-  return hex;
+  pb::fnv1a64 f;
+  f.update(data.data(), data.size());
+  return f.hex();
 }
 
 // ----------------------------------------------------------------- tags
@@ -190,13 +184,13 @@ std::vector<double> gather_network_params(const std::vector<stage_model>& stages
 }
 
 std::string params_digest(const std::vector<stage_model>& stages) {
-  std::string text;
-  for (const stage_model& st : stages)
-    for (double v : st.current_params()) {
-      text += format_double(v);
-      text.push_back('\n');
-    }
-  return fnv1a64_hex(text);
+  // same text and hash as trainer.cpp:599-607, formatted on host threads
+  std::vector<pb::value_span> spans;
+  for (const stage_model& st : stages) {
+    const std::vector<double>& p = st.current_params();
+    spans.push_back({p.data(), static_cast<int64_t>(p.size())});
+  }
+  return pb::digest_spans(spans);
 }
 
 dataset make_synthetic_task(int samples, std::uint64_t seed) {

@@ -83,8 +83,13 @@ void check_config(const train_config& cfg, const dataset& data) {
     throw structural_error("dataset width does not match the network");
 }
 
+// A cached session is shared by every caller with the same config; `use`
+// serialises load_params .. read_params so concurrent same-shaped calls on
+// different threads cannot interleave on one device state (the reference's
+// train_epoch is re-entrant).
 struct SessionHandle {
   pb_session* s = nullptr;
+  std::mutex use;
   ~SessionHandle() {
     if (s) pb_session_destroy(s);
   }
@@ -180,6 +185,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
 
   int units = 1;
   std::shared_ptr<SessionHandle> h = session_for(cfg, mode, snaps, &units);
+  std::lock_guard<std::mutex> in_use(h->use);
 
   // Rebase: version 0 := the current weights (trainer.cpp:372-379).
   const std::vector<double> flat = gather_network_params(stages);
@@ -228,7 +234,8 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
     if (every_mini) {
       // digest after mini k's stage-1 commit: stage s holds its latest commit
       // strictly before that slot (trainer.cpp:492-501)
-      std::string text;
+      std::vector<std::vector<double>> vals;
+      std::vector<pb::value_span> spans;
       for (int s = 1; s <= W; ++s) {
         int v = k;
         if (grid && s > 1) {
@@ -236,12 +243,10 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
           for (const auto& c : ledger.commits)
             if (c.stage == s && c.slot < ledger.full_commit_slot[k]) v = std::max(v, c.version);
         }
-        for (double x : version_values(s, v)) {
-          text += format_double(x);
-          text.push_back('\n');
-        }
+        vals.push_back(version_values(s, v));
       }
-      m.checksum = fnv1a64_hex(text);
+      for (const auto& v : vals) spans.push_back({v.data(), static_cast<int64_t>(v.size())});
+      m.checksum = pb::digest_spans(spans);
     }
     log.minis.push_back(std::move(m));
   }
@@ -291,6 +296,7 @@ double network_loss(const network_spec& spec, const std::vector<double>& params,
   check_config(cfg, data);
   int units = 1;
   auto h = session_for(cfg, train_mode::sequential, false, &units);
+  std::lock_guard<std::mutex> in_use(h->use);
   ok(pb_session_load_params(h->s, params.data(), static_cast<int64_t>(params.size())));
   ok(pb_session_upload(h->s, data.x.data.data(), PB_DTYPE_F64, data.y.data.data(), PB_DTYPE_F64));
   double loss = 0.0;
@@ -314,6 +320,7 @@ std::vector<double> network_gradient(const network_spec& spec, const std::vector
   check_config(cfg, data);
   int units = 1;
   auto h = session_for(cfg, train_mode::sequential, false, &units);
+  std::lock_guard<std::mutex> in_use(h->use);
   ok(pb_session_load_params(h->s, params.data(), static_cast<int64_t>(params.size())));
   ok(pb_session_upload(h->s, data.x.data.data(), PB_DTYPE_F64, data.y.data.data(), PB_DTYPE_F64));
   ok(pb_session_run_epoch(h->s, nullptr));

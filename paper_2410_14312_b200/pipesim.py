@@ -656,6 +656,13 @@ class Session:
         N.check(_L().pb_session_snapshot(self._h, stage, version, _dp(out), len(out)))
         return out
 
+    def read_version(self, stage, version) -> np.ndarray:
+        """Committed weights of a version retained after the epoch (M and
+        M-1 without snapshots; any committed version with snapshots)."""
+        out = np.zeros(self.stage_sizes[stage - 1])
+        N.check(_L().pb_session_read_version(self._h, stage, version, _dp(out), len(out)))
+        return out
+
     @staticmethod
     def _dtype(a, labels=False):
         if labels:
@@ -886,6 +893,14 @@ def train_epoch(stages: List[StageModel], data: Dataset, cfg: TrainConfig, mode:
     if want == "automatic":
         want = "every_mini" if P <= b200.digest_auto_limit else "final_only"
     snaps = want == "every_mini" or observer is not None
+    if mode != "sequential" and not snaps:
+        # retained versions older than M-1 (1F1B stashes) are read from snapshots
+        sc0 = SimConfig(cfg.workers, cfg.micro_batches, cfg.mini_batches,
+                        samples_per_mini_batch=cfg.mini_batch_size)
+        g0 = _build(sc0, mode)
+        t0 = build_retention_timeline(assign_versions(g0, sc0), g0)
+        snaps = any(b > t0.horizon and v < cfg.mini_batches - 1
+                    for iv in t0.intervals for v, a, b in iv)
     sess = _session_for(cfg, mode, snaps)
     sess.load_params(gather_network_params(stages))
     sess.upload(data.x, data.y)
@@ -939,8 +954,10 @@ def train_epoch(stages: List[StageModel], data: Dataset, cfg: TrainConfig, mode:
         store = {M: cur}
         if timeline is not None:
             for v, a, b in timeline.intervals[s]:
-                if b > timeline.horizon and v != M and snaps:
-                    store[int(v)] = sess.snapshot(s + 1, int(v))
+                if b > timeline.horizon and v != M:
+                    # retained past the horizon (trainer.cpp:420-429): M-1 is
+                    # always readable, older 1F1B stashes need snapshots
+                    store[int(v)] = sess.read_version(s + 1, int(v))
         st.version_store = store
         st.current_version = M
 
@@ -971,8 +988,90 @@ def network_loss(spec: NetworkSpec, params, data: Dataset) -> float:
         s.close()
 
 
+# ================================================================ checkpoint
+def checkpoint_filename(stage_id: int, epoch: int) -> str:
+    """checkpoint_filename (checkpoint.hpp:44)."""
+    return f"stage-{stage_id}-epoch-{epoch}.ckpt"
+
+
+def checkpoint_stage(stage: StageModel, loss: str, epoch: int, path: str) -> None:
+    """checkpoint_stage (checkpoint.hpp:29-31): the reference's text format
+    (checkpoint.cpp:39-67), written by the native library."""
+    lay = np.ascontiguousarray([[l.in_, l.out, ACTIVATIONS.index(l.act)] for l in stage.layers],
+                               np.int32)
+    p = np.ascontiguousarray(stage.current_params(), np.float64)
+    N.check(_L().pb_checkpoint_stage(stage.stage_id, stage.first_layer, len(stage.layers),
+                                     _ip(lay), stage.current_version, _dp(p), len(p),
+                                     LOSSES.index(loss), epoch, os.fsencode(path)))
+
+
+@dataclass
+class RestoredStage:
+    """restored_stage (checkpoint.hpp:33-38)."""
+    stage: StageModel
+    loss: str
+    epoch: int
+
+
+def restore_stage(path: str, expected_stage: int = 0, expected_epoch: int = 0,
+                  max_layers: int = 4096, max_values: int = 0) -> RestoredStage:
+    """restore_stage (checkpoint.hpp:40-42): strict parse, digest check,
+    IntegrityError on a missing / truncated / tampered / mismatched file."""
+    if max_values <= 0:
+        max_values = max(1, os.path.getsize(path) // 2) if os.path.exists(path) else 1
+    info = N.pb_restored_stage()
+    lay = np.zeros((max_layers, 3), np.int32)
+    vals = np.zeros(max_values)
+    N.check(_L().pb_restore_stage(os.fsencode(path), expected_stage, expected_epoch,
+                                  C.byref(info), _ip(lay), max_layers, _dp(vals), len(vals)))
+    layers = [LayerSpec(int(a), int(b), ACTIVATIONS[int(c)]) for a, b, c in lay[:info.n_layers]]
+    st = StageModel(info.stage_id, info.first_layer, layers,
+                    {info.version: vals[:info.n_values].copy()}, info.version)
+    return RestoredStage(st, LOSSES[info.loss], info.epoch)
+
+
+@dataclass
+class TrainRunResult:
+    """train_run_result (trainer.hpp:175-183)."""
+    logs: List[EpochLog]
+    first_epoch: int
+    final_checksum: str
+
+
 def run_training(cfg: TrainConfig, mode: str, data: Dataset, checkpoint_dir: str = "",
-                 resume: bool = False):
-    """run_training (trainer.hpp:185-188) with per-stage checkpoints."""
-    from . import checkpoint as ck
-    return ck.run_training(cfg, mode, data, checkpoint_dir, resume)
+                 resume: bool = False) -> TrainRunResult:
+    """run_training (trainer.hpp:185-188; trainer.cpp:704-758): epochs of
+    train_epoch on B200, a checkpoint per stage after every epoch, and resume
+    from the newest epoch that has any stage file (a missing sibling stage
+    file is an IntegrityError)."""
+    _check_train_config(cfg, data)
+    stages = partition_model(cfg.net, cfg.workers)
+    load_network_params(stages, init_network_params(cfg.net, cfg.seed), 0)
+    first = 1
+    if resume and checkpoint_dir:
+        newest = 0
+        for e in range(cfg.epochs, 0, -1):
+            if any(os.path.exists(os.path.join(checkpoint_dir, checkpoint_filename(s, e)))
+                   for s in range(1, cfg.workers + 1)):
+                newest = e
+                break
+        if newest > 0:
+            for s in range(1, cfg.workers + 1):
+                path = os.path.join(checkpoint_dir, checkpoint_filename(s, newest))
+                if not os.path.exists(path):
+                    raise IntegrityError(f"resume refused: checkpoint for stage {s} epoch "
+                                         f"{newest} is missing", s, newest)
+                r = restore_stage(path, s, newest, max_values=stages[s - 1].param_count())
+                stages[s - 1].version_store = {0: r.stage.current_params()}
+                stages[s - 1].current_version = 0
+            first = newest + 1
+    logs = []
+    for e in range(first, cfg.epochs + 1):
+        logs.append(train_epoch(stages, data, cfg, mode, e))
+        if checkpoint_dir:
+            os.makedirs(checkpoint_dir, exist_ok=True)
+            for st in stages:
+                checkpoint_stage(st, cfg.net.loss, e,
+                                 os.path.join(checkpoint_dir,
+                                              checkpoint_filename(st.stage_id, e)))
+    return TrainRunResult(logs, first, params_digest(stages))

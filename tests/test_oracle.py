@@ -93,6 +93,14 @@ def test_train_goldens_restatement(name, mode):
     logged = [float(line.split(" loss ")[1].split()[0]) for line in log.splitlines()
               if " loss " in line]
     np.testing.assert_allclose(logged, np.array(losses).reshape(-1), rtol=1e-12)
+    # ... and its final checksum is the digest of the final parameters, in the
+    # reference's FNV-1a variant (offset basis 1469598103934665603, text.cpp:39-51)
+    final = log.splitlines()[-1]
+    assert final.startswith("epoch 2 final checksum ")
+    want = final.split()[-1]
+    assert O.params_digest(g[key + ".params"]) == want
+    from paper_2410_14312_b200 import pipesim as P
+    assert P.digest_values(g[key + ".params"]) == want
 
 
 def test_c1_summary_restatement():

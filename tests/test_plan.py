@@ -171,3 +171,14 @@ def test_digest_matches_to_chars_restatement():
     assert P.digest_values(vals) == O.params_digest(vals)
     for v in vals:
         assert P.format_double(float(v)) == O.format_double(float(v))
+
+
+def test_parallel_digest_matches_serial_restatement():
+    """Above 2^18 values the digest formats chunks on host threads and folds
+    them in order; the text and hash are those of the serial reference loop
+    (trainer.cpp:599-607), across chunk and ring boundaries."""
+    rng = np.random.default_rng(1)
+    n = (1 << 15) * 37 + 12345
+    vals = (rng.normal(size=n) * 10.0 ** rng.integers(-6, 6, n)).astype(np.float32)
+    vals = vals.astype(np.float64)
+    assert P.digest_values(vals) == O.params_digest(vals)
