@@ -357,6 +357,18 @@ struct options {
 };
 void set_options(const options& o);
 options get_options();
+
+// Host wall-clock breakdown of the calling thread's last train_epoch (ms):
+// plan (grid / ledger / retention), load (fp64 params -> device masters and
+// version 0), upload (the epoch's fp64 x / y), step (the epoch on the device,
+// launch to completion; device_ms = its CUDA-event time), readback (final
+// masters + retained versions -> fp64 version_store), digest (per-mini-batch
+// and final params_digest), total.
+struct epoch_timing {
+  double plan_ms = 0, load_ms = 0, upload_ms = 0, step_ms = 0, device_ms = 0,
+         readback_ms = 0, digest_ms = 0, total_ms = 0;
+};
+epoch_timing last_epoch_timing();
 }  // namespace b200
 
 }  // namespace pipesim

@@ -224,3 +224,12 @@ def restore_stage(path, expected_stage=0, expected_epoch=0, cap=1 << 24):
     _check(lib().ref_restore_stage(str(path).encode(), expected_stage, expected_epoch, _dp(out),
                                    cap, C.byref(n), C.byref(v), C.byref(e)))
     return out[:n.value].copy(), v.value, e.value
+
+
+def digest_seconds(values):
+    """(seconds, digest) of the reference's params_digest over `values`."""
+    v = np.ascontiguousarray(values, np.float64)
+    secs = C.c_double()
+    out = C.create_string_buffer(17)
+    _check(lib().ref_digest_seconds(_dp(v), C.c_int64(len(v)), C.byref(secs), out))
+    return secs.value, out.value.decode()

@@ -404,4 +404,22 @@ int ref_restore_stage(const char* path, int expected_stage, int expected_epoch, 
   }
 }
 
+// Seconds the reference's params_digest (trainer.cpp:599-607) takes over the
+// given values (one stage holding them): the per-mini-batch fixed cost of
+// replay_grid, reported beside the reference arm's throughput.
+int ref_digest_seconds(const double* values, int64_t n, double* seconds, char* out17) {
+  try {
+    std::vector<stage_model> st(1);
+    st[0].stage_id = 1;
+    st[0].version_store[0] = std::vector<double>(values, values + n);
+    const auto t0 = std::chrono::steady_clock::now();
+    const std::string d = params_digest(st);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    put_str(d, out17, 17);
+    return 0;
+  } catch (...) {
+    return fail();
+  }
+}
+
 }  // extern "C"

@@ -6,6 +6,7 @@
 // version_store holding exactly the retained versions, epoch_log layout,
 // exceptions) and reach the GPU only through the C ABI (pipesim_b200.h).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <filesystem>
@@ -35,9 +36,21 @@ options get_options() {
   std::lock_guard<std::mutex> lk(g_opt_mu);
   return g_opt;
 }
+namespace {
+thread_local epoch_timing g_timing;
+}
+epoch_timing last_epoch_timing() { return g_timing; }
 }  // namespace b200
 
 namespace {
+
+using clk = std::chrono::steady_clock;
+double ms_since(clk::time_point& t) {
+  const clk::time_point now = clk::now();
+  const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+  t = now;
+  return ms;
+}
 
 [[noreturn]] void rethrow_status(int st) {
   char msg[4096];
@@ -153,6 +166,9 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   if (static_cast<int>(stages.size()) != cfg.workers)
     throw structural_error("stage count does not match workers");
   const int W = cfg.workers, M = cfg.mini_batches;
+  b200::epoch_timing tm;
+  const clk::time_point t_start = clk::now();
+  clk::time_point tp = t_start;
 
   // Plan of this epoch (same as replay_grid's, trainer.cpp:401-404).
   std::unique_ptr<schedule_grid> grid;
@@ -171,6 +187,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
     timeline = build_retention_timeline(ledger, *grid);
   }
 
+  tm.plan_ms = ms_since(tp);
   const b200::options opt = b200::get_options();
   const long long P = cfg.net.param_count();
   bool every_mini = opt.digest == b200::digest_policy::every_mini ||
@@ -190,7 +207,11 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   // Rebase: version 0 := the current weights (trainer.cpp:372-379).
   const std::vector<double> flat = gather_network_params(stages);
   ok(pb_session_load_params(h->s, flat.data(), static_cast<int64_t>(flat.size())));
+  ok(pb_synchronize());
+  tm.load_ms = ms_since(tp);
   ok(pb_session_upload(h->s, data.x.data.data(), PB_DTYPE_F64, data.y.data.data(), PB_DTYPE_F64));
+  ok(pb_synchronize());
+  tm.upload_ms = ms_since(tp);
 
   std::vector<double> losses(M);
   std::vector<int> pinned(static_cast<size_t>(M) * units), consumed(M),
@@ -199,6 +220,8 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   pb_epoch_out out{losses.data(), pinned.data(), consumed.data(), dev_fwd.data(),
                    dev_bwd.data(), dev_cur.data(), 0.f};
   ok(pb_session_run_epoch(h->s, &out));
+  tm.step_ms = ms_since(tp);
+  tm.device_ms = out.device_ms;
 
   // The device-observed version trace must equal the ledger, bit for bit.
   for (int k = 0; k < M; ++k)
@@ -216,10 +239,12 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   }
   std::vector<double> final_flat(offs[W]);
   ok(pb_session_read_params(h->s, final_flat.data(), offs[W]));
+  tm.readback_ms += ms_since(tp);
 
   auto version_values = [&](int s1, int v) {
     std::vector<double> vals(sizes[s1 - 1]);
     ok(pb_session_read_version(h->s, s1, v, vals.data(), sizes[s1 - 1]));
+    tm.readback_ms += ms_since(tp);
     return vals;
   };
 
@@ -247,6 +272,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
       }
       for (const auto& v : vals) spans.push_back({v.data(), static_cast<int64_t>(v.size())});
       m.checksum = pb::digest_spans(spans);
+      tm.digest_ms += ms_since(tp);
     }
     log.minis.push_back(std::move(m));
   }
@@ -261,7 +287,9 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
           st.version_store[iv.version] = version_values(s + 1, iv.version);
     st.current_version = M;
   }
+  tm.readback_ms += ms_since(tp);
   log.final_checksum = params_digest(stages);
+  tm.digest_ms += ms_since(tp);
 
   if (observer && grid) {
     // verify mode: replay the retention timeline with the committed snapshots
@@ -280,6 +308,8 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
       observer(t, view);
     }
   }
+  tm.total_ms = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
+  b200::g_timing = tm;
   return log;
 }
 

@@ -27,7 +27,7 @@ def test_reference_arm_line(monkeypatch, capsys):
         def __init__(self, *a, **k):
             pass
 
-        def submit(self, fn):
+        def submit(self, fn, *a):
             return _Fut()
 
         def shutdown(self):
@@ -36,6 +36,8 @@ def test_reference_arm_line(monkeypatch, capsys):
     import concurrent.futures as cf
     monkeypatch.setattr(cf, "ProcessPoolExecutor", _Pool)
     monkeypatch.setattr(bench, "ref_parallel_runs", lambda: 3)
+    monkeypatch.setattr(os, "cpu_count", lambda: 8)
+    monkeypatch.setattr(bench, "_ref_digest_seconds", lambda: 0.5)
     monkeypatch.delenv("RANK", raising=False)
 
     class A:
@@ -50,6 +52,8 @@ def test_reference_arm_line(monkeypatch, capsys):
     assert line["impl"] == "reference"
     assert abs(line["value"] - 3 * samples / 2.0) < 1e-12  # aggregate of 3 runs
     assert line["cpu_baseline"]["cores"] == 3
+    assert line["steps"] == 1 and line["warmup"] == 0  # what each process actually ran
+    assert abs(line["cpu_baseline"]["digest_share"] - 0.25) < 1e-12
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
 
 

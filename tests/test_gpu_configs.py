@@ -101,7 +101,8 @@ def test_c3_structure_steady_state():
     assert np.array_equal(log.dev_fwd, np.repeat(pins[:, :, None], W, axis=2))
     assert np.array_equal(log.dev_bwd, np.repeat(np.arange(M)[:, None], W, axis=1))
     # steady state reached: update_source gap k - consumed = measured v = 1
-    assert all(k + 1 - c == 1 for k, c in enumerate(ref["consumed"][M // 2:]))
+    cons = ref["consumed"]
+    assert all(k + 1 - cons[k] == 1 for k in range(M // 2, M))
     losses = np.array([m.loss for m in log.minis])
     assert np.abs(losses - ref["losses"]).max() / np.abs(ref["losses"]).max() < 1e-4
     got = P.gather_network_params(stages)
