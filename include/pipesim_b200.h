@@ -294,6 +294,9 @@ int pb_session_destroy(pb_session* s);
 int pb_session_info_get(pb_session* s, pb_session_info* info);
 /* load_network_params(stages, flat, 0) — trainer.hpp:99-100 */
 int pb_session_load_params(pb_session* s, const double* flat, int64_t n);
+/* The same for one stage (1-based): its W then b per layer, n = the stage's
+ * parameter count (stage_model::current_params(), trainer.hpp:81-83). */
+int pb_session_load_stage_params(pb_session* s, int stage, const double* p, int64_t n);
 /* gather_network_params — trainer.hpp:102-103 (current versions, fp32 -> f64) */
 int pb_session_read_params(pb_session* s, double* flat, int64_t n);
 /* Host (pinned or pageable) -> HBM copy of an epoch's data: x [M*B][in],
@@ -377,6 +380,19 @@ int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg,
 int pb_plan_transfers(const pb_net_spec* net, const pb_train_config* cfg,
                       int rank, int world, int* n, int* kinds, int* dirs,
                       int* peers, int64_t* bytes, int cap);
+
+/* Device memory one rank's session holds per stage, without touching a GPU
+ * (the session's own arena layout): weight_bytes[s] = weight versions (the
+ * bf16 version pool + fp32 masters, split or whole), act_bytes[s] =
+ * activations kept for the backward (activation slots, scratch deltas,
+ * boundary buffers, logits); pool[s] / act_slots[s] = weight versions /
+ * mini-batch activation sets held at peak.  Stages other ranks own get 0.
+ * The per-stage figures behind the slot model's memory_footprint
+ * (proj/src/metrics.cpp:73-101: peak retained versions x params + peak
+ * stashed samples x width).  Arrays have W entries; any may be NULL. */
+int pb_plan_memory(const pb_net_spec* net, const pb_train_config* cfg, int rank,
+                   int world, int64_t* weight_bytes, int64_t* act_bytes, int* pool,
+                   int* act_slots);
 
 /* Synthetic classification data: x ~ U[0,1) from
  * mt19937_64(seed) row-major via (rng()>>11)*2^-53, then labels rng() % C.

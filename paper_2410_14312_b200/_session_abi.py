@@ -47,6 +47,7 @@ def signatures():
         "pb_session_destroy": (i, [p]),
         "pb_session_info_get": (i, [p, P(pb_session_info)]),
         "pb_session_load_params": (i, [p, P(C.c_double), i64]),
+        "pb_session_load_stage_params": (i, [p, i, P(C.c_double), i64]),
         "pb_session_read_params": (i, [p, P(C.c_double), i64]),
         "pb_session_upload": (i, [p, p, i, p, i]),
         "pb_session_run_epoch": (i, [p, P(pb_epoch_out)]),
@@ -63,6 +64,8 @@ def signatures():
                                        C.c_size_t, P(p)]),
         "pb_plan_transfers": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i), P(i), P(i),
                                   P(i), P(i64), i]),
+        "pb_plan_memory": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i64), P(i64), P(i),
+                               P(i)]),
         "pb_make_classification_task": (i, [i, i, i, u64, P(C.c_double), P(C.c_float),
                                             P(C.c_int)]),
     }

@@ -164,6 +164,27 @@ int pb_plan_transfers(const pb_net_spec* net, const pb_train_config* cfg, int ra
   PB_GUARD_END
 }
 
+int pb_plan_memory(const pb_net_spec* net, const pb_train_config* cfg, int rank, int world,
+                   int64_t* weight_bytes, int64_t* act_bytes, int* pool, int* act_slots) {
+  PB_GUARD_BEGIN
+  pb::SessionConfig c = make_config(net, cfg);
+  c.rank = rank;
+  c.world = world;
+  c.plan_only = true;
+  c.use_graph = false;
+  pb::Session sess(c);
+  const auto b = sess.stage_bytes();
+  const auto ps = sess.pool_sizes();
+  const auto as = sess.act_slot_counts();
+  for (size_t i = 0; i < b.size(); ++i) {
+    if (weight_bytes) weight_bytes[i] = b[i].first;
+    if (act_bytes) act_bytes[i] = b[i].second;
+    if (pool) pool[i] = ps[i];
+    if (act_slots) act_slots[i] = as[i];
+  }
+  PB_GUARD_END
+}
+
 int pb_session_destroy(pb_session* s) {
   PB_GUARD_BEGIN
   delete s;
@@ -203,6 +224,18 @@ int pb_session_load_params(pb_session* s, const double* flat, int64_t n) {
                                         ? "parameter vector shorter than the network"
                                         : "parameter vector longer than the network");
   x.load_params(flat);
+  PB_GUARD_END
+}
+
+int pb_session_load_stage_params(pb_session* s, int stage, const double* p, int64_t n) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  if (stage < 1 || stage > x.config().W) throw std::invalid_argument("stage out of range");
+  if (n != x.stage_param_count(stage))
+    throw pipesim::structural_error(n < x.stage_param_count(stage)
+                                        ? "parameter vector shorter than the stage"
+                                        : "parameter vector longer than the stage");
+  x.load_stage_params(stage, p);
   PB_GUARD_END
 }
 

@@ -1132,7 +1132,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   uint64_t* tfull_bar = empty_bar + S;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's are used)
   uint64_t* sgd_bar = tempty_bar + 2;    // [3 per epilogue warp] (TMA SGD epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 3 * Cfg::kEpiWarps);
+  // (own 16-byte slot, apart from the barriers thread 0 initialises)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::kBarOff + 448);
+  static_assert(sizeof(uint64_t) * (2 * Cfg::kStages + 4 + 3 * Cfg::kEpiWarps) <= 448,
+                "barrier region overlaps the TMEM address slot");
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -1168,6 +1171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       }
     ptx::fence_mbar_init();
   }
+  __syncthreads();  // barrier init (thread 0) before the pair's TMEM allocation
   if (warp == 1) ptx::tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   ptx::cluster_sync();

@@ -862,8 +862,22 @@ void launch_f32_to_bf16_rows(cudaStream_t st, const float* src, int rows,
   launch_convert_f32_bf16(st, src, rows, cols, ld_src, dst, ld_dst);
 }
 
+__global__ void f32_f64_kernel(const float* __restrict__ src, double* __restrict__ dst,
+                               size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<double>(src[i]);
+}
+
+void launch_convert_f32_f64(cudaStream_t st, const float* src, double* dst, size_t n) {
+  if (n == 0) return;
+  f32_f64_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
+  PB_CUDA(cudaGetLastError());
+}
+
 void launch_convert_f64_f32(cudaStream_t st, const double* src, float* dst,
                             size_t n) {
+  if (n == 0) return;
   f64_f32_kernel<<<grid_for(n), 256, 0, st>>>(src, dst, n);
   PB_CUDA(cudaGetLastError());
 }

@@ -111,6 +111,7 @@ void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
                              int ld_dst);
 void launch_convert_f64_f32(cudaStream_t st, const double* src, float* dst,
                             size_t n);
+void launch_convert_f32_f64(cudaStream_t st, const float* src, double* dst, size_t n);
 void launch_f32_to_bf16_rows(cudaStream_t st, const float* src, int rows,
                              int cols, int ld_src, __nv_bfloat16* dst,
                              int ld_dst);

@@ -1,5 +1,6 @@
 // Session implementation — see session.hpp for the design summary.
 #include "session.hpp"
+#include "host_xfer.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -94,6 +95,9 @@ struct Session::Impl {
     cudaStream_t bstream = nullptr;  // backwards (split mode; forwards keep `stream`)
     cudaStream_t biasstream = nullptr;  // bias gradient + SGD of a backward
     int64_t param_offset = 0, param_count = 0;
+    // device bytes held for this stage: weight versions (pool + masters) and
+    // activations (slots, scratch deltas, boundary buffers, logits)
+    int64_t bytes_weights = 0, bytes_acts = 0;
   };
 
   struct Task {
@@ -214,6 +218,22 @@ struct Session::Impl {
   cudaGraphExec_t sexec = nullptr;
   HostInput sgraph_key;  // host buffers the streamed graph was captured with
   std::vector<double> kt_flops;    // [timed launches] 2*M*N*K
+  // parameter transfers at the boundary (load / read of fp64 masters):
+  // pinned double-buffered staging and per-layer device scratch
+  std::unique_ptr<HostStager> stager;
+  double* p64 = nullptr;  // one layer's W then b, fp64
+  float* p32 = nullptr;   // one layer's W, fp32
+  size_t p_cap = 0;       // elements of p64 / p32
+  void param_scratch() {
+    if (p64) return;
+    size_t mx = 0;
+    for (auto& st : stages)
+      for (auto& d : st.layers) mx = std::max(mx, static_cast<size_t>(d.in) * d.out + d.out);
+    PB_CUDA(cudaMalloc(&p64, mx * 8));
+    PB_CUDA(cudaMalloc(&p32, mx * 4));
+    p_cap = mx;
+    stager = std::make_unique<HostStager>();
+  }
   std::unique_ptr<P2P> p2p;
   // IPC peer-memory transport (SessionConfig::transport == 1)
   std::unique_ptr<IpcLink> ipc;
@@ -274,6 +294,9 @@ struct Session::Impl {
       for (float* p : v)
         if (p) cudaFreeHost(p);
     if (arena && !plan_only) cudaFree(arena);
+    stager.reset();
+    if (p64) cudaFree(p64);
+    if (p32) cudaFree(p32);
   }
 
   bool plan_only = false;
@@ -479,6 +502,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   for (int s = 0; s < W; ++s) {
     Impl::Stage& st = I.stages[s];
     st.param_offset = off;
+    size_t wb = 0, ab = 0;
     for (int l = 0; l < st.L; ++l) {
       const int gl = st.first_layer + l;
       Impl::LayerDev d;
@@ -490,20 +514,23 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       st.layers.push_back(d);
       st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
       if (!I.local(s)) continue;
-      need += 2 * ((I.split ? bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2)
-                            : bytes_of(static_cast<size_t>(d.in) * d.out, 4)) +
-                   bytes_of(d.out, 4));
-      need += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2 * I.sc) + bytes_of(d.out, 4));
-      need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
-      if (l + 1 < st.L) need += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
+      wb += 2 * ((I.split ? bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2)
+                          : bytes_of(static_cast<size_t>(d.in) * d.out, 4)) +
+                 bytes_of(d.out, 4));
+      wb += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2 * I.sc) + bytes_of(d.out, 4));
+      ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
+      if (l + 1 < st.L) ab += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
     }
     off += st.param_count;
     if (!I.local(s)) continue;
     if (s > 0 && !I.local(s - 1))  // boundary buffers: received input + outgoing delta
-      need += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2 * I.sc);
-    need += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
-    need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2 * I.sc);
-    if (s == W - 1) need += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
+      ab += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2 * I.sc);
+    wb += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
+    ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2 * I.sc);
+    if (s == W - 1) ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
+    st.bytes_weights = static_cast<int64_t>(wb);
+    st.bytes_acts = static_cast<int64_t>(ab);
+    need += wb + ab;
   }
   const size_t rows = static_cast<size_t>(M) * c.B;
   need += bytes_of(rows * I.ld_x, 2 * I.sc) + bytes_of(rows * I.n_out, 4) + bytes_of(rows, 4) +
@@ -1215,6 +1242,12 @@ std::vector<int> Session::pool_sizes() const {
   return v;
 }
 
+std::vector<std::pair<int64_t, int64_t>> Session::stage_bytes() const {
+  std::vector<std::pair<int64_t, int64_t>> v;
+  for (const auto& s : impl_->stages) v.push_back({s.bytes_weights, s.bytes_acts});
+  return v;
+}
+
 std::vector<int> Session::act_slot_counts() const {
   std::vector<int> v;
   for (const auto& s : impl_->stages) v.push_back(static_cast<int>(s.acts.size()));
@@ -1228,39 +1261,40 @@ const float* Session::snapshot(int s, int version) const {
 
 // ------------------------------------------------------------------ params
 void Session::load_params(const double* flat) {
+  for (auto& st : impl_->stages)
+    if (impl_->local(st.id - 1)) load_stage_params(st.id, flat + st.param_offset);
+}
+
+// Version 0 of one stage := p (fp64, per layer W then b).  The fp64 values
+// cross PCIe once (pinned, double-buffered, host copies split over threads);
+// rounding to fp32 and the split into hi / lo (or the fp32 master and its
+// bf16 copy) run on the device.
+void Session::load_stage_params(int stage, const double* p) {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
-  std::vector<float> host;
-  for (auto& st : I.stages) {
-    if (!I.local(st.id - 1)) continue;
-    const int c0 = st.version_colour[0];
-    size_t po = static_cast<size_t>(st.param_offset);
-    for (int l = 0; l < st.L; ++l) {
-      auto& d = st.layers[l];
-      const size_t nw = static_cast<size_t>(d.in) * d.out;
-      host.assign(flat + po, flat + po + nw + d.out);
-      // every copy is ordered on the origin stream: a synchronous cudaMemcpy
-      // from pageable memory may return before its DMA lands, and the
-      // non-blocking origin stream's kernels below read the destination
-      PB_CUDA(cudaMemcpyAsync(d.b32[0], host.data() + nw, d.out * 4, cudaMemcpyHostToDevice,
-                              I.origin));
-      PB_CUDA(cudaMemcpyAsync(st.pool[c0].b32[l], host.data() + nw, d.out * 4,
-                              cudaMemcpyHostToDevice, I.origin));
-      PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
-      if (I.split) {  // version 0 = hi in pool colour(0) + lo[0] (lo[1] kept equal)
-        float* tmp = nullptr;
-        PB_CUDA(cudaMalloc(&tmp, nw * 4));
-        PB_CUDA(cudaMemcpyAsync(tmp, host.data(), nw * 4, cudaMemcpyHostToDevice, I.origin));
-        launch_split_master(I.origin, tmp, d.out, d.in, d.in, st.pool[c0].w16[l], d.lo[0],
-                            d.ld_in);
-        PB_CUDA(cudaMemcpyAsync(d.lo[1], d.lo[0], sizeof(uint16_t) * d.out * d.ld_in,
-                                cudaMemcpyDeviceToDevice, I.origin));
-        PB_CUDA(cudaStreamSynchronize(I.origin));
-        PB_CUDA(cudaFree(tmp));
-        po += nw + d.out;
-        continue;
-      }
-      PB_CUDA(cudaMemcpyAsync(d.w32[0], host.data(), nw * 4, cudaMemcpyHostToDevice, I.origin));
+  Impl::Stage& st = I.stages.at(stage - 1);
+  if (!I.local(stage - 1)) throw std::invalid_argument("stage is not held by this process");
+  I.param_scratch();
+  const int c0 = st.version_colour[0];
+  size_t po = 0;
+  for (int l = 0; l < st.L; ++l) {
+    auto& d = st.layers[l];
+    const size_t nw = static_cast<size_t>(d.in) * d.out;
+    // every step is ordered on the origin stream (its kernels read the
+    // destination)
+    I.stager->h2d(I.p64, p + po, (nw + d.out) * 8, I.origin);
+    launch_convert_f64_f32(I.origin, I.p64 + nw, d.b32[0], d.out);
+    PB_CUDA(cudaMemcpyAsync(st.pool[c0].b32[l], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice,
+                            I.origin));
+    PB_CUDA(cudaMemcpyAsync(d.b32[1], d.b32[0], d.out * 4, cudaMemcpyDeviceToDevice, I.origin));
+    if (I.split) {  // version 0 = hi in pool colour(0) + lo[0] (lo[1] kept equal)
+      launch_convert_f64_f32(I.origin, I.p64, I.p32, nw);
+      launch_split_master(I.origin, I.p32, d.out, d.in, d.in, st.pool[c0].w16[l], d.lo[0],
+                          d.ld_in);
+      PB_CUDA(cudaMemcpyAsync(d.lo[1], d.lo[0], sizeof(uint16_t) * d.out * d.ld_in,
+                              cudaMemcpyDeviceToDevice, I.origin));
+    } else {
+      launch_convert_f64_f32(I.origin, I.p64, d.w32[0], nw);
       if (I.v32)
         launch_rows_to_f32(I.origin, d.w32[0], false, d.out, d.in, d.in,
                            reinterpret_cast<float*>(st.pool[c0].w16[l]), d.ld_in);
@@ -1269,60 +1303,48 @@ void Session::load_params(const double* flat) {
                                 d.ld_in);
       // keep the odd master in sync so an M-odd rebase copy is always valid
       PB_CUDA(cudaMemcpyAsync(d.w32[1], d.w32[0], nw * 4, cudaMemcpyDeviceToDevice, I.origin));
-      po += nw + d.out;
     }
-    // the rebase copies pool[colour(M)] -> pool[colour(0)]: make it a no-op
-    const int cM = st.version_colour[cfg_.M];
-    if (cM != c0)
-      for (int l = 0; l < st.L; ++l) {
-        auto& d = st.layers[l];
-        PB_CUDA(cudaMemcpyAsync(st.pool[cM].w16[l], st.pool[c0].w16[l],
-                                sizeof(__nv_bfloat16) * I.sc * d.out * static_cast<size_t>(d.ld_in),
-                                cudaMemcpyDeviceToDevice, I.origin));
-        PB_CUDA(cudaMemcpyAsync(st.pool[cM].b32[l], st.pool[c0].b32[l], 4 * d.out,
-                                cudaMemcpyDeviceToDevice, I.origin));
-      }
+    po += nw + d.out;
   }
-  PB_CUDA(cudaStreamSynchronize(I.origin));
-  if (!I.snaps.empty())
-    for (auto& st : I.stages) {
-      const int s = st.id - 1;
-      if (!I.local(s)) continue;
-      std::vector<float> h(flat + st.param_offset, flat + st.param_offset + st.param_count);
-      std::copy(h.begin(), h.end(), I.snaps[s][0]);
+  // the rebase copies pool[colour(M)] -> pool[colour(0)]: make it a no-op
+  const int cM = st.version_colour[cfg_.M];
+  if (cM != c0)
+    for (int l = 0; l < st.L; ++l) {
+      auto& d = st.layers[l];
+      PB_CUDA(cudaMemcpyAsync(st.pool[cM].w16[l], st.pool[c0].w16[l],
+                              sizeof(__nv_bfloat16) * I.sc * d.out * static_cast<size_t>(d.ld_in),
+                              cudaMemcpyDeviceToDevice, I.origin));
+      PB_CUDA(cudaMemcpyAsync(st.pool[cM].b32[l], st.pool[c0].b32[l], 4 * d.out,
+                              cudaMemcpyDeviceToDevice, I.origin));
     }
+  PB_CUDA(cudaStreamSynchronize(I.origin));
+  if (!I.snaps.empty()) {
+    float* dst = I.snaps[stage - 1][0];
+    for (int64_t i = 0; i < st.param_count; ++i) dst[i] = static_cast<float>(p[i]);
+  }
 }
 
 namespace {
 // fp32 master of `version` of one stage's layers -> out (flat, W then b per
-// layer, widened to fp64); split masters are joined on the device first
+// layer, widened to fp64 on the device); split masters are joined first
 void read_master(Session::Impl& I, Session::Impl::Stage& st, int version, double* out) {
   const int p = version & 1;
-  std::vector<float> host;
-  float* tmp = nullptr;
+  I.param_scratch();
   size_t po = 0;
   for (size_t l = 0; l < st.layers.size(); ++l) {
     auto& d = st.layers[l];
     const size_t nw = static_cast<size_t>(d.in) * d.out;
-    host.resize(nw + d.out);
+    const float* w = d.w32[p];
     if (I.split) {
-      if (!tmp) {
-        size_t mx = 0;
-        for (auto& e : st.layers) mx = std::max(mx, static_cast<size_t>(e.in) * e.out);
-        PB_CUDA(cudaMalloc(&tmp, mx * 4));
-      }
       launch_join_master(I.origin, st.pool[st.version_colour[version]].w16[l], d.lo[p], d.out,
-                         d.in, d.ld_in, tmp, d.in);
-      PB_CUDA(cudaStreamSynchronize(I.origin));
-      PB_CUDA(cudaMemcpy(host.data(), tmp, nw * 4, cudaMemcpyDeviceToHost));
-    } else {
-      PB_CUDA(cudaMemcpy(host.data(), d.w32[p], nw * 4, cudaMemcpyDeviceToHost));
+                         d.in, d.ld_in, I.p32, d.in);
+      w = I.p32;
     }
-    PB_CUDA(cudaMemcpy(host.data() + nw, d.b32[p], d.out * 4, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < host.size(); ++i) out[po + i] = host[i];
+    launch_convert_f32_f64(I.origin, w, I.p64, nw);
+    launch_convert_f32_f64(I.origin, d.b32[p], I.p64 + nw, d.out);
+    I.stager->d2h(out + po, I.p64, (nw + d.out) * 8, I.origin);
     po += nw + d.out;
   }
-  if (tmp) PB_CUDA(cudaFree(tmp));
 }
 }  // namespace
 

@@ -128,6 +128,8 @@ class Session {
 
   // Installs a flat whole-network parameter vector as version 0.
   void load_params(const double* flat);
+  // version 0 of one stage (1-based) := p, W then b per layer (fp64)
+  void load_stage_params(int stage, const double* p);
   // Copies the current version's fp32 masters out as doubles (flat layout).
   void read_params(double* flat);
   // fp32 snapshot of `version` of stage s (requires snapshots=true).
@@ -159,6 +161,8 @@ class Session {
   int horizon() const { return horizon_; }
   std::vector<int> pool_sizes() const;
   std::vector<int> act_slot_counts() const;
+  // per stage: {weight-version bytes, activation bytes} this process allocated
+  std::vector<std::pair<int64_t, int64_t>> stage_bytes() const;
   int64_t device_bytes() const { return arena_bytes_; }
   int kernels_per_epoch() const { return kernels_per_epoch_; }
   // Schedule document (export.cpp schema) of the last epoch with the version

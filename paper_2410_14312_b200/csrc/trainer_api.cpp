@@ -204,9 +204,12 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   std::shared_ptr<SessionHandle> h = session_for(cfg, mode, snaps, &units);
   std::lock_guard<std::mutex> in_use(h->use);
 
-  // Rebase: version 0 := the current weights (trainer.cpp:372-379).
-  const std::vector<double> flat = gather_network_params(stages);
-  ok(pb_session_load_params(h->s, flat.data(), static_cast<int64_t>(flat.size())));
+  // Rebase: version 0 := the current weights (trainer.cpp:372-379), stage by
+  // stage straight from the caller's vectors (no gathered copy).
+  for (int s = 0; s < W; ++s) {
+    const std::vector<double>& cur = stages[s].current_params();
+    ok(pb_session_load_stage_params(h->s, s + 1, cur.data(), static_cast<int64_t>(cur.size())));
+  }
   ok(pb_synchronize());
   tm.load_ms = ms_since(tp);
   ok(pb_session_upload(h->s, data.x.data.data(), PB_DTYPE_F64, data.y.data.data(), PB_DTYPE_F64));
@@ -232,13 +235,18 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   for (int s = 0; s < W; ++s)
     if (dev_cur[s] != M) throw structural_error("device current version diverged from the ledger");
 
-  std::vector<int64_t> sizes(W), offs(W + 1, 0);
+  std::vector<int64_t> sizes(W);
+  for (int s = 0; s < W; ++s) sizes[s] = stages[s].param_count();
+  // Final weights (version M) straight into each stage's version store.  The
+  // caller's current vector is reused as the buffer (same size, pages already
+  // mapped), so repeated epochs do not fault 2 GB of fresh pages per call.
+  std::vector<std::vector<double>> final_vals(W);
   for (int s = 0; s < W; ++s) {
-    sizes[s] = stages[s].param_count();
-    offs[s + 1] = offs[s] + sizes[s];
+    auto it = stages[s].version_store.find(stages[s].current_version);
+    if (it != stages[s].version_store.end()) final_vals[s] = std::move(it->second);
+    final_vals[s].resize(static_cast<size_t>(sizes[s]));
+    ok(pb_session_read_version(h->s, s + 1, M, final_vals[s].data(), sizes[s]));
   }
-  std::vector<double> final_flat(offs[W]);
-  ok(pb_session_read_params(h->s, final_flat.data(), offs[W]));
   tm.readback_ms += ms_since(tp);
 
   auto version_values = [&](int s1, int v) {
@@ -280,7 +288,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   for (int s = 0; s < W; ++s) {
     stage_model& st = stages[s];
     st.version_store.clear();
-    st.version_store[M].assign(final_flat.begin() + offs[s], final_flat.begin() + offs[s + 1]);
+    st.version_store[M] = std::move(final_vals[s]);
     if (grid)
       for (const auto& iv : timeline.per_stage[s])
         if (iv.freed_at_slot > timeline.horizon && iv.version != M)

@@ -825,6 +825,29 @@ def plan_transfers(net: NetworkSpec, workers, micro_batches, mini_batch_size, mi
     return [("send" if k[i] else "recv", int(d[i]), int(p[i]), int(b[i])) for i in range(n.value)]
 
 
+def plan_memory(net: NetworkSpec, workers, micro_batches, mini_batch_size, mini_batches,
+                mode="timeprest", rank=0, world=1, precision="bf16"):
+    """Device bytes the session holds per stage, from its own arena layout
+    (host only, no GPU): dict of numpy arrays `weight_bytes`, `act_bytes`,
+    `pool` (weight versions held at peak), `act_slots` (mini-batch
+    activation sets held at peak).  The measured counterpart of the slot
+    model's memory_footprint (proj/src/metrics.cpp:73-101)."""
+    cfg = pb_train_config(workers, micro_batches, mini_batch_size, mini_batches, 0.05,
+                          TRAIN_MODES.index(mode), 0, 0, 0)
+    cfg.precision = 1 if precision == "fp32" else 0
+    spec = net._c()
+    W = int(workers)
+    wb = np.zeros(W, np.int64)
+    ab = np.zeros(W, np.int64)
+    pool = np.zeros(W, np.int32)
+    acts = np.zeros(W, np.int32)
+    i64p = C.POINTER(C.c_int64)
+    N.check(_L().pb_plan_memory(C.byref(spec), C.byref(cfg), rank, world,
+                                wb.ctypes.data_as(i64p), ab.ctypes.data_as(i64p), _ip(pool),
+                                _ip(acts)))
+    return {"weight_bytes": wb, "act_bytes": ab, "pool": pool, "act_slots": acts}
+
+
 _SESSIONS: Dict[tuple, Session] = {}
 
 

@@ -91,3 +91,29 @@ def test_gloo_two_process_exchange():
         p.join(180)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) == "ok"
+
+
+@pytest.mark.parametrize("mode", ["timeprest", "pipedream"])
+@pytest.mark.parametrize("W,N", [(2, 4), (4, 2), (8, 8)])
+def test_plan_memory_matches_slot_model(mode, W, N):
+    """The session's weight-version pool per stage is exactly the slot
+    model's peak retained versions (metrics.cpp:73-75 /
+    build_retention_timeline), and TiMePReSt never holds more bytes than
+    PipeDream (the paper's memory claim)."""
+    widths = [64] * (W + 1)
+    net = P.NetworkSpec(widths, ["relu"] * (W - 1) + ["linear"], "softmax_cross_entropy")
+    M = 2 * (W + N)
+    cfg = P.SimConfig(workers=W, micro_batches=N, mini_batches=M, samples_per_mini_batch=8 * N)
+    grid = P.build_nf1b_schedule(cfg) if mode == "timeprest" else P.build_1f1b_schedule(cfg)
+    tl = P.build_retention_timeline(P.assign_versions(grid, cfg), grid)
+    mem = P.plan_memory(net, W, N, 8 * N, M, mode=mode)
+    assert mem["pool"].tolist() == list(tl.peak_concurrent)
+    assert (mem["weight_bytes"] > 0).all() and (mem["act_bytes"] > 0).all()
+    if mode == "pipedream":
+        t = P.plan_memory(net, W, N, 8 * N, M, mode="timeprest")
+        assert (t["weight_bytes"] <= mem["weight_bytes"]).all()
+        assert (t["weight_bytes"] + t["act_bytes"] <= mem["weight_bytes"] + mem["act_bytes"]).all()
+    # split across ranks: each rank accounts only for its own stages
+    half = P.plan_memory(net, W, N, 8 * N, M, mode=mode, rank=0, world=2)
+    assert (half["weight_bytes"][W // 2:] == 0).all()
+    assert (half["weight_bytes"][:W // 2] == mem["weight_bytes"][:W // 2]).all()
