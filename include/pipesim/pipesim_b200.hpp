@@ -351,8 +351,11 @@ enum class digest_policy { automatic, every_mini, final_only };
 struct options {
   int device = 0;
   bool use_graph = true;                 // capture the epoch as a CUDA graph
+  // mini_log::checksum of every mini-batch (trainer.cpp:492-501) is computed
+  // on the device inside the epoch (digest_dev.hpp); automatic = every
+  // mini-batch for networks up to digest_auto_limit params, final only above
   digest_policy digest = digest_policy::automatic;
-  long long digest_auto_limit = 4000000; // params; above: final_only
+  long long digest_auto_limit = 1LL << 40;
   bool verify_fp32 = false;              // fp32 FFMA verify precision (no bf16 rounding)
 };
 void set_options(const options& o);
@@ -362,8 +365,8 @@ options get_options();
 // plan (grid / ledger / retention), load (fp64 params -> device masters and
 // version 0), upload (the epoch's fp64 x / y), step (the epoch on the device,
 // launch to completion; device_ms = its CUDA-event time), readback (final
-// masters + retained versions -> fp64 version_store), digest (per-mini-batch
-// and final params_digest), total.
+// masters + retained versions -> fp64 version_store), digest (fetching the
+// device digests; the per-mini-batch ones run inside the epoch, in step), total.
 struct epoch_timing {
   double plan_ms = 0, load_ms = 0, upload_ms = 0, step_ms = 0, device_ms = 0,
          readback_ms = 0, digest_ms = 0, total_ms = 0;

@@ -147,6 +147,16 @@ int pb_make_synthetic_task(int samples, uint64_t seed, double* x, double* y);
 /* FNV-1a over shortest round-trip decimals ("%.17g"-free, std::to_chars) of
  * values[0..n) each followed by '\n'; out receives 16 hex chars + NUL. */
 int pb_params_digest(const double* values, int64_t n, char* out17);
+/* The same digest computed on the current CUDA device (digest_dev.hpp:
+ * device shortest-decimal formatting + parallel FNV-1a fold), for values
+ * given as fp32 (host memory; each is formatted as the double it widens to,
+ * as the reference's fp64 params that hold these values would be).
+ * ms (optional) = device time of the digest kernels. */
+int pb_device_digest_f32(const float* values, int64_t n, char* out17, float* ms);
+/* Device shortest round-trip formatting (shortest.cuh) of fp32 values as
+ * doubles, for tests against std::to_chars: out[i*32 ..] holds the text of
+ * values[i] (NUL-padded). */
+int pb_device_format_f32(const float* values, int64_t n, char* out);
 
 /* checkpoint_stage / restore_stage (checkpoint.hpp:29-44; file format of
  * checkpoint.cpp:39-153).  A stage is its id, first layer, n_layers
@@ -258,6 +268,9 @@ typedef struct {
   int transport;        /* multi-process split: PB_TRANSPORT_* */
   int precision;        /* PB_PRECISION_*: bf16 tensor cores (fp32 accumulate,
                            fp32 masters) or the fp32 FFMA verify mode */
+  int digests;          /* params_digest on the device inside the epoch: after
+                           every mini-batch's stage-1 commit and at the end
+                           (trainer.cpp:492-501, :506); pb_session_digests */
 } pb_train_config;      /* train_config, trainer.hpp:117-126 */
 
 enum { PB_PRECISION_BF16 = 0, PB_PRECISION_FP32_VERIFY = 1 };
@@ -393,6 +406,15 @@ int pb_plan_transfers(const pb_net_spec* net, const pb_train_config* cfg,
 int pb_plan_memory(const pb_net_spec* net, const pb_train_config* cfg, int rank,
                    int world, int64_t* weight_bytes, int64_t* act_bytes, int* pool,
                    int* act_slots);
+
+/* The M + 1 digests of the last epoch of a session created with digests = 1:
+ * hex[17*i ..] = 16 hex chars + NUL of mini-batch i+1's checksum
+ * (mini_log::checksum), the last one the epoch's final checksum.  cap = the
+ * number of 17-byte entries hex holds. */
+int pb_session_digests(pb_session* s, char* hex, int64_t cap);
+/* params_digest (trainer.cpp:599-607) of every stage's `version` (0 after
+ * load, M after an epoch), computed on the device; out17 = 16 hex + NUL. */
+int pb_session_params_digest(pb_session* s, int version, char* out17);
 
 /* Synthetic classification data: x ~ U[0,1) from
  * mt19937_64(seed) row-major via (rng()>>11)*2^-53, then labels rng() % C.

@@ -11,7 +11,8 @@ class pb_train_config(C.Structure):
                 ("learning_rate", C.c_double), ("mode", C.c_int), ("device", C.c_int),
                 ("use_graph", C.c_int), ("snapshots", C.c_int),
                 ("fwd_merge", C.c_int), ("timed_kernel", C.c_int),
-                ("transport", C.c_int), ("precision", C.c_int)]
+                ("transport", C.c_int), ("precision", C.c_int),
+                ("digests", C.c_int)]
 
 
 class pb_epoch_out(C.Structure):
@@ -64,6 +65,10 @@ def signatures():
                                        C.c_size_t, P(p)]),
         "pb_plan_transfers": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i), P(i), P(i),
                                   P(i), P(i64), i]),
+        "pb_device_digest_f32": (i, [P(C.c_float), i64, C.c_char_p, P(C.c_float)]),
+        "pb_device_format_f32": (i, [P(C.c_float), i64, C.c_char_p]),
+        "pb_session_digests": (i, [p, C.c_char_p, i64]),
+        "pb_session_params_digest": (i, [p, i, C.c_char_p]),
         "pb_plan_memory": (i, [P(pb_net_spec), P(pb_train_config), i, i, P(i64), P(i64), P(i),
                                P(i)]),
         "pb_make_classification_task": (i, [i, i, i, u64, P(C.c_double), P(C.c_float),

@@ -86,6 +86,7 @@ pb::SessionConfig make_config(const pb_net_spec* net, const pb_train_config* cfg
   c.timed_kernel = cfg->timed_kernel;
   c.transport = cfg->transport;
   c.verify_fp32 = cfg->precision == 1;
+  c.digests = cfg->digests != 0;
   if (const char* e = std::getenv("PIPESIM_FWD_MERGE")) c.fwd_merge = std::atoi(e);
   if (const char* e = std::getenv("PIPESIM_SIDE")) c.side_streams = std::atoi(e) != 0;
   return c;
@@ -182,6 +183,30 @@ int pb_plan_memory(const pb_net_spec* net, const pb_train_config* cfg, int rank,
     if (pool) pool[i] = ps[i];
     if (act_slots) act_slots[i] = as[i];
   }
+  PB_GUARD_END
+}
+
+namespace {
+void hex16(uint64_t h, char* out) {
+  static const char kHex[] = "0123456789abcdef";
+  for (int i = 15; i >= 0; --i, h >>= 4) out[i] = kHex[h & 15];
+  out[16] = 0;
+}
+}  // namespace
+
+int pb_session_digests(pb_session* s, char* hex, int64_t cap) {
+  PB_GUARD_BEGIN
+  pb::Session& x = S(s);
+  const auto& d = x.last_result().digests;
+  if (d.empty()) throw std::logic_error("no digests: create the session with digests = 1 and run an epoch");
+  if (cap < static_cast<int64_t>(d.size())) throw pb::capacity_error("digest buffer too small");
+  for (size_t i = 0; i < d.size(); ++i) hex16(d[i], hex + 17 * i);
+  PB_GUARD_END
+}
+
+int pb_session_params_digest(pb_session* s, int version, char* out17) {
+  PB_GUARD_BEGIN
+  hex16(S(s).params_digest(version), out17);
   PB_GUARD_END
 }
 

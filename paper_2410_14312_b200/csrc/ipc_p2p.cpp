@@ -153,28 +153,38 @@ void IpcLink::connect(const std::vector<std::vector<uint8_t>>& blobs) {
   connected_ = true;
 }
 
-void IpcLink::send(int idx, cudaStream_t st, uint32_t e) {
+// Binary flags, reset by the side that waits on them right after its wait:
+// the value waited for is always 1, so the enqueued operations are identical
+// every epoch and the epoch can be a CUDA graph replayed as is.  A flag's next
+// set cannot overtake its reset: the receiver posts message i of the next
+// epoch only after (its stream order) waiting for done[i] of this one, which
+// the sender writes after resetting posted[i]; the sender signals done[i] of
+// the next epoch only after that post, which the receiver issues after
+// resetting done[i].  (Writes carry the default system-scope memory barrier.)
+void IpcLink::send(int idx, cudaStream_t st) {
   if (!connected_) throw std::logic_error("IPC transport is not connected");
   const StreamMemOps& ops = memops();
   const CUstream cs = reinterpret_cast<CUstream>(st);
-  cu_check(ops.wait(cs, reinterpret_cast<CUdeviceptr>(flags_ + idx), e, CU_STREAM_WAIT_VALUE_GEQ),
-           "cuStreamWaitValue32 (posted)");
+  const CUdeviceptr own = reinterpret_cast<CUdeviceptr>(flags_ + idx);
+  cu_check(ops.wait(cs, own, 1, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32 (posted)");
+  cu_check(ops.write(cs, own, 0, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32 (reset)");
   PB_CUDA(cudaMemcpyAsync(remote_dst_[idx], msgs_[idx].src, msgs_[idx].bytes,
                           cudaMemcpyDeviceToDevice, st));
-  cu_check(ops.write(cs, reinterpret_cast<CUdeviceptr>(remote_flag_[idx]), e,
+  cu_check(ops.write(cs, reinterpret_cast<CUdeviceptr>(remote_flag_[idx]), 1,
                      CU_STREAM_WRITE_VALUE_DEFAULT),
            "cuStreamWriteValue32 (done)");
 }
 
-void IpcLink::recv(int idx, cudaStream_t st, uint32_t e) {
+void IpcLink::recv(int idx, cudaStream_t st) {
   if (!connected_) throw std::logic_error("IPC transport is not connected");
   const StreamMemOps& ops = memops();
   const CUstream cs = reinterpret_cast<CUstream>(st);
-  cu_check(ops.write(cs, reinterpret_cast<CUdeviceptr>(remote_flag_[idx]), e,
+  const CUdeviceptr own = reinterpret_cast<CUdeviceptr>(flags_ + idx);
+  cu_check(ops.write(cs, reinterpret_cast<CUdeviceptr>(remote_flag_[idx]), 1,
                      CU_STREAM_WRITE_VALUE_DEFAULT),
            "cuStreamWriteValue32 (posted)");
-  cu_check(ops.wait(cs, reinterpret_cast<CUdeviceptr>(flags_ + idx), e, CU_STREAM_WAIT_VALUE_GEQ),
-           "cuStreamWaitValue32 (done)");
+  cu_check(ops.wait(cs, own, 1, CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32 (done)");
+  cu_check(ops.write(cs, own, 0, CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32 (reset)");
 }
 
 }  // namespace pb

@@ -5,15 +5,16 @@
 // the sender's transfer stream.  Flow control is a two-flag handshake per
 // message, all on the device (stream memory operations, no host round trip):
 //
-//   receiver stream:  write posted[msg] = e   (the slot is free: its previous
+//   receiver stream:  write posted[msg] = 1   (the slot is free: its previous
 //                                               occupant's backward is done)
-//                     wait  done[msg] >= e
-//   sender stream:    wait  posted[msg] >= e
+//                     wait  done[msg] == 1;  write done[msg] = 0
+//   sender stream:    wait  posted[msg] == 1; write posted[msg] = 0
 //                     copy  src -> receiver slot (peer / same-device copy)
-//                     write done[msg] = e
+//                     write done[msg] = 1
 //
-// e is the epoch number (1, 2, ...), so flags never need resetting and a
-// peer running ahead into the next epoch cannot be confused with this one.
+// Every flag is reset by its waiter right after the wait, so the operations
+// are the same every epoch: an epoch is captured once as a CUDA graph
+// (memory-operation nodes) and replayed (ordering argument at send()).
 // Each flag lives in the memory of the side that waits on it; the other side
 // writes it through its IPC mapping.  The i-th send of a channel (boundary,
 // direction) pairs with the i-th receive of the same channel: the programs of
@@ -55,9 +56,9 @@ class IpcLink {
   void connect(const std::vector<std::vector<uint8_t>>& blobs);
   bool connected() const { return connected_; }
 
-  // Enqueue message `idx` (program order) on `st` for epoch value `e` >= 1.
-  void send(int idx, cudaStream_t st, uint32_t e);
-  void recv(int idx, cudaStream_t st, uint32_t e);
+  // Enqueue message `idx` (program order) on `st`.
+  void send(int idx, cudaStream_t st);
+  void recv(int idx, cudaStream_t st);
 
  private:
   struct Entry {

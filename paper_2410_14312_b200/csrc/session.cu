@@ -1,5 +1,6 @@
 // Session implementation — see session.hpp for the design summary.
 #include "session.hpp"
+#include "digest_dev.hpp"
 #include "host_xfer.hpp"
 
 #include <algorithm>
@@ -107,9 +108,10 @@ struct Session::Impl {
   };
 
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
-                      send, recv, mark, ktime, xwait };
+                      send, recv, mark, ktime, xwait, digest };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
+  static constexpr int kDigest = -6;  // in-epoch params digests
   static constexpr int kSideBase = -100;  // side stream of stage s: kSideBase - s
   static constexpr int kBwdBase = -1000;  // backward stream of stage s (split mode)
   static constexpr int kBiasBase = -2000;  // bias-gradient stream of stage s
@@ -221,9 +223,57 @@ struct Session::Impl {
   // parameter transfers at the boundary (load / read of fp64 masters):
   // pinned double-buffered staging and per-layer device scratch
   std::unique_ptr<HostStager> stager;
+  // device digests: scratch, one plan per digest (M per-mini + final), the
+  // results [M + 1], and their stream
+  std::unique_ptr<DeviceDigest> digest;
+  std::vector<DeviceDigest::Plan> dplans;
+  uint64_t* d_digest = nullptr;
+  cudaStream_t dstream = nullptr;
+  // the span table of every local stage's masters of `version(s)`
+  std::vector<DigestSpan> digest_spans(const std::vector<int>& version) const {
+    std::vector<DigestSpan> v;
+    for (size_t s = 0; s < stages.size(); ++s) {
+      const Stage& st = stages[s];
+      const int ver = version[s], p = ver & 1;
+      for (size_t l = 0; l < st.layers.size(); ++l) {
+        const LayerDev& d = st.layers[l];
+        DigestSpan w;
+        w.rows = d.out;
+        w.cols = d.in;
+        if (split) {
+          w.hi = st.pool[st.version_colour[ver]].w16[l];
+          w.lo = d.lo[p];
+          w.ld = d.ld_in;
+        } else {
+          w.f32 = d.w32[p];
+          w.ld = d.in;
+        }
+        v.push_back(w);
+        DigestSpan b;
+        b.f32 = d.b32[p];
+        b.rows = 1;
+        b.cols = d.out;
+        b.ld = d.out;
+        v.push_back(b);
+      }
+    }
+    return v;
+  }
   double* p64 = nullptr;  // one layer's W then b, fp64
   float* p32 = nullptr;   // one layer's W, fp32
   size_t p_cap = 0;       // elements of p64 / p32
+  bool staged_upload = false;  // Session::upload: pageable copies via the stager
+  void ensure_stager() {
+    if (!stager) stager = std::make_unique<HostStager>();
+  }
+  void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (staged_upload) {
+      ensure_stager();
+      stager->h2d(dst, src, bytes, st);
+    } else {
+      PB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    }
+  }
   void param_scratch() {
     if (p64) return;
     size_t mx = 0;
@@ -232,13 +282,12 @@ struct Session::Impl {
     PB_CUDA(cudaMalloc(&p64, mx * 8));
     PB_CUDA(cudaMalloc(&p32, mx * 4));
     p_cap = mx;
-    stager = std::make_unique<HostStager>();
+    ensure_stager();
   }
   std::unique_ptr<P2P> p2p;
   // IPC peer-memory transport (SessionConfig::transport == 1)
   std::unique_ptr<IpcLink> ipc;
   std::vector<IpcLink::Msg> msgs;  // this rank's transfers in program order
-  uint32_t epoch_no = 0;
   int add_msg(bool send, int dir, int peer, size_t bytes, const void* src, void* dst) {
     msgs.push_back(IpcLink::Msg{send, dir, peer, bytes, src, dst});
     return static_cast<int>(msgs.size()) - 1;
@@ -251,6 +300,7 @@ struct Session::Impl {
     if (idx <= kBwdBase) return stages[kBwdBase - idx].bstream;
     if (idx <= kSideBase) return stages[kSideBase - idx].side;
     if (idx == -1) return origin;
+    if (idx == kDigest) return dstream;
     return comm[-idx - 2];
   }
 
@@ -295,6 +345,10 @@ struct Session::Impl {
         if (p) cudaFreeHost(p);
     if (arena && !plan_only) cudaFree(arena);
     stager.reset();
+    if (digest)
+      for (auto& p : dplans) digest->free_plan(p);
+    digest.reset();
+    if (dstream) cudaStreamDestroy(dstream);
     if (p64) cudaFree(p64);
     if (p32) cudaFree(p32);
   }
@@ -539,6 +593,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   I.stage_bytes = rows * (static_cast<size_t>(c.widths.front()) + I.n_out) * 8;
   need += bytes_of(I.stage_bytes, 1);
   need += bytes_of(static_cast<size_t>(M) * U * W, 4) + bytes_of(static_cast<size_t>(M) * W, 4);
+  need += bytes_of(static_cast<size_t>(M) + 1, 8);
   need += 64 * kAlign;
 
   if (c.plan_only) {
@@ -596,9 +651,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   I.stage_buf = I.carve<char>(I.stage_bytes);
   I.fwd_trace = I.carve<int>(static_cast<size_t>(M) * U * W);
   I.bwd_trace = I.carve<int>(static_cast<size_t>(M) * W);
+  I.d_digest = I.carve<uint64_t>(static_cast<size_t>(M) + 1);
 
   if (!c.plan_only) {
   PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
+  if (c.digests) PB_CUDA(cudaStreamCreateWithFlags(&I.dstream, cudaStreamNonBlocking));
   // Stream priorities (PIPESIM_PRIO): 0 all equal; 1 stage streams (forwards,
   // loss, the dgrad chain) above the side streams (wgrad + SGD); 2 also
   // later stages above earlier ones (their backwards start the chain).
@@ -714,6 +771,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     push(z);
     z.dst = st.cur_version;
     push(z);
+    if (c.digests && !c.plan_only) {  // the digest stream starts after the rebase
+      Impl::Op r{OK::record};
+      r.stream = s;
+      r.ev = I.new_event();
+      push(r);
+      Impl::Op w{OK::wait};
+      w.stream = Impl::kDigest;
+      w.ev = r.ev;
+      push(w);
+    }
   }
 
   // Skinny forwards split K (lower latency, more SM-time) when this process
@@ -747,8 +814,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     int order;                     // position of the first member in issue order
     std::vector<int> deps;         // node ids (same-stage predecessor + cross-stage)
     cudaEvent_t done = nullptr;
+    int digest = -1;               // >= 0: in-epoch digest node (index into dplans)
   };
   std::vector<Node> nodes;
+  std::vector<std::vector<int>> digest_version;  // [digest][stage] version read
   const int merge = c.fwd_merge > 0 ? c.fwd_merge : U;
   {
     // last_on_stage: stream-order predecessor (split mode: per kind)
@@ -838,6 +907,40 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       std::sort(n.deps.begin(), n.deps.end());
       n.deps.erase(std::unique(n.deps.begin(), n.deps.end()), n.deps.end());
     }
+    // In-epoch digests (trainer.cpp:492-501): digest k reads, on every stage,
+    // the version current when stage 1 commits mini k (stage s > 1: its latest
+    // commit in an earlier slot); it runs after those commits and before each
+    // stage's commit two versions later, which overwrites that version's
+    // master residual / pool slot.  Both edges point forward in slot order,
+    // so the DAG stays acyclic.  Digest M+1 is the final one (:506).
+    if (c.digests && !c.plan_only) {
+      if (c.world > 1)
+        throw std::invalid_argument("in-epoch digests need every stage in one process");
+      int max_order = 0;
+      for (const Node& n : nodes) max_order = std::max(max_order, n.order);
+      for (int k = 1; k <= M + 1; ++k) {
+        std::vector<int> vs(W, std::min(k, M));
+        if (grid_ && k <= M) {
+          const int t1 = grid_->backward_slot(k, 1);
+          for (int s0 = 1; s0 < W; ++s0) {
+            int v = 0;
+            for (int u = 1; u <= M; ++u)
+              if (grid_->backward_slot(u, s0 + 1) < t1) v = u;
+            vs[s0] = v;
+          }
+        }
+        digest_version.push_back(vs);
+        Node n{false, -1, std::min(k, M), 0, 0, 0,
+               k <= M ? nodes[bwd_node.at({k, 0})].order : max_order + 1, {}};
+        n.digest = k - 1;
+        for (int s0 = 0; s0 < W; ++s0)
+          if (vs[s0] >= 1) n.deps.push_back(bwd_node.at({vs[s0], s0}));
+        nodes.push_back(n);
+        const int id = static_cast<int>(nodes.size()) - 1;
+        for (int s0 = 0; s0 < W; ++s0)
+          if (vs[s0] + 2 <= M) nodes[bwd_node.at({vs[s0] + 2, s0})].deps.push_back(id);
+      }
+    }
   }
   // Kahn's algorithm, earliest original position first.
   std::vector<int> topo;
@@ -902,6 +1005,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   }
   std::map<std::pair<int, int>, int> bwd_id, first_fwd_id;  // (k, s0) -> node
   for (int i = 0; i < static_cast<int>(nodes.size()); ++i) {
+    if (nodes[i].digest >= 0) continue;
     if (!nodes[i].fwd) bwd_id[{nodes[i].k, nodes[i].s}] = i;
     else if (!first_fwd_id.count({nodes[i].k, nodes[i].s})) first_fwd_id[{nodes[i].k, nodes[i].s}] = i;
   }
@@ -910,6 +1014,24 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   for (int id : topo) {
     Node& node = nodes[id];
     const int s = node.s;
+    if (node.digest >= 0) {
+      for (int d : node.deps) {
+        Impl::Op w{OK::wait};
+        w.stream = Impl::kDigest;
+        w.ev = nodes[d].done;
+        push(w);
+      }
+      Impl::Op o{OK::digest};
+      o.stream = Impl::kDigest;
+      o.value = node.digest;
+      push(o);
+      Impl::Op r{OK::record};
+      r.stream = Impl::kDigest;
+      r.ev = I.new_event();
+      node.done = r.ev;
+      push(r);
+      continue;
+    }
     if (!I.local(s)) continue;  // another GPU's stage
     Impl::Stage& st = I.stages[s];
     Impl::Task tk;
@@ -938,7 +1060,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     for (int d : node.deps) {
       // same-stage order is the stream order (same kind, or one stream per stage)
       if (nodes[d].s == s && (nodes[d].fwd == node.fwd || !I.split_fb)) continue;
-      if (I.local(nodes[d].s)) {
+      if (nodes[d].digest >= 0 || I.local(nodes[d].s)) {
         wait_on(ns, nodes[d].done);
         continue;
       }
@@ -1205,6 +1327,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   }
   if (c.world > 1 && c.transport == 1 && !c.plan_only)
     I.ipc = std::make_unique<IpcLink>(c.rank, c.world, c.device, I.arena, I.msgs);
+  if (!digest_version.empty()) {
+    I.digest = std::make_unique<DeviceDigest>(int64_t{1} << 24);
+    for (const auto& vs : digest_version) {
+      I.dplans.push_back(I.digest->make_plan(I.digest_spans(vs)));
+      kernels_per_epoch_ += I.digest->launches_per(I.dplans.back());
+    }
+  }
 }
 
 Session::~Session() = default;
@@ -1324,6 +1453,27 @@ void Session::load_stage_params(int stage, const double* p) {
   }
 }
 
+uint64_t Session::params_digest(int version) {
+  Impl& I = *impl_;
+  if (cfg_.world > 1) throw std::logic_error("params_digest: multi-process session");
+  if (version < 0 || version > cfg_.M) throw std::invalid_argument("version out of range");
+  PB_CUDA(cudaSetDevice(cfg_.device));
+  if (!I.digest) I.digest = std::make_unique<DeviceDigest>(int64_t{1} << 24);
+  if (I.d_digest == nullptr) throw std::logic_error("session has no digest slot");
+  DeviceDigest::Plan p =
+      I.digest->make_plan(I.digest_spans(std::vector<int>(cfg_.W, version)));
+  // after everything queued so far (the last epoch); the result goes to the
+  // final slot and is read back here
+  PB_CUDA(cudaStreamSynchronize(I.origin));
+  uint64_t* out = I.d_digest + cfg_.M;
+  I.digest->enqueue(p, out, I.origin);
+  uint64_t h = 0;
+  PB_CUDA(cudaMemcpyAsync(&h, out, 8, cudaMemcpyDeviceToHost, I.origin));
+  PB_CUDA(cudaStreamSynchronize(I.origin));
+  I.digest->free_plan(p);
+  return h;
+}
+
 namespace {
 // fp32 master of `version` of one stage's layers -> out (flat, W then b per
 // layer, widened to fp64 on the device); split masters are joined first
@@ -1377,7 +1527,19 @@ void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
   if (!st) st = I.origin;
-  upload_rows(I, 0, static_cast<size_t>(cfg_.M) * cfg_.B, x, xt, y, yt, st);
+  // pageable host buffers: pinned staging with threaded host copies
+  cudaPointerAttributes a{};
+  const bool pinned = cudaPointerGetAttributes(&a, x) == cudaSuccess &&
+                      a.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  I.staged_upload = !pinned;
+  try {
+    upload_rows(I, 0, static_cast<size_t>(cfg_.M) * cfg_.B, x, xt, y, yt, st);
+  } catch (...) {
+    I.staged_upload = false;
+    throw;
+  }
+  I.staged_upload = false;
   if (st != I.origin) {
     cudaEvent_t e = I.new_event();
     PB_CUDA(cudaEventRecord(e, st));
@@ -1411,17 +1573,14 @@ void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType
                               static_cast<size_t>(in) * 2, static_cast<size_t>(in) * 2, n,
                               cudaMemcpyHostToDevice, st));
   } else if (xt == HostDType::f64 || xt == HostDType::f32) {
-    PB_CUDA(cudaMemcpyAsync(xb, static_cast<const char*>(x) + r0 * in * xes, n * in * xes,
-                            cudaMemcpyHostToDevice, st));
+    I.copy_h2d(xb, static_cast<const char*>(x) + r0 * in * xes, n * in * xes, st);
   } else {
     throw std::invalid_argument("x must be f64, f32 or bf16");
   }
   if (yt == HostDType::f64) {
-    PB_CUDA(cudaMemcpyAsync(yb, static_cast<const char*>(y) + r0 * I.n_out * 8, n * I.n_out * 8,
-                            cudaMemcpyHostToDevice, st));
+    I.copy_h2d(yb, static_cast<const char*>(y) + r0 * I.n_out * 8, n * I.n_out * 8, st);
   } else if (yt == HostDType::f32) {
-    PB_CUDA(cudaMemcpyAsync(ydst, static_cast<const float*>(y) + r0 * I.n_out, n * I.n_out * 4,
-                            cudaMemcpyHostToDevice, st));
+    I.copy_h2d(ydst, static_cast<const float*>(y) + r0 * I.n_out, n * I.n_out * 4, st);
   } else if (yt == HostDType::labels_i32) {  // the loss kernel reads labels directly
     PB_CUDA(cudaMemcpyAsync(I.ylab + r0, static_cast<const int*>(y) + r0, n * 4,
                             cudaMemcpyHostToDevice, st));
@@ -1466,6 +1625,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
     if (c) streams.push_back(c);
   if (I.h2d) streams.push_back(I.h2d);
   if (I.h2dc) streams.push_back(I.h2dc);
+  if (I.dstream) streams.push_back(I.dstream);
   if (!I.fork_ev) I.fork_ev = I.new_event();
   while (I.join_ev.size() < streams.size()) I.join_ev.push_back(I.new_event());
   cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
@@ -1507,13 +1667,13 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         break;
       case OK::send:
         if (I.ipc)
-          I.ipc->send(o.value, s, I.epoch_no);
+          I.ipc->send(o.value, s);
         else
           I.p2p->send(o.src, o.bytes, o.peer, o.dir, s);
         break;
       case OK::recv:
         if (I.ipc)
-          I.ipc->recv(o.value, s, I.epoch_no);
+          I.ipc->recv(o.value, s);
         else
           I.p2p->recv(o.dst, o.bytes, o.peer, o.dir, s);
         break;
@@ -1522,6 +1682,9 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         break;
       case OK::xwait:
         if (I.streaming) PB_CUDA(cudaStreamWaitEvent(s, I.x_ready[o.value], 0));
+        break;
+      case OK::digest:
+        I.digest->enqueue(I.dplans[o.value], I.d_digest + o.value, s);
         break;
       case OK::ktime:  // an event record node when captured
         PB_CUDA(cudaEventRecordWithFlags(I.kt_ev[o.value], s,
@@ -1539,12 +1702,10 @@ void issue(Session::Impl& I, cudaStream_t origin) {
 EpochResult Session::run_epoch() {
   Impl& I = *impl_;
   PB_CUDA(cudaSetDevice(cfg_.device));
-  if (I.ipc) {
-    if (!I.ipc->connected()) throw std::logic_error("IPC transport: call ipc_connect first");
-    ++I.epoch_no;  // the handshake values of this epoch
-  }
+  if (I.ipc && !I.ipc->connected())
+    throw std::logic_error("IPC transport: call ipc_connect first");
   PB_CUDA(cudaEventRecord(I.t0, I.origin));
-  if (cfg_.use_graph && !I.ipc) {
+  if (cfg_.use_graph) {
     if (I.exec && I.graph_labels != static_cast<int>(I.use_labels)) {
       cudaGraphExecDestroy(I.exec);
       cudaGraphDestroy(I.graph);
@@ -1599,8 +1760,8 @@ EpochResult Session::train_epoch_host(const void* x, HostDType xt, const void* y
     }
     return a.type == cudaMemoryTypeHost;  // page-locked (cudaHostAlloc / registered)
   };
-  // IPC (eager epochs) or pageable buffers (not capturable): upload, then the epoch
-  if (I.ipc || !pinned(x) || !pinned(y)) {
+  // pageable buffers (not capturable): upload, then the epoch
+  if (!pinned(x) || !pinned(y)) {
     upload(x, xt, y, yt);
     return run_epoch();
   }
@@ -1661,10 +1822,8 @@ EpochResult Session::profile_epoch(EpochProfile* prof) {
     I.mark_ev.assign(2 * I.node_meta.size(), nullptr);
     for (cudaEvent_t& e : I.mark_ev) PB_CUDA(cudaEventCreate(&e));
   }
-  if (I.ipc) {
-    if (!I.ipc->connected()) throw std::logic_error("IPC transport: call ipc_connect first");
-    ++I.epoch_no;
-  }
+  if (I.ipc && !I.ipc->connected())
+    throw std::logic_error("IPC transport: call ipc_connect first");
   PB_CUDA(cudaEventRecord(I.t0, I.origin));
   I.profiling = true;
   try {
@@ -1722,6 +1881,11 @@ EpochResult Session::collect_result() {
   }
   for (const auto& p : ledger_.pins) r.pinned.push_back(p.version);
   r.consumed = ledger_.update_source;
+  if (!I.dplans.empty()) {
+    r.digests.resize(static_cast<size_t>(M) + 1);
+    PB_CUDA(cudaMemcpy(r.digests.data(), I.d_digest, r.digests.size() * 8,
+                       cudaMemcpyDeviceToHost));
+  }
   last_ = r;
   return r;
 }

@@ -77,6 +77,10 @@ struct SessionConfig {
   // forwards and backwards of a stage on separate streams, with the slot
   // order's hazards as explicit events (PIPESIM_SPLIT_FB overrides)
   bool split_fb = true;
+  // the reference's params_digest (trainer.cpp:492-501, :506) on the device,
+  // inside the epoch: after every mini-batch's stage-1 commit over all stages'
+  // then-current masters, and once over the final ones (digest_dev.hpp)
+  bool digests = false;
 };
 
 // One point-to-point transfer of the program, in this process's issue order.
@@ -95,6 +99,7 @@ struct EpochResult {
   std::vector<int> dev_bwd;       // [M * W] tags propagated through by backwards
   std::vector<int> dev_current;   // [W] current version after the epoch
   float device_ms = 0.f;          // graph/stream time of the epoch
+  std::vector<uint64_t> digests;  // [M + 1] per-mini-batch, then final (digests on)
 };
 
 // Per-node device timeline of one epoch (profile_epoch): a node is one
@@ -128,6 +133,11 @@ class Session {
 
   // Installs a flat whole-network parameter vector as version 0.
   void load_params(const double* flat);
+  // params_digest (trainer.cpp:599-607) of every stage's current version,
+  // computed on the device; single-process sessions
+  // (version: 0 after load_params, M after an epoch)
+  uint64_t params_digest(int version);
+  const EpochResult& last_result() const { return last_; }
   // version 0 of one stage (1-based) := p, W then b per layer (fp64)
   void load_stage_params(int stage, const double* p);
   // Copies the current version's fp32 masters out as doubles (flat layout).

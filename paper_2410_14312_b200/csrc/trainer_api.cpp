@@ -112,23 +112,24 @@ struct SessionHandle {
 std::mutex g_cache_mu;
 std::map<std::string, std::shared_ptr<SessionHandle>> g_cache;
 
-std::string cache_key(const train_config& cfg, train_mode mode, bool snaps, int device,
-                      bool graph) {
+std::string cache_key(const train_config& cfg, train_mode mode, bool snaps, bool digests,
+                      int device, bool graph) {
   std::ostringstream k;
   for (int w : cfg.net.widths) k << w << ',';
   k << '|';
   for (auto a : cfg.net.activations) k << static_cast<int>(a) << ',';
   k << '|' << static_cast<int>(cfg.net.loss) << '|' << cfg.workers << '|' << cfg.micro_batches
     << '|' << cfg.mini_batch_size << '|' << cfg.mini_batches << '|' << format_double(cfg.learning_rate)
-    << '|' << static_cast<int>(mode) << '|' << snaps << '|' << device << '|' << graph;
+    << '|' << static_cast<int>(mode) << '|' << snaps << '|' << digests << '|' << device << '|'
+    << graph;
   return k.str();
 }
 
 std::shared_ptr<SessionHandle> session_for(const train_config& cfg, train_mode mode, bool snaps,
-                                           int* units) {
+                                           int* units, bool digests = false) {
   const b200::options opt = b200::get_options();
-  const std::string key =
-      cache_key(cfg, mode, snaps, opt.device, opt.use_graph) + (opt.verify_fp32 ? "|fp32" : "");
+  const std::string key = cache_key(cfg, mode, snaps, digests, opt.device, opt.use_graph) +
+                          (opt.verify_fp32 ? "|fp32" : "");
   std::lock_guard<std::mutex> lk(g_cache_mu);
   auto it = g_cache.find(key);
   *units = mode == train_mode::timeprest ? cfg.micro_batches : 1;
@@ -151,6 +152,7 @@ std::shared_ptr<SessionHandle> session_for(const train_config& cfg, train_mode m
   tc.use_graph = opt.use_graph ? 1 : 0;
   tc.snapshots = snaps ? 1 : 0;
   tc.precision = opt.verify_fp32 ? PB_PRECISION_FP32_VERIFY : PB_PRECISION_BF16;
+  tc.digests = digests ? 1 : 0;
   auto h = std::make_shared<SessionHandle>();
   ok(pb_session_create(&net, &tc, &h->s));
   g_cache[key] = h;
@@ -190,18 +192,23 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   tm.plan_ms = ms_since(tp);
   const b200::options opt = b200::get_options();
   const long long P = cfg.net.param_count();
-  bool every_mini = opt.digest == b200::digest_policy::every_mini ||
-                    (opt.digest == b200::digest_policy::automatic && P <= opt.digest_auto_limit);
+  // Per-mini-batch checksums (trainer.cpp:492-501) are computed on the
+  // device inside the epoch (digest_dev.hpp), so the reference's contract --
+  // a checksum for every mini-batch -- holds at every network size;
+  // final_only (or automatic above digest_auto_limit) keeps only the final one.
+  const bool every_mini = opt.digest == b200::digest_policy::every_mini ||
+                          (opt.digest == b200::digest_policy::automatic &&
+                           P <= opt.digest_auto_limit);
   // retained versions older than M-1 (1F1B stashes) need snapshots
   bool old_retained = false;
   if (grid)
     for (int s = 0; s < W; ++s)
       for (const auto& iv : timeline.per_stage[s])
         if (iv.freed_at_slot > timeline.horizon && iv.version < M - 1) old_retained = true;
-  const bool snaps = every_mini || static_cast<bool>(observer) || old_retained;
+  const bool snaps = static_cast<bool>(observer) || old_retained;
 
   int units = 1;
-  std::shared_ptr<SessionHandle> h = session_for(cfg, mode, snaps, &units);
+  std::shared_ptr<SessionHandle> h = session_for(cfg, mode, snaps, &units, every_mini);
   std::lock_guard<std::mutex> in_use(h->use);
 
   // Rebase: version 0 := the current weights (trainer.cpp:372-379), stage by
@@ -225,6 +232,14 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
   ok(pb_session_run_epoch(h->s, &out));
   tm.step_ms = ms_since(tp);
   tm.device_ms = out.device_ms;
+  // the epoch's digests (every mini-batch + final) were computed in the graph;
+  // otherwise only the final one, on the device now
+  std::vector<char> digests(static_cast<size_t>(M + 1) * 17, 0);
+  if (every_mini)
+    ok(pb_session_digests(h->s, digests.data(), M + 1));
+  else
+    ok(pb_session_params_digest(h->s, M, digests.data() + static_cast<size_t>(M) * 17));
+  tm.digest_ms += ms_since(tp);
 
   // The device-observed version trace must equal the ledger, bit for bit.
   for (int k = 0; k < M; ++k)
@@ -264,24 +279,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
     m.loss = losses[k - 1];
     for (int j = 0; j < units; ++j) m.pinned.push_back(pinned[(k - 1) * units + j]);
     m.consumed = consumed[k - 1];
-    if (every_mini) {
-      // digest after mini k's stage-1 commit: stage s holds its latest commit
-      // strictly before that slot (trainer.cpp:492-501)
-      std::vector<std::vector<double>> vals;
-      std::vector<pb::value_span> spans;
-      for (int s = 1; s <= W; ++s) {
-        int v = k;
-        if (grid && s > 1) {
-          v = 0;
-          for (const auto& c : ledger.commits)
-            if (c.stage == s && c.slot < ledger.full_commit_slot[k]) v = std::max(v, c.version);
-        }
-        vals.push_back(version_values(s, v));
-      }
-      for (const auto& v : vals) spans.push_back({v.data(), static_cast<int64_t>(v.size())});
-      m.checksum = pb::digest_spans(spans);
-      tm.digest_ms += ms_since(tp);
-    }
+    if (every_mini) m.checksum.assign(digests.data() + static_cast<size_t>(k - 1) * 17, 16);
     log.minis.push_back(std::move(m));
   }
 
@@ -296,8 +294,7 @@ epoch_log train_epoch(std::vector<stage_model>& stages, const dataset& data,
     st.current_version = M;
   }
   tm.readback_ms += ms_since(tp);
-  log.final_checksum = params_digest(stages);
-  tm.digest_ms += ms_since(tp);
+  log.final_checksum = std::string(digests.data() + static_cast<size_t>(M) * 17, 16);
 
   if (observer && grid) {
     // verify mode: replay the retention timeline with the committed snapshots

@@ -570,8 +570,12 @@ def format_double(v: float) -> str:
         ("-" if sexp < 0 else "+") + f"{abs(sexp):02d}"
     if point <= 0:
         fix = "0." + "0" * (-point) + digits
-    elif point >= nd:
-        fix = digits + "0" * (point - nd)
+    elif point > nd:
+        # trailing zeros would be needed: v is an integer, and std::to_chars
+        # prints its exact digits (same length, zero difference)
+        fix = str(abs(int(v)))
+    elif point == nd:
+        fix = digits
     else:
         fix = digits[:point] + "." + digits[point:]
     return ("-" if neg else "") + (fix if len(fix) <= len(sci) else sci)
@@ -590,7 +594,7 @@ class Session:
     def __init__(self, net: NetworkSpec, workers, micro_batches, mini_batch_size,
                  mini_batches, learning_rate, mode="timeprest", device=0, use_graph=True,
                  snapshots=False, fwd_merge=0, rank=0, world=1, nccl_ids=b"",
-                 timed_kernel=None, transport="nccl", precision="bf16"):
+                 timed_kernel=None, transport="nccl", precision="bf16", digests=False):
         if mode not in TRAIN_MODES:
             raise DomainError(f"unknown training mode: {mode}", "mode")
         self.net = net
@@ -601,7 +605,8 @@ class Session:
                               float(learning_rate), TRAIN_MODES.index(mode), device,
                               int(use_graph), int(snapshots), int(fwd_merge),
                               TIMED_KERNELS.index(timed_kernel),
-                              TRANSPORTS.index(transport), PRECISIONS.index(precision))
+                              TRANSPORTS.index(transport), PRECISIONS.index(precision),
+                              int(digests))
         spec = net._c()
         h = C.c_void_p()
         if world > 1:
@@ -778,6 +783,21 @@ class Session:
                         start_ms=float(t0[i]), end_ms=float(t1[i])) for i in range(n)])
         return r
 
+    def digests(self):
+        """The M + 1 in-epoch digests of the last epoch (digests=True): the
+        per-mini-batch checksums (mini_log::checksum), then the final one."""
+        buf = C.create_string_buffer(17 * (self.M + 1))
+        N.check(_L().pb_session_digests(self._h, buf, self.M + 1))
+        return [buf.raw[17 * i:17 * i + 16].decode() for i in range(self.M + 1)]
+
+    def params_digest(self, version=None):
+        """params_digest of every stage's `version` (default M: after an
+        epoch), computed on the device."""
+        out = C.create_string_buffer(17)
+        N.check(_L().pb_session_params_digest(self._h, self.M if version is None else version,
+                                              out))
+        return out.value.decode()
+
     def run_epoch(self):
         M, U, W = self.M, self.units, self.W
         r = dict(mini_loss=np.zeros(M), pinned=np.zeros(M * U, np.int32),
@@ -855,15 +875,16 @@ class b200:
     """Execution knobs of the GPU build (not part of the reference API)."""
     device = int(os.environ.get("PIPESIM_B200_DEVICE", "0"))
     use_graph = True
+    # per-mini-batch checksums are computed on the device inside the epoch
     digest = "automatic"         # "automatic" | "every_mini" | "final_only"
-    digest_auto_limit = 4_000_000
+    digest_auto_limit = 1 << 40  # params; automatic above it: final only
     precision = "bf16"           # "bf16" (tensor cores) | "fp32" (FFMA verify mode)
 
 
-def _session_for(cfg: TrainConfig, mode: str, snapshots: bool) -> Session:
+def _session_for(cfg: TrainConfig, mode: str, snapshots: bool, digests: bool = False) -> Session:
     key = (tuple(cfg.net.widths), tuple(cfg.net.activations), cfg.net.loss, cfg.workers,
            cfg.micro_batches, cfg.mini_batch_size, cfg.mini_batches, float(cfg.learning_rate),
-           mode, snapshots, b200.device, b200.use_graph, b200.precision)
+           mode, snapshots, digests, b200.device, b200.use_graph, b200.precision)
     s = _SESSIONS.get(key)
     if s is None:
         if len(_SESSIONS) > 8:
@@ -872,7 +893,7 @@ def _session_for(cfg: TrainConfig, mode: str, snapshots: bool) -> Session:
             _SESSIONS.clear()
         s = Session(cfg.net, cfg.workers, cfg.micro_batches, cfg.mini_batch_size,
                     cfg.mini_batches, cfg.learning_rate, mode, b200.device, b200.use_graph,
-                    snapshots, precision=b200.precision)
+                    snapshots, precision=b200.precision, digests=digests)
         _SESSIONS[key] = s
     return s
 
@@ -915,7 +936,7 @@ def train_epoch(stages: List[StageModel], data: Dataset, cfg: TrainConfig, mode:
     want = b200.digest
     if want == "automatic":
         want = "every_mini" if P <= b200.digest_auto_limit else "final_only"
-    snaps = want == "every_mini" or observer is not None
+    snaps = observer is not None
     if mode != "sequential" and not snaps:
         # retained versions older than M-1 (1F1B stashes) are read from snapshots
         sc0 = SimConfig(cfg.workers, cfg.micro_batches, cfg.mini_batches,
@@ -924,7 +945,7 @@ def train_epoch(stages: List[StageModel], data: Dataset, cfg: TrainConfig, mode:
         t0 = build_retention_timeline(assign_versions(g0, sc0), g0)
         snaps = any(b > t0.horizon and v < cfg.mini_batches - 1
                     for iv in t0.intervals for v, a, b in iv)
-    sess = _session_for(cfg, mode, snaps)
+    sess = _session_for(cfg, mode, snaps, want == "every_mini")
     sess.load_params(gather_network_params(stages))
     sess.upload(data.x, data.y)
     r = sess.run_epoch()
@@ -948,28 +969,14 @@ def train_epoch(stages: List[StageModel], data: Dataset, cfg: TrainConfig, mode:
         ledger = assign_versions(grid, sc)
         timeline = build_retention_timeline(ledger, grid)
 
-    def version_at(stage, t_slot):
-        # current version of `stage` just before slot t_slot (stage-1 commit)
-        v = 0
-        for c in ledger.commits:
-            if c[2] == stage and c[3] < t_slot:
-                v = max(v, int(c[0]))
-        return v
-
+    # checksums: computed on the device (digest_dev.hpp) -- in the epoch after
+    # every stage-1 commit (trainer.cpp:492-501), or the final one now
+    dig = sess.digests() if want == "every_mini" else None
     for k in range(1, M + 1):
-        chk = ""
-        if want == "every_mini":
-            if mode == "sequential":
-                vals = [sess.snapshot(s, k) for s in range(1, W + 1)]
-            else:
-                t = int(ledger.full_commit_slot[k])
-                vals = [sess.snapshot(1, k)] + [sess.snapshot(s, version_at(s, t))
-                                               for s in range(2, W + 1)]
-            chk = digest_values(np.concatenate(vals))
         log.minis.append(MiniLog(k, float(r["mini_loss"][k - 1]),
                                  [int(v) for v in r["pinned"][k - 1]],
-                                 int(r["consumed"][k - 1]), chk))
-    log.final_checksum = digest_values(final)
+                                 int(r["consumed"][k - 1]), dig[k - 1] if dig else ""))
+    log.final_checksum = dig[M] if dig else sess.params_digest(M)
 
     # install the final state into the stage objects
     for s, st in enumerate(stages):
