@@ -11,7 +11,10 @@ import os
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "lib" / "libpipesim_b200.so"
+# PIPESIM_LIB: an alternative build of the same library (A/B experiments,
+# tools/gpu/build_variants.sh); the default is the in-tree build
+LIB_PATH = pathlib.Path(os.environ["PIPESIM_LIB"]) if os.environ.get("PIPESIM_LIB") else \
+    _HERE / "lib" / "libpipesim_b200.so"
 
 
 class PipesimError(RuntimeError):

@@ -102,6 +102,19 @@ __device__ __forceinline__ float act_grad_from_out(float a, int act) {
   }
 }
 
+// wgrad+SGD pair kernel: operand ring depth and split-master buffers per
+// epilogue warp (kSgdBufs - 2 chunks of masters are loaded ahead: the
+// update is HBM-latency-bound per warp)
+#ifndef PB_WGRAD_STAGES
+#define PB_WGRAD_STAGES 4
+#endif
+#ifndef PB_SGD_BUFS
+#define PB_SGD_BUFS 3
+#endif
+#ifndef PB_SGD_L2PF
+#define PB_SGD_L2PF 0
+#endif
+
 template <int BN>
 struct GemmCfg {
   static constexpr int kBM = 128;
@@ -892,7 +905,7 @@ __global__ void __launch_bounds__(128, 1)
 // are clipped by the tensor maps.  n_cols is a multiple of 64.
 struct SgdTmaState {
   int g = 0;                  // chunks processed by this warp so far
-  uint32_t phase[3] = {0, 0, 0};
+  uint32_t phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 __device__ __forceinline__ void sgd_tma_load(const EpiMaps& maps, uint8_t* buf32, uint64_t* bar,
@@ -994,16 +1007,21 @@ __device__ __forceinline__ void split_master(float w, uint32_t& hi16, uint32_t& 
 
 // TMA epilogue of wgrad + SGD with split masters: one warp, 32 rows x n_cols,
 // 32 x 32 chunks.  hi and lo of the current version arrive by TMA (64-byte
-// swizzle, 2 KB each) one chunk ahead into one of three 4 KB buffers; each
+// swizzle, 2 KB each) into one of kBufs 4 KB buffers, kBufs - 2 chunks ahead
+// (across the tile boundary into the warp's part of the next tile); each
 // thread rebuilds its row's fp32 masters, applies the update and writes the
-// new hi / lo back in place; one lane stores both with TMA.  Three buffers:
-// the load of chunk c+1 waits only for the store of chunk c-2 to have read
-// its buffer, not for the store just issued.
+// new hi / lo back in place; one lane stores both with TMA.  The load of
+// chunk c + kBufs - 2 reuses the buffer of chunk c - 2, whose store has read
+// it once at most one bulk group (chunk c - 1's) is still reading.  The
+// per-warp update is bound by HBM latency x chunks in flight, so the depth
+// sets its rate.
+template <int kBufs>
 __device__ __forceinline__ void epilogue_warp_tma_sgd_split(
     const EpiParams& ep, const EpiMaps& maps, int row_base, int n_base, int n_cols,
     uint32_t t_row, uint8_t* wbuf, uint64_t* bars, SgdTmaState& st, bool first_tile,
     int next_row, int next_col) {
-  constexpr int kBufs = 3;
+  static_assert(kBufs >= 3 && kBufs <= 6, "split SGD epilogue: 3..6 buffers");
+  constexpr int kAhead = kBufs - 2;
   const int lane = threadIdx.x % 32;
   const bool skip_ld = ep.dbg_skip & 2, skip_st = ep.dbg_skip & 4;  // timing experiments
   auto buf = [&](int g) { return wbuf + (g % kBufs) * 4096; };
@@ -1013,18 +1031,41 @@ __device__ __forceinline__ void epilogue_warp_tma_sgd_split(
     ptx::tma_load_2d(buf(g), &maps.w_cur, bar, col, row);
     ptx::tma_load_2d(buf(g) + 2048, &maps.w_new, bar, col, row);
   };
-  if (first_tile && lane == 0 && !skip_ld) load(st.g, n_base, row_base);
+  // chunk `a` chunks after chunk c of this tile: its coordinates, or false
+  // past the next tile
+  auto ahead = [&](int c, int a, int* col, int* row) {
+    const int cc = c + 32 * a;
+    if (cc < n_cols) {
+      *col = n_base + cc;
+      *row = row_base;
+      return true;
+    }
+    if (next_row < 0 || cc - n_cols >= n_cols) return false;
+    *col = next_col + (cc - n_cols);
+    *row = next_row;
+    return true;
+  };
+  if (first_tile && lane == 0 && !skip_ld)
+    for (int a = 0; a < kAhead; ++a) {
+      int col, row;
+      if (ahead(0, a, &col, &row)) load(st.g + a, col, row);
+    }
 #pragma unroll 1
   for (int c = 0; c < n_cols; c += 32) {
     const int g = st.g;
     const int b = g % kBufs;
     if (lane == 0) {
-      ptx::bulk_wait_group_read<1>();  // chunk g-2's store has read buffer (g+1) % 3
-      if (skip_ld) {
-      } else if (c + 32 < n_cols)
-        load(g + 1, n_base + c + 32, row_base);
-      else if (next_row >= 0)
-        load(g + 1, next_col, next_row);
+      ptx::bulk_wait_group_read<1>();  // chunk g-2's store has read buffer (g+kAhead) % kBufs
+      int col, row;
+      if (!skip_ld && ahead(c, kAhead, &col, &row)) load(g + kAhead, col, row);
+#if PB_SGD_L2PF
+      // the same chunk of the warp's next tile into L2 a tile ahead: its TMA
+      // load then waits on L2, not HBM, latency (no shared memory held)
+      if (!skip_ld && next_row >= 0) {
+        ptx::tma_prefetch_2d(&maps.w_cur, next_col + c, next_row);
+        ptx::tma_prefetch_2d(&maps.w_new, next_col + c, next_row);
+      }
+#endif
     }
     uint32_t r[32];
     ptx::tmem_ld32(t_row + c, r);
@@ -1095,15 +1136,18 @@ struct Gemm2Cfg {
   static constexpr int kBSub = (kMmaN / 2) * kBK * 2;  // this CTA's B rows of one MMA
   static constexpr int kBHalf = kSub * kBSub;          // this CTA's B rows
   static constexpr int kStageBytes = kAHalf + kBHalf;
-  // wgrad tiles are short in K (one mini-batch): 4 stages leave room for the
-  // TMA epilogue's double-buffered master tiles
+  // wgrad tiles are short in K (one mini-batch): a shallower ring leaves room
+  // for the TMA epilogue's master-tile buffers (PB_WGRAD_STAGES)
   static constexpr int kStages =
-      EPI == kEpiWgradSgd ? 4 : (BN > 256 ? 4 : (BN >= 256 ? 6 : 8));
+      EPI == kEpiWgradSgd ? PB_WGRAD_STAGES : (BN > 256 ? 4 : (BN >= 256 ? 6 : 8));
   static constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  // per epilogue warp: staging block (vector epilogue) or, for SGD, 2 x (fp32
-  // 32x32 master tile 4 KB + bf16 32x32 tile 2 KB) for the TMA epilogue
-  static constexpr int kSgdWarpBytes = 2 * (4096 + 2048);
+  // per epilogue warp: staging block (vector epilogue) or, for SGD, the TMA
+  // epilogue's buffers: split masters kSgdBufs x 4 KB (hi + lo of a 32x32
+  // chunk), fp32 masters 2 x (fp32 32x32 tile 4 KB + bf16 32x32 tile 2 KB)
+  static constexpr int kSgdBufs = PB_SGD_BUFS;
+  static constexpr int kSgdWarpBytes =
+      kSgdBufs * 4096 > 2 * (4096 + 2048) ? kSgdBufs * 4096 : 2 * (4096 + 2048);
   static constexpr int kEpiBytes = EPI == kEpiWgradSgd ? kEpiWarps * kSgdWarpBytes
                                                        : kEpiWarps * 32 * kVecLd * 4;
   static constexpr int kBarOff = kStages * kStageBytes + kEpiBytes;
@@ -1131,10 +1175,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;   // [2]
   uint64_t* tempty_bar = tfull_bar + 2;  // [2] (leader's are used)
-  uint64_t* sgd_bar = tempty_bar + 2;    // [3 per epilogue warp] (TMA SGD epilogue)
+  uint64_t* sgd_bar = tempty_bar + 2;    // [kSgdBufs per epilogue warp] (TMA SGD epilogue)
   // (own 16-byte slot, apart from the barriers thread 0 initialises)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::kBarOff + 448);
-  static_assert(sizeof(uint64_t) * (2 * Cfg::kStages + 4 + 3 * Cfg::kEpiWarps) <= 448,
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::kBarOff + 496);
+  static_assert(sizeof(uint64_t) * (2 * Cfg::kStages + 4 +
+                                    (EPI == kEpiWgradSgd ? Cfg::kSgdBufs * Cfg::kEpiWarps : 0)) <=
+                    496,
                 "barrier region overlaps the TMEM address slot");
 
   const int warp = threadIdx.x / 32;
@@ -1163,7 +1209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
     }
     if constexpr (EPI == kEpiWgradSgd)
       if (ep.rowwise == 3) {
-        for (int i = 0; i < 3 * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
+        for (int i = 0; i < Cfg::kSgdBufs * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
         ptx::tma_prefetch_desc(&maps.w_cur);
         ptx::tma_prefetch_desc(&maps.w_new);
         if (ep.has_w16) ptx::tma_prefetch_desc(&maps.w16);
@@ -1319,13 +1365,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             next_col = (nt % tiles_n) * BN + c_off;
           }
           if (ep.split_master)
-            epilogue_warp_tma_sgd_split(ep, maps, row_base, tn * BN + c_off, kColsPerWarp,
-                                        t_row, sgd_buf, sgd_bar + 3 * e, sgd_st, local == 0,
-                                        next_row, next_col);
+            epilogue_warp_tma_sgd_split<Cfg::kSgdBufs>(
+                ep, maps, row_base, tn * BN + c_off, kColsPerWarp, t_row, sgd_buf,
+                sgd_bar + Cfg::kSgdBufs * e, sgd_st, local == 0, next_row, next_col);
           else
             epilogue_warp_tma_sgd(ep, maps, row_base, tn * BN + c_off, kColsPerWarp, t_row,
-                                  sgd_buf, sgd_bar + 3 * e, sgd_st, local == 0, next_row,
-                                  next_col);
+                                  sgd_buf, sgd_bar + Cfg::kSgdBufs * e, sgd_st, local == 0,
+                                  next_row, next_col);
         }
       } else if (ep.rowwise == 2) {
         with_act<EPI>(ep, [&](auto A) {
