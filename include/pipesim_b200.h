@@ -233,6 +233,35 @@ int pb_loss_fwd_bwd(void* stream, const float* y, int rows, int cols, int ld_y,
                     const float* targets, int ld_t, int loss, int act_last,
                     float denom, uint16_t* dz, int ld_dz, float* row_loss);
 
+/* ---- VGG-style conv stages (BASELINE configs[3]; no reference counterpart,
+ * SPEC.md:379).  NHWC bf16 activations [n][h][w][c]; 3x3 convolution, pad 1,
+ * stride 1; weights [cout][ld_w] bf16 with K = (3r + s) * cin + c (tap-major),
+ * ld_w >= 9 * cin.  cin and cout multiples of 64 (the network input goes
+ * through pb_im2col_first + the Linear kernels). */
+/* y[n*h*w, cout] = act(conv(x, w) + b) (implicit GEMM: im2col TMA operand). */
+int pb_conv_fwd(void* stream, const uint16_t* x, int n, int h, int w, int cin,
+                const uint16_t* wt, int cout, int ld_w, const float* bias, int act,
+                uint16_t* y);
+/* d[n*h*w, cin] = conv_transpose(dz, w) .* act'(xin). */
+int pb_conv_bwd_dx(void* stream, const uint16_t* dz, int n, int h, int w, int cout,
+                   const uint16_t* wt, int cin, int ld_w, const uint16_t* xin,
+                   int act_prev, uint16_t* d);
+/* w_new = w_cur - lr * dW, dW[cout, 9*cin] = sum_p dz[p]^T im2col(x)[p]
+ * (split-K fp32 partial slabs, then an in-order reduction fused with SGD);
+ * w16 (may be NULL) = bf16(w_new).  w_cur / w_new fp32 [cout][ld_w32]. */
+int pb_conv_bwd_dw_sgd(void* stream, const uint16_t* dz, int n, int h, int w, int cout,
+                       const uint16_t* x, int cin, const float* w_cur, float* w_new,
+                       int ld_w32, uint16_t* w16, int ld_w16, float lr);
+/* 2x2 max pooling, stride 2 (gradient to the first maximum of a window). */
+int pb_maxpool2_fwd(void* stream, const uint16_t* in, int n, int h, int w, int c,
+                    uint16_t* out);
+int pb_maxpool2_bwd(void* stream, const uint16_t* d_out, const uint16_t* in,
+                    const uint16_t* out, int n, int h, int w, int c, uint16_t* d_in);
+/* out[n*h*w, ldo] = im2col of a narrow NHWC input (k = (3r+s)*c + ch, zero
+ * padded to ldo); x rows of ld_x elements per image. */
+int pb_im2col_first(void* stream, const uint16_t* x, int ld_x, int n, int h, int w, int c,
+                    uint16_t* out, int ldo);
+
 /* Elementwise conversions used at the host boundary. */
 int pb_convert_f64_to_bf16(void* stream, const double* src, int rows, int cols,
                            int ld_src, uint16_t* dst, int ld_dst);

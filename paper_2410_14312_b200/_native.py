@@ -161,6 +161,12 @@ def _declare(L: C.CDLL) -> None:
         "pb_join_master": (i, [p, p, p, i, i, i, p, i]),
         "pb_bias_sgd": (i, [p, p, i, i, i, p, p, p, f]),
         "pb_loss_fwd_bwd": (i, [p, p, i, i, i, p, i, i, i, f, p, i, p]),
+        "pb_conv_fwd": (i, [p, p, i, i, i, i, p, i, i, p, i, p]),
+        "pb_conv_bwd_dx": (i, [p, p, i, i, i, i, p, i, i, p, i, p]),
+        "pb_conv_bwd_dw_sgd": (i, [p, p, i, i, i, i, p, i, p, p, i, p, i, f]),
+        "pb_maxpool2_fwd": (i, [p, p, i, i, i, i, p]),
+        "pb_maxpool2_bwd": (i, [p, p, p, p, i, i, i, i, p]),
+        "pb_im2col_first": (i, [p, p, i, i, i, i, i, p, i]),
         "pb_convert_f64_to_bf16": (i, [p, p, i, i, i, p, i]),
         "pb_convert_f32_to_bf16": (i, [p, p, i, i, i, p, i]),
     }

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <string>
 
+#include "conv_ops.cuh"
 #include "layer_ops.cuh"
 #include "pipesim_core.hpp"
 #include "status.hpp"
@@ -198,6 +199,68 @@ int pb_loss_fwd_bwd(void* stream, const float* y, int rows, int cols, int ld_y,
   PB_GUARD_BEGIN
   pb::launch_loss(as_stream(stream), y, rows, cols, ld_y, targets, ld_t, loss,
                   act_last, denom, bfm(dz), ld_dz, row_loss);
+  PB_GUARD_END
+}
+
+int pb_conv_fwd(void* stream, const uint16_t* x, int n, int h, int w, int cin,
+                const uint16_t* wt, int cout, int ld_w, const float* bias, int act,
+                uint16_t* y) {
+  PB_GUARD_BEGIN
+  pb::Nhwc t{bf(x), n, h, w, cin};
+  pb::Mat16 mw{bf(wt), cout, 9 * cin, ld_w};
+  pb::GemmLaunch g = pb::plan_conv_fwd(t, 0, n, mw, bias, act, bfm(y), 0);
+  pb::launch_fwd(g, as_stream(stream));
+  PB_GUARD_END
+}
+
+int pb_conv_bwd_dx(void* stream, const uint16_t* dz, int n, int h, int w, int cout,
+                   const uint16_t* wt, int cin, int ld_w, const uint16_t* xin,
+                   int act_prev, uint16_t* d) {
+  PB_GUARD_BEGIN
+  pb::Nhwc t{bf(dz), n, h, w, cout};
+  pb::GemmLaunch g = pb::plan_conv_dgrad(t, bf(wt), cin, ld_w, bf(xin), act_prev, bfm(d));
+  pb::launch_dgrad(g, as_stream(stream));
+  PB_GUARD_END
+}
+
+int pb_conv_bwd_dw_sgd(void* stream, const uint16_t* dz, int n, int h, int w, int cout,
+                       const uint16_t* x, int cin, const float* w_cur, float* w_new,
+                       int ld_w32, uint16_t* w16, int ld_w16, float lr) {
+  PB_GUARD_BEGIN
+  const int pixels = n * h * w;
+  int lds = 0;
+  const size_t floats = pb::wgrad_partial_floats(cout, 9 * cin, pixels, &lds);
+  float* ws = nullptr;
+  cudaStream_t st = as_stream(stream);
+  PB_CUDA(cudaMallocAsync(&ws, floats * 4, st));
+  int S = 0;
+  pb::Mat16 mdz{bf(dz), pixels, cout, cout};
+  pb::GemmLaunch g = pb::plan_conv_wgrad_partial(mdz, pb::Nhwc{bf(x), n, h, w, cin}, 0, ws, lds, &S);
+  pb::launch_wgrad_partial(g, st);
+  pb::launch_reduce_sgd(st, ws, S, static_cast<long long>(cout) * lds, cout, 9 * cin, lds, w_cur,
+                        w_new, ld_w32, bfm(w16), ld_w16, lr);
+  PB_CUDA(cudaFreeAsync(ws, st));
+  PB_GUARD_END
+}
+
+int pb_maxpool2_fwd(void* stream, const uint16_t* in, int n, int h, int w, int c,
+                    uint16_t* out) {
+  PB_GUARD_BEGIN
+  pb::launch_maxpool2_fwd(as_stream(stream), bf(in), n, h, w, c, bfm(out));
+  PB_GUARD_END
+}
+
+int pb_maxpool2_bwd(void* stream, const uint16_t* d_out, const uint16_t* in,
+                    const uint16_t* out, int n, int h, int w, int c, uint16_t* d_in) {
+  PB_GUARD_BEGIN
+  pb::launch_maxpool2_bwd(as_stream(stream), bf(d_out), bf(in), bf(out), n, h, w, c, bfm(d_in));
+  PB_GUARD_END
+}
+
+int pb_im2col_first(void* stream, const uint16_t* x, int ld_x, int n, int h, int w, int c,
+                    uint16_t* out, int ldo) {
+  PB_GUARD_BEGIN
+  pb::launch_im2col_first(as_stream(stream), bf(x), ld_x, n, h, w, c, bfm(out), ldo);
   PB_GUARD_END
 }
 

@@ -1,0 +1,157 @@
+// Convolution-stage kernels of the VGG-style pipeline (BASELINE configs[3],
+// SURVEY §8(f)#4).  The reference has no convolution; these
+// extend its Linear stage math to 3x3 / pad 1 convolutions and 2x2 max
+// pooling on NHWC bf16 activations.  The conv GEMMs themselves are the
+// tcgen05 pair kernel with im2col TMA operands (gemm_sm100.cuh, conv modes);
+// this file holds the memory-bound pieces around them:
+//   * im2col of the network input (3 channels: too narrow for a 64-channel
+//     im2col TMA box), K padded with zeros to the operand's leading dimension;
+//   * 2x2 max pooling forward / backward (the gradient goes to the first
+//     maximum of each window, in (0,0) (0,1) (1,0) (1,1) order);
+//   * the in-order reduction of the conv wgrad's split-K fp32 partial slabs
+//     fused with the SGD update and the bf16 copy of the new version.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "conv_ops.cuh"
+#include "status.hpp"
+
+namespace pb {
+namespace {
+
+int blocks_for(size_t n, int threads = 256) {
+  size_t g = (n + threads - 1) / threads;
+  return static_cast<int>(std::min<size_t>(std::max<size_t>(g, 1), 148 * 32));
+}
+
+// out[(n*H + h)*W + w][k], k = (3r + s) * C + c; zero outside the image and
+// for k >= 9C
+__global__ void im2col_first_kernel(const __nv_bfloat16* __restrict__ x, int ld_x, int n_imgs,
+                                    int H, int W, int C, __nv_bfloat16* __restrict__ out,
+                                    int ldo) {
+  const size_t total = static_cast<size_t>(n_imgs) * H * W * ldo;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % ldo);
+    const size_t p = i / ldo;
+    const int w = static_cast<int>(p % W);
+    const int h = static_cast<int>((p / W) % H);
+    const size_t n = p / (static_cast<size_t>(W) * H);
+    __nv_bfloat16 v = __float2bfloat16(0.f);
+    if (k < 9 * C) {
+      const int tap = k / C, c = k - tap * C;
+      const int ih = h + tap / 3 - 1, iw = w + tap % 3 - 1;
+      if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+        v = x[n * ld_x + (static_cast<size_t>(ih) * W + iw) * C + c];
+    }
+    out[i] = v;
+  }
+}
+
+// 8 channels (16 bytes) per thread
+__global__ void maxpool2_fwd_kernel(const __nv_bfloat16* __restrict__ in, int n_imgs, int H,
+                                    int W, int C, __nv_bfloat16* __restrict__ out) {
+  const int Ho = H / 2, Wo = W / 2, C8 = C / 8;
+  const size_t total = static_cast<size_t>(n_imgs) * Ho * Wo * C8;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c8 = static_cast<int>(i % C8);
+    const size_t p = i / C8;
+    const int wo = static_cast<int>(p % Wo), ho = static_cast<int>((p / Wo) % Ho);
+    const size_t n = p / (static_cast<size_t>(Wo) * Ho);
+    const __nv_bfloat16* base = in + ((n * H + 2 * ho) * W + 2 * wo) * C + 8 * c8;
+    uint4 q[4];
+    q[0] = *reinterpret_cast<const uint4*>(base);
+    q[1] = *reinterpret_cast<const uint4*>(base + C);
+    q[2] = *reinterpret_cast<const uint4*>(base + static_cast<size_t>(W) * C);
+    q[3] = *reinterpret_cast<const uint4*>(base + static_cast<size_t>(W) * C + C);
+    const __nv_bfloat162* v[4];
+    for (int j = 0; j < 4; ++j) v[j] = reinterpret_cast<const __nv_bfloat162*>(&q[j]);
+    uint4 r;
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = __hmax2(__hmax2(v[0][e], v[1][e]), __hmax2(v[2][e], v[3][e]));
+    *reinterpret_cast<uint4*>(out + p * C + 8 * c8) = r;
+  }
+}
+
+__global__ void maxpool2_bwd_kernel(const __nv_bfloat16* __restrict__ d_out,
+                                    const __nv_bfloat16* __restrict__ in,
+                                    const __nv_bfloat16* __restrict__ out, int n_imgs, int H,
+                                    int W, int C, __nv_bfloat16* __restrict__ d_in) {
+  const int Ho = H / 2, Wo = W / 2;
+  const size_t total = static_cast<size_t>(n_imgs) * Ho * Wo * C;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % C);
+    const size_t p = i / C;
+    const int wo = static_cast<int>(p % Wo), ho = static_cast<int>((p / Wo) % Ho);
+    const size_t n = p / (static_cast<size_t>(Wo) * Ho);
+    const float m = __bfloat162float(out[i]);
+    const float g = __bfloat162float(d_out[i]);
+    bool taken = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const size_t a = ((n * H + 2 * ho + (j >> 1)) * W + 2 * wo + (j & 1)) * C + c;
+      const bool hit = !taken && __bfloat162float(in[a]) == m;
+      taken |= hit;
+      d_in[a] = __float2bfloat16(hit ? g : 0.f);
+    }
+  }
+}
+
+// w_new = w_cur - lr * sum_{s < S} slab_s (in split order); w16 = bf16(w_new)
+__global__ void reduce_sgd_kernel(const float* __restrict__ slabs, int S, long long slab,
+                                  int rows, int cols, int lds, const float* __restrict__ w_cur,
+                                  float* __restrict__ w_new, int ldw,
+                                  __nv_bfloat16* __restrict__ w16, int ld16, float lr) {
+  const size_t total = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    const float* p = slabs + r * lds + c;
+    float g = 0.f;
+    for (int s = 0; s < S; ++s) g += p[static_cast<size_t>(s) * slab];
+    const float w = w_cur[r * ldw + c] - lr * g;
+    w_new[r * ldw + c] = w;
+    if (w16) w16[r * ld16 + c] = __float2bfloat16(w);
+  }
+}
+
+}  // namespace
+
+void launch_im2col_first(cudaStream_t st, const __nv_bfloat16* x, int ld_x, int n_imgs, int H,
+                         int W, int C, __nv_bfloat16* out, int ldo) {
+  const size_t total = static_cast<size_t>(n_imgs) * H * W * ldo;
+  im2col_first_kernel<<<blocks_for(total), 256, 0, st>>>(x, ld_x, n_imgs, H, W, C, out, ldo);
+  PB_CUDA(cudaGetLastError());
+}
+
+void launch_maxpool2_fwd(cudaStream_t st, const __nv_bfloat16* in, int n_imgs, int H, int W,
+                         int C, __nv_bfloat16* out) {
+  if (C % 8 != 0 || H % 2 != 0 || W % 2 != 0)
+    throw std::invalid_argument("maxpool2: C % 8 and even H, W required");
+  const size_t total = static_cast<size_t>(n_imgs) * (H / 2) * (W / 2) * (C / 8);
+  maxpool2_fwd_kernel<<<blocks_for(total), 256, 0, st>>>(in, n_imgs, H, W, C, out);
+  PB_CUDA(cudaGetLastError());
+}
+
+void launch_maxpool2_bwd(cudaStream_t st, const __nv_bfloat16* d_out, const __nv_bfloat16* in,
+                         const __nv_bfloat16* out, int n_imgs, int H, int W, int C,
+                         __nv_bfloat16* d_in) {
+  const size_t total = static_cast<size_t>(n_imgs) * (H / 2) * (W / 2) * C;
+  maxpool2_bwd_kernel<<<blocks_for(total), 256, 0, st>>>(d_out, in, out, n_imgs, H, W, C, d_in);
+  PB_CUDA(cudaGetLastError());
+}
+
+void launch_reduce_sgd(cudaStream_t st, const float* slabs, int S, long long slab, int rows,
+                       int cols, int lds, const float* w_cur, float* w_new, int ldw,
+                       __nv_bfloat16* w16, int ld16, float lr) {
+  const size_t total = static_cast<size_t>(rows) * cols;
+  reduce_sgd_kernel<<<blocks_for(total), 256, 0, st>>>(slabs, S, slab, rows, cols, lds, w_cur,
+                                                       w_new, ldw, w16, ld16, lr);
+  PB_CUDA(cudaGetLastError());
+}
+
+}  // namespace pb

@@ -809,6 +809,19 @@ __global__ void __launch_bounds__(128, 1)
       if constexpr (!B_MN) {
         ptx::tma_load_2d(b_dst, &tmap_b, &full_bar[s], k0 + sh.b_k_off,
                          n0 + sh.b_mn_off);
+      } else if (sh.conv == 2) {
+        // implicit-GEMM conv wgrad: B = im2col(x), 64 pixels x 64 channels
+        // of tap n / C per 64 output columns
+        const int hw = sh.conv_h * sh.conv_w;
+        const int p = k0 + sh.b_k_off;
+        const int pn = p / hw, ph = (p - pn * hw) / sh.conv_w, pw = p - pn * hw - ph * sh.conv_w;
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h) {
+          const int n = n0 + h * 64;
+          const int tap = n / sh.conv_c, c0 = n - tap * sh.conv_c;
+          ptx::tma_load_im2col(b_dst + h * 8192, &tmap_b, &full_bar[s], c0, pw - 1, ph - 1, pn,
+                               tap % 3, tap / 3);
+        }
       } else {
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h)
@@ -856,7 +869,13 @@ __global__ void __launch_bounds__(128, 1)
   }
   // the operand ring is idle now: reuse it for the per-warp transpose blocks
   float* T = reinterpret_cast<float*>(sA) + warp * 32 * kVecLd;
-  if (ep.dbg_skip & 1) {
+  if (ep.partial_slab) {
+    // split-K into partial slabs: this split's own fp32 slab, plain store
+    EpiParams epp = ep;
+    epp.y32 = ep.y32 + static_cast<size_t>(split) * ep.partial_slab;
+    if constexpr (EPI == kEpiFwd)
+      epilogue_warp_vec<EPI, kLinear>(epp, sh, m0 + warp * 32, n0, BN, t_row, T);
+  } else if (ep.dbg_skip & 1) {
   } else if (EPI == kEpiFwd && sh.splits > 1) {
     static_assert(SplitSmem<BN>::kBytes <= S * Cfg::kStageBytes, "partial must fit the ring");
     float* part = reinterpret_cast<float*>(sA);
@@ -1156,6 +1175,52 @@ struct Gemm2Cfg {
   static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
+// Operand loads of one k-block of an implicit-GEMM 3x3 convolution (pad 1,
+// stride 1, NHWC; GemmShape::conv).  K is tap-major: k = tap * C + channel,
+// tap = 3 * r + s, so a 64-wide k-block is one tap and 64 channels.
+// Forward / dgrad: A (128 output pixels x 64 channels) comes straight from
+// the activation by an im2col TMA load -- the patch matrix is never built.
+template <class Cfg>
+__device__ __forceinline__ void conv_loads_fd(const GemmShape& sh, const CUtensorMap* ta,
+                                              const CUtensorMap* tb, uint32_t fb, uint8_t* a_dst,
+                                              uint8_t* b_dst, int k0, int n_tile, uint32_t rank,
+                                              int px_n, int px_h, int px_w) {
+  // dgrad: dX[h,w] = sum_rs dz[h+1-r, w+1-s] W[r,s]; the k-block's tap t
+  // reads dz at window offset t and pairs it with the weights of tap 8 - t
+  const int tap = k0 / sh.conv_c, c0 = k0 - tap * sh.conv_c;
+  ptx::tma_load_im2col_pair(a_dst, ta, fb, c0, px_w - 1, px_h - 1, px_n, tap % 3, tap / 3);
+#pragma unroll
+  for (int j = 0; j < Cfg::kSub; ++j) {
+    const int nbj = n_tile + j * Cfg::kMmaN + static_cast<int>(rank) * (Cfg::kMmaN / 2);
+    uint8_t* bj = b_dst + j * Cfg::kBSub;
+    if (sh.conv == 1) {
+      ptx::tma_load_2d_pair(bj, tb, fb, k0, nbj);  // W [Cout, 9C], K-major
+    } else {
+      // W viewed [Cout][9][Cin]: 64 output channels (K) x 64 input channels
+      // (N) of the flipped tap, MN-major
+#pragma unroll
+      for (int h = 0; h < Cfg::kMmaN / 128; ++h)
+        ptx::tma_load_3d_pair(bj + h * 8192, tb, fb, nbj + h * 64, 8 - tap, c0);
+    }
+  }
+}
+
+// wgrad: B = im2col(x), 64 pixels (K) x 64 channels of tap n / C (N) for
+// every 64 output columns, MN-major.
+template <class Cfg>
+__device__ __forceinline__ void conv_wgrad_b(const GemmShape& sh, const CUtensorMap* tb,
+                                             uint32_t fb, uint8_t* bj, int k0, int nbj) {
+  const int hw = sh.conv_h * sh.conv_w;
+  const int p = k0 + sh.b_k_off;
+  const int pn = p / hw, ph = (p - pn * hw) / sh.conv_w, pw = p - pn * hw - ph * sh.conv_w;
+#pragma unroll
+  for (int h = 0; h < Cfg::kMmaN / 128; ++h) {
+    const int n = nbj + h * 64;
+    const int tap = n / sh.conv_c, c0 = n - tap * sh.conv_c;
+    ptx::tma_load_im2col_pair(bj + h * 8192, tb, fb, c0, pw - 1, ph - 1, pn, tap % 3, tap / 3);
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a,
@@ -1233,6 +1298,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
         const int tm = tile / tiles_n, tn = tile % tiles_n;
         const int m0 = tm * 256 + static_cast<int>(rank) * 128;
         const int kb_lo = split * kbps, kb_hi = min(kb_all, kb_lo + kbps);
+        // implicit-GEMM conv, A = im2col: this CTA's first output pixel
+        int px_n = 0, px_h = 0, px_w = 0;
+        if (sh.conv == 1 || sh.conv == 3) {
+          const int hw = sh.conv_h * sh.conv_w;
+          const int p = m0 + sh.a_mn_off;
+          px_n = p / hw;
+          px_h = (p - px_n * hw) / sh.conv_w;
+          px_w = p - px_n * hw - px_h * sh.conv_w;
+        }
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
           const int s = it % S;
           if (it >= S) ptx::mbar_wait(&empty_bar[s], ((it / S) - 1) & 1);
@@ -1241,6 +1315,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
           const int k0 = kb * Cfg::kBK;
           uint8_t* a_dst = sA + s * Cfg::kAHalf;
           uint8_t* b_dst = sB + s * Cfg::kBHalf;
+          if (sh.conv == 1 || sh.conv == 3) {
+            conv_loads_fd<Cfg>(sh, &tmap_a, &tmap_b, fb, a_dst, b_dst, k0, tn * BN, rank, px_n,
+                               px_h, px_w);
+            continue;
+          }
           if constexpr (!A_MN) {
             ptx::tma_load_2d_pair(a_dst, &tmap_a, fb, k0 + sh.a_k_off, m0 + sh.a_mn_off);
           } else {
@@ -1254,6 +1333,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             // MMA j of the k-block: this CTA's B rows of N block j
             const int nbj = tn * BN + j * Cfg::kMmaN + static_cast<int>(rank) * (Cfg::kMmaN / 2);
             uint8_t* bj = b_dst + j * Cfg::kBSub;
+            if (B_MN && sh.conv == 2) {
+              conv_wgrad_b<Cfg>(sh, &tmap_b, fb, bj, k0, nbj);
+              continue;
+            }
             if constexpr (!B_MN) {
               ptx::tma_load_2d_pair(bj, &tmap_b, fb, k0 + sh.b_k_off, nbj + sh.b_mn_off);
             } else {

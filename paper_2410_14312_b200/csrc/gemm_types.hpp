@@ -19,6 +19,15 @@ struct GemmShape {
   // chunks of kb_per_split 64-wide k-blocks, one CTA of a (1,1,splits)
   // cluster each (0/1 = no split); see gemm_sm100.cuh.
   int splits, kb_per_split;
+  // Implicit-GEMM 3x3 convolution (pad 1, stride 1, NHWC bf16; pair kernel):
+  //  1 forward: A = im2col(x) [pixels, 9*C] (tap-major K), B = W [Cout, 9*C]
+  //  3 dgrad:   A = im2col(dz) with the taps flipped [pixels, 9*C],
+  //             B = W viewed [Cout][9][Cin] (3-D map, MN-major)
+  //  2 wgrad:   A = dz [pixels, Cout] (MN-major), B = im2col(x) (MN-major,
+  //             64-pixel columns)
+  // conv_h / conv_w: image size; conv_c: channels of the im2col'd tensor.
+  // a_mn_off (modes 1, 3) / b_k_off (mode 2) are pixel offsets.
+  int conv = 0, conv_h = 0, conv_w = 0, conv_c = 0;
 };
 
 // Tensor maps of the TMA epilogue of wgrad+SGD (EpiParams::rowwise == 3).
@@ -71,6 +80,10 @@ struct EpiParams {
   int split_master;
   // timing experiments: nonzero skips the epilogue's global traffic
   int dbg_skip;
+  // split-K into fp32 partial slabs (single-CTA kernel, forward epilogue
+  // without bias / activation): split z writes y32 + z * partial_slab; a
+  // separate in-order reduction consumes them (conv wgrad, conv_ops.cu)
+  long long partial_slab;
 };
 
 }  // namespace pb

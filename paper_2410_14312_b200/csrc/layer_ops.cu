@@ -9,6 +9,7 @@
 
 #include "gemm_sm100.cuh"
 #include "layer_ops.cuh"
+#include "conv_ops.cuh"
 #include "status.hpp"
 
 namespace pb {
@@ -132,7 +133,7 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     constexpr int smem = GemmCfg<BN>::kSmem;
     const int splits = std::max(1, g.sh.splits);
     dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128, splits);
-    if (splits > 1) {  // the splits of a tile are one cluster (DSMEM reduction)
+    if (splits > 1 && !g.ep.partial_slab) {  // the splits of a tile are one cluster (DSMEM reduction)
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = grid;
       cfg.blockDim = dim3(128);
@@ -187,6 +188,9 @@ void init_gemm_attributes() {
     set_attr<256, false, true, kEpiDgrad>();
     set_attr<128, true, true, kEpiWgradSgd>();
     set_attr<256, true, true, kEpiWgradSgd>();
+    // conv wgrad: split-K partial slabs (single-CTA, MN / MN operands)
+    set_attr<128, true, true, kEpiFwd>();
+    set_attr<256, true, true, kEpiFwd>();
   });
 }
 
@@ -522,6 +526,177 @@ void launch_join_master(cudaStream_t st, const __nv_bfloat16* hi, const uint16_t
                         int cols, int ld, float* w, int ld_w) {
   join_master_kernel<<<conv_grid(rows, cols), 256, 0, st>>>(hi, lo, rows, cols, ld, w, ld_w);
   PB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ conv plans
+namespace {
+PFN_cuTensorMapEncodeIm2col_v12000 im2col_encode_fn() {
+  static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    PB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw cuda_failure("cuTensorMapEncodeIm2col entry point unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+  });
+  return fn;
+}
+
+// im2col view of an NHWC tensor for 3x3 / pad 1 / stride 1: the window of
+// output pixel (h, w) starts at input (h - 1, w - 1); the bounding box of
+// start positions is [-1, H - 2] x [-1, W - 2] (corners -1 / -1), so the
+// pixels walked are exactly the output pixels, image after image.
+CUtensorMap make_im2col_tmap(const Nhwc& t, int pixels_per_column) {
+  if (t.c % 64 != 0) throw std::invalid_argument("im2col operand: channels must be a multiple of 64");
+  if ((reinterpret_cast<uintptr_t>(t.ptr) & 15) != 0)
+    throw std::invalid_argument("im2col operand must be 16-byte aligned");
+  CUtensorMap map;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(t.c), static_cast<cuuint64_t>(t.w),
+                        static_cast<cuuint64_t>(t.h), static_cast<cuuint64_t>(t.n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(t.c) * 2,
+                           static_cast<cuuint64_t>(t.c) * 2 * t.w,
+                           static_cast<cuuint64_t>(t.c) * 2 * t.w * t.h};
+  int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = im2col_encode_fn()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(static_cast<const void*>(t.ptr)),
+      dims, strides, lower, upper, 64, static_cast<cuuint32_t>(pixels_per_column), estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeIm2col failed (code " + std::to_string(static_cast<int>(r)) +
+                       ")");
+  return map;
+}
+
+// conv weights [Cout][ld] viewed as [Cout][9][Cin]: box 64 Cin x 1 tap x 64 Cout
+CUtensorMap make_w3d_tmap(const __nv_bfloat16* w, int cout, int cin, int ld) {
+  if (cin % 64 != 0 || ld % 8 != 0) throw std::invalid_argument("conv weights: Cin % 64, ld % 8");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin), 9, static_cast<cuuint64_t>(cout)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[3] = {64, 1, 64};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                           const_cast<void*>(static_cast<const void*>(w)), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeTiled (3-D) failed (code " +
+                       std::to_string(static_cast<int>(r)) + ")");
+  return map;
+}
+
+// split count of a partial-slab wgrad: about two waves of 128 x bn tiles
+int partial_splits(int M, int N, int K, int bn, int* kbps) {
+  const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int kb = (K + 63) / 64;
+  int S = std::max(1, std::min(kb, (2 * sm_count() + tiles - 1) / tiles));
+  *kbps = (kb + S - 1) / S;
+  return (kb + *kbps - 1) / *kbps;
+}
+}  // namespace
+
+GemmLaunch plan_conv_fwd(const Nhwc& x, int img0, int imgs, const Mat16& w, const float* bias,
+                         int act, __nv_bfloat16* y16, int y_row_off) {
+  const int hw = x.h * x.w;
+  GemmLaunch g;
+  g.pair = true;
+  g.bn = w.rows > 128 ? 256 : 128;
+  g.ta = make_im2col_tmap(x, 128);
+  g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
+  g.sh = GemmShape{imgs * hw, w.rows, 9 * x.c, img0 * hw, 0, 0, 0, 1, 0};
+  g.sh.conv = 1;
+  g.sh.conv_h = x.h;
+  g.sh.conv_w = x.w;
+  g.sh.conv_c = x.c;
+  g.ep = empty_epi(kEpiFwd);
+  g.ep.bias = bias;
+  g.ep.act = act;
+  g.ep.y16 = y16;
+  g.ep.ld_y16 = w.rows;
+  g.ep.y_row_off = y_row_off;
+  vec_or_fallback(g.ep, kEpiFwd);
+  return g;
+}
+
+GemmLaunch plan_conv_dgrad(const Nhwc& dz, const __nv_bfloat16* w, int cin, int ld_w,
+                           const __nv_bfloat16* xin, int act_prev, __nv_bfloat16* d) {
+  GemmLaunch g;
+  g.pair = true;
+  g.bn = cin > 128 ? 256 : 128;
+  g.ta = make_im2col_tmap(dz, 128);
+  g.tb = make_w3d_tmap(w, dz.c, cin, ld_w);
+  g.sh = GemmShape{dz.n * dz.h * dz.w, cin, 9 * dz.c, 0, 0, 0, 0, 1, 0};
+  g.sh.conv = 3;
+  g.sh.conv_h = dz.h;
+  g.sh.conv_w = dz.w;
+  g.sh.conv_c = dz.c;
+  g.ep = empty_epi(kEpiDgrad);
+  g.ep.xin = xin;
+  g.ep.ld_xin = cin;
+  g.ep.act_prev = act_prev;
+  g.ep.d16 = d;
+  g.ep.ld_d16 = cin;
+  vec_or_fallback(g.ep, kEpiDgrad);
+  return g;
+}
+
+size_t wgrad_partial_floats(int M, int N, int K, int* lds) {
+  const int bn = N >= 256 ? 256 : 128;
+  int kbps = 0;
+  const int S = partial_splits(M, N, K, bn, &kbps);
+  *lds = (N + 7) / 8 * 8;
+  return static_cast<size_t>(S) * M * *lds;
+}
+
+namespace {
+GemmLaunch partial_common(const Mat16& dz, int N, float* ws, int lds, int* splits) {
+  GemmLaunch g;
+  const int M = dz.cols, K = dz.rows;
+  g.pair = false;
+  g.bn = N >= 256 ? 256 : 128;
+  int kbps = 0;
+  const int S = partial_splits(M, N, K, g.bn, &kbps);
+  *splits = S;
+  g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
+  g.sh = GemmShape{M, N, K, 0, 0, 0, 0, S, kbps};
+  g.ep = empty_epi(kEpiFwd);
+  g.ep.act = kLinear;
+  g.ep.y32 = ws;
+  g.ep.ld_y32 = lds;
+  g.ep.partial_slab = static_cast<long long>(M) * lds;
+  g.ep.rowwise = 2;
+  if (lds % 4 != 0 || !al(ws, 16)) throw std::invalid_argument("partial slabs: 16-byte rows");
+  return g;
+}
+}  // namespace
+
+GemmLaunch plan_conv_wgrad_partial(const Mat16& dz, const Nhwc& x, int img0, float* ws, int lds,
+                                   int* splits) {
+  GemmLaunch g = partial_common(dz, 9 * x.c, ws, lds, splits);
+  g.tb = make_im2col_tmap(x, 64);
+  g.sh.b_k_off = img0 * x.h * x.w;
+  g.sh.conv = 2;
+  g.sh.conv_h = x.h;
+  g.sh.conv_w = x.w;
+  g.sh.conv_c = x.c;
+  return g;
+}
+
+GemmLaunch plan_wgrad_partial(const Mat16& dz, const Mat16& x, float* ws, int lds, int* splits) {
+  GemmLaunch g = partial_common(dz, x.cols, ws, lds, splits);
+  g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
+  return g;
+}
+
+void launch_wgrad_partial(const GemmLaunch& g, cudaStream_t st) {
+  if (g.bn == 256)
+    launch_one<256, true, true, kEpiFwd>(g, st);
+  else
+    launch_one<128, true, true, kEpiFwd>(g, st);
 }
 
 void launch_fwd(const GemmLaunch& g, cudaStream_t st) {

@@ -263,6 +263,44 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// 2-CTA 3-D tiled load (conv dgrad weights viewed as [Cout][9][Cin]).
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::"
+      "complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// Single-CTA im2col load (see tma_load_im2col_pair).
+__device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c, int w, int h, int n, int w_off,
+                                                int h_off) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(static_cast<uint16_t>(w_off)), "h"(static_cast<uint16_t>(h_off))
+      : "memory");
+}
+
+// 2-CTA im2col load of an NHWC activation (implicit-GEMM conv operand):
+// pixelsPerColumn consecutive output pixels x channelsPerPixel channels,
+// starting at input position {c, w, h, n} (the first pixel's window corner)
+// shifted by the filter tap {w_off, h_off}; out-of-image taps read zeros.
+// (Coordinate convention pinned on sm_100a by tools/im2col_probe.cu.)
+__device__ __forceinline__ void tma_load_im2col_pair(void* dst, const CUtensorMap* map,
+                                                     uint32_t bar_cluster, int c, int w, int h,
+                                                     int n, int w_off, int h_off) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::"
+      "complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(static_cast<uint16_t>(w_off)), "h"(static_cast<uint16_t>(h_off))
+      : "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {
   asm volatile(

@@ -122,3 +122,47 @@ def graph_time_us(fns, reps: int = 60) -> float:
     e1.record(st)
     e1.synchronize()
     return e0.elapsed_time(e1) * 1000.0 / reps
+
+
+# ---------------------------------------------------------------- conv stages
+# NHWC bf16 activations as torch [n, h, w, c] contiguous tensors; conv weights
+# [cout, 9 * cin] (tap-major K, k = (3r + s) * cin + c).
+
+def conv_fwd(x, w, bias, act, y):
+    n, h, ww, cin = x.shape
+    cout = w.shape[0]
+    _native.check(_native.lib().pb_conv_fwd(
+        _stream(), _ptr(x), n, h, ww, cin, _ptr(w), cout, _ld(w), _ptr(bias), ACT[act], _ptr(y)))
+
+
+def conv_bwd_dx(dz, w, xin, act_prev, d):
+    n, h, ww, cout = dz.shape
+    cin = d.shape[-1]
+    _native.check(_native.lib().pb_conv_bwd_dx(
+        _stream(), _ptr(dz), n, h, ww, cout, _ptr(w), cin, _ld(w), _ptr(xin), ACT[act_prev],
+        _ptr(d)))
+
+
+def conv_bwd_dw_sgd(dz, x, w_cur, w_new, w16, lr):
+    n, h, ww, cout = dz.shape
+    cin = x.shape[-1]
+    _native.check(_native.lib().pb_conv_bwd_dw_sgd(
+        _stream(), _ptr(dz), n, h, ww, cout, _ptr(x), cin, _ptr(w_cur), _ptr(w_new),
+        _ld(w_cur), _ptr(w16), _ld(w16) if w16 is not None else 0, float(lr)))
+
+
+def maxpool2_fwd(x, y):
+    n, h, ww, c = x.shape
+    _native.check(_native.lib().pb_maxpool2_fwd(_stream(), _ptr(x), n, h, ww, c, _ptr(y)))
+
+
+def maxpool2_bwd(d_out, x, y, d_in):
+    n, h, ww, c = x.shape
+    _native.check(_native.lib().pb_maxpool2_bwd(_stream(), _ptr(d_out), _ptr(x), _ptr(y), n, h,
+                                                ww, c, _ptr(d_in)))
+
+
+def im2col_first(x, out):
+    n, h, ww, c = x.shape
+    _native.check(_native.lib().pb_im2col_first(_stream(), _ptr(x), h * ww * c, n, h, ww, c,
+                                                _ptr(out), _ld(out)))
