@@ -411,6 +411,40 @@ int pb_session_ipc_connect(pb_session* s, const uint8_t* blobs, const int64_t* l
  * and shares them (e.g. torch.distributed broadcast). */
 int pb_nccl_unique_id(uint8_t* out128);
 
+/* ---- convolutional networks (VGG-style stages, BASELINE configs[3]; the
+ * reference's networks are MLPs only, so this is an extension
+ * of pb_session_create with the same session entry points afterwards).
+ * A network is conv layers then linear layers; the first linear layer reads
+ * the last conv output flattened in NHWC order.  conv3x3: `in` -> `out`
+ * channels on height x width NHWC images, pad 1, stride 1, activation, then
+ * (pool != 0) 2x2 / stride-2 max pooling; weights [out][9*in] with
+ * k = (3r + s) * in + c, then b[out].  Input rows are NHWC images
+ * (height*width*in values).  Channel counts: out % 64 == 0; in % 64 == 0
+ * except a first layer with in <= 8. */
+enum { PB_LAYER_LINEAR = 0, PB_LAYER_CONV3X3 = 1 };
+typedef struct {
+  int kind;           /* PB_LAYER_* */
+  int in, out;        /* features (linear) or channels (conv) */
+  int height, width;  /* conv: input image size */
+  int pool;           /* conv: 2x2 max pooling after the activation */
+  int act;            /* PB_ACT_* */
+} pb_layer_spec;
+typedef struct {
+  int n_layers;
+  const pb_layer_spec* layers;
+  int loss;                 /* PB_LOSS_* */
+  const int* stage_layers;  /* [workers] layers per stage, or NULL: the
+                               flop-balanced partition (pb_partition_layers) */
+} pb_layer_net;
+/* Contiguous partition minimising the largest stage's forward flops. */
+int pb_partition_layers(const pb_layer_net* net, int workers, int* first_layer,
+                        int* n_layers);
+/* A session for a layer network (rank / world / nccl_ids as
+ * pb_session_create_dist; world 1 = every stage in this process). */
+int pb_session_create_layers(const pb_layer_net* net, const pb_train_config* cfg,
+                             int rank, int world, const uint8_t* nccl_ids,
+                             size_t ids_bytes, pb_session** out);
+
 /* pb_session_create for one rank of a world-size pipeline. */
 int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg,
                            int rank, int world, const uint8_t* nccl_ids,

@@ -493,14 +493,34 @@ class Net:
         self.loss = LOSSES[loss] if isinstance(loss, (int, np.integer)) else loss
 
 
-def train_epoch(net, W, N, B, M, lr, x, y, params, mode="timeprest", observe=False):
+def train_epoch(net, W, N, B, M, lr, x, y, params, mode="timeprest", observe=False,
+                layer_math=None):
     """train_epoch (trainer.cpp:642-660) → replay_grid (:388-508) or
     sequential_epoch (:510-553).  `params` is the whole-network flat vector
-    (current versions).  Returns dict(params, losses, pinned, consumed, held)."""
+    (current versions).  Returns dict(params, losses, pinned, consumed, held).
+
+    layer_math (optional) replaces the Linear stage math for other layer
+    kinds (oracle/convnet_ref.py): an object with `layers` (per stage),
+    `sizes` (per-stage parameter counts), `forward(layers, params, x)` and
+    `backward(layers, prop, cache, delta)` with stage_forward /
+    stage_backward's contracts; the replay itself is unchanged."""
+    global stage_forward, stage_backward
+    if layer_math is not None:
+        saved = (stage_forward, stage_backward)
+        stage_forward, stage_backward = layer_math.forward, layer_math.backward
+        try:
+            return _train_epoch(net, W, N, B, M, lr, x, y, params, mode, observe,
+                                layer_math.sizes, layer_math.layers)
+        finally:
+            stage_forward, stage_backward = saved
     parts = partition_model(net.widths, W)
     sizes = [sum(net.widths[l] * net.widths[l + 1] + net.widths[l + 1]
                  for l in range(f, f + c)) for f, c in parts]
     layers = [_layers(net.widths, net.acts, f, c) for f, c in parts]
+    return _train_epoch(net, W, N, B, M, lr, x, y, params, mode, observe, sizes, layers)
+
+
+def _train_epoch(net, W, N, B, M, lr, x, y, params, mode, observe, sizes, layers):
     offs = np.cumsum([0] + sizes)
     stores = [{0: params[offs[s]:offs[s + 1]].copy()} for s in range(W)]
     current = [0] * W

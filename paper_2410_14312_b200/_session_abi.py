@@ -39,6 +39,16 @@ class pb_session_info(C.Structure):
                 ("stage_layers", C.POINTER(C.c_int))]
 
 
+class pb_layer_spec(C.Structure):
+    _fields_ = [("kind", C.c_int), ("in_", C.c_int), ("out", C.c_int), ("height", C.c_int),
+                ("width", C.c_int), ("pool", C.c_int), ("act", C.c_int)]
+
+
+class pb_layer_net(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("layers", C.POINTER(pb_layer_spec)),
+                ("loss", C.c_int), ("stage_layers", C.POINTER(C.c_int))]
+
+
 def signatures():
     from ._native import pb_net_spec
     i, p, i64, u64 = C.c_int, C.c_void_p, C.c_int64, C.c_uint64
@@ -46,6 +56,9 @@ def signatures():
     return {
         "pb_session_create": (i, [P(pb_net_spec), P(pb_train_config), P(p)]),
         "pb_session_destroy": (i, [p]),
+        "pb_session_create_layers": (i, [P(pb_layer_net), P(pb_train_config), i, i, C.c_char_p,
+                                         C.c_size_t, P(p)]),
+        "pb_partition_layers": (i, [P(pb_layer_net), i, P(i), P(i)]),
         "pb_session_info_get": (i, [p, P(pb_session_info)]),
         "pb_session_load_params": (i, [p, P(C.c_double), i64]),
         "pb_session_load_stage_params": (i, [p, i, P(C.c_double), i64]),

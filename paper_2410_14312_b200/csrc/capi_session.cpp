@@ -118,6 +118,71 @@ int pb_session_create_dist(const pb_net_spec* net, const pb_train_config* cfg, i
   PB_GUARD_END
 }
 
+namespace {
+std::vector<pb::LayerSpec> layer_list(const pb_layer_net* net) {
+  if (!net || net->n_layers < 1 || !net->layers) throw std::invalid_argument("empty layer list");
+  std::vector<pb::LayerSpec> v;
+  for (int i = 0; i < net->n_layers; ++i) {
+    const pb_layer_spec& a = net->layers[i];
+    if (a.kind != PB_LAYER_LINEAR && a.kind != PB_LAYER_CONV3X3)
+      throw std::invalid_argument("bad layer kind " + std::to_string(a.kind));
+    pb::LayerSpec l;
+    l.kind = a.kind == PB_LAYER_CONV3X3 ? pb::LayerKind::conv3x3 : pb::LayerKind::linear;
+    l.in = a.in;
+    l.out = a.out;
+    l.h = a.height;
+    l.w = a.width;
+    l.pool = a.pool != 0;
+    l.act = a.act;
+    v.push_back(l);
+  }
+  pb::check_layers(v);
+  return v;
+}
+}  // namespace
+
+int pb_partition_layers(const pb_layer_net* net, int workers, int* first_layer, int* n_layers) {
+  PB_GUARD_BEGIN
+  const std::vector<int> n = pb::partition_by_flops(layer_list(net), workers);
+  for (int s = 0, f = 0; s < workers; ++s) {
+    if (first_layer) first_layer[s] = f;
+    if (n_layers) n_layers[s] = n[s];
+    f += n[s];
+  }
+  PB_GUARD_END
+}
+
+int pb_session_create_layers(const pb_layer_net* net, const pb_train_config* cfg, int rank,
+                             int world, const uint8_t* nccl_ids, size_t ids_bytes,
+                             pb_session** out) {
+  PB_GUARD_BEGIN
+  if (!out || !net || !cfg) throw std::invalid_argument("null argument");
+  pb::SessionConfig c;
+  {
+    // the train-config fields (make_config needs a net spec: a 1-layer stub)
+    const int w[2] = {1, 1}, a[1] = {0};
+    const pb_net_spec stub{1, w, a, net->loss};
+    c = make_config(&stub, cfg);
+  }
+  c.layers = layer_list(net);
+  c.widths.clear();
+  c.acts.clear();
+  c.loss = net->loss;
+  if (net->stage_layers) c.stage_layers.assign(net->stage_layers, net->stage_layers + cfg->workers);
+  c.rank = rank;
+  c.world = world;
+  if (nccl_ids && ids_bytes) c.nccl_ids.assign(nccl_ids, nccl_ids + ids_bytes);
+  auto* s = new pb_session;
+  try {
+    s->impl = std::make_unique<pb::Session>(c);
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  *out = s;
+  PB_GUARD_END
+}
+
 int pb_session_ipc_export(pb_session* s, uint8_t* buf, int64_t cap, int64_t* len) {
   PB_GUARD_BEGIN
   const std::vector<uint8_t> b = S(s).ipc_export();
@@ -230,13 +295,9 @@ int pb_session_info_get(pb_session* s, pb_session_info* info) {
     if (info->pool_sizes) info->pool_sizes[i] = ps[i];
     if (info->act_slots) info->act_slots[i] = as[i];
   }
-  pipesim::network_spec net;
-  net.widths = x.config().widths;
-  for (int a : x.config().acts) net.activations.push_back(static_cast<pipesim::activation_kind>(a));
-  const auto part = pipesim::partition_model(net, x.config().W);
-  for (size_t i = 0; i < part.size(); ++i) {
-    if (info->stage_first_layer) info->stage_first_layer[i] = part[i].first_layer;
-    if (info->stage_layers) info->stage_layers[i] = static_cast<int>(part[i].layers.size());
+  for (int i = 0; i < x.config().W; ++i) {
+    if (info->stage_first_layer) info->stage_first_layer[i] = x.stage_first_layer(i + 1);
+    if (info->stage_layers) info->stage_layers[i] = x.stage_layer_count(i + 1);
   }
   PB_GUARD_END
 }

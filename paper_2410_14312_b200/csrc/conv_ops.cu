@@ -119,7 +119,50 @@ __global__ void reduce_sgd_kernel(const float* __restrict__ slabs, int S, long l
   }
 }
 
+// grid (chunks, cols / 64): 32 row lanes x 8 column groups of 8 (16-byte
+// loads); the 32 lane sums of a column are added in lane order
+__global__ void __launch_bounds__(256)
+    colsum_partial_kernel(const __nv_bfloat16* __restrict__ dz, int rows, int cols, int ld,
+                          int rows_per_chunk, float* __restrict__ partial) {
+  __shared__ float red[32][65];
+  const int cg = threadIdx.x % 8, lane = threadIdx.x / 8;
+  const int c0 = blockIdx.y * 64 + cg * 8;
+  const int r0 = blockIdx.x * rows_per_chunk;
+  const int r1 = min(rows, r0 + rows_per_chunk);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c0 < cols)
+    for (int r = r0 + lane; r < r1; r += 32) {
+      const uint4 q = *reinterpret_cast<const uint4*>(dz + static_cast<size_t>(r) * ld + c0);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[lane][cg * 8 + k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < 64 && blockIdx.y * 64 + threadIdx.x < cols) {
+    float sum = 0.f;
+    for (int i = 0; i < 32; ++i) sum += red[i][threadIdx.x];
+    partial[static_cast<size_t>(blockIdx.x) * cols + blockIdx.y * 64 + threadIdx.x] = sum;
+  }
+}
+
 }  // namespace
+
+void launch_colsum_partial(cudaStream_t st, const __nv_bfloat16* dz, int rows, int cols, int ld,
+                           float* partial) {
+  if (cols % 8 != 0 || ld % 8 != 0 || (reinterpret_cast<uintptr_t>(dz) & 15) != 0)
+    throw std::invalid_argument("colsum: 16-byte rows required");
+  const int chunks = colsum_chunks(rows);
+  const int per = (rows + chunks - 1) / chunks;
+  colsum_partial_kernel<<<dim3(chunks, (cols + 63) / 64), 256, 0, st>>>(dz, rows, cols, ld, per,
+                                                                        partial);
+  PB_CUDA(cudaGetLastError());
+}
 
 void launch_im2col_first(cudaStream_t st, const __nv_bfloat16* x, int ld_x, int n_imgs, int H,
                          int W, int C, __nv_bfloat16* out, int ldo) {

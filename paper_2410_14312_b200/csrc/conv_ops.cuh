@@ -16,6 +16,17 @@ void launch_maxpool2_fwd(cudaStream_t st, const __nv_bfloat16* in, int n_imgs, i
 void launch_maxpool2_bwd(cudaStream_t st, const __nv_bfloat16* d_out, const __nv_bfloat16* in,
                          const __nv_bfloat16* out, int n_imgs, int H, int W, int C,
                          __nv_bfloat16* d_in);
+// Column sums of a tall bf16 matrix (rows x cols, cols % 8 == 0) by row
+// blocks: partial[c * cols + j] = sum of column j over row block c, for
+// c < colsum_chunks(rows) (a fixed split: the bias gradient stays
+// deterministic; launch_bias_sgd then sums the partials in order).
+constexpr int kColsumChunks = 512;
+inline int colsum_chunks(int rows) {
+  const int c = (rows + 1023) / 1024;
+  return c < 1 ? 1 : (c > kColsumChunks ? kColsumChunks : c);
+}
+void launch_colsum_partial(cudaStream_t st, const __nv_bfloat16* dz, int rows, int cols, int ld,
+                           float* partial);
 void launch_reduce_sgd(cudaStream_t st, const float* slabs, int S, long long slab, int rows,
                        int cols, int lds, const float* w_cur, float* w_new, int ldw,
                        __nv_bfloat16* w16, int ld16, float lr);

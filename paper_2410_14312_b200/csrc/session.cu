@@ -1,5 +1,6 @@
 // Session implementation — see session.hpp for the design summary.
 #include "session.hpp"
+#include "conv_ops.cuh"
 #include "digest_dev.hpp"
 #include "host_xfer.hpp"
 
@@ -58,11 +59,81 @@ std::vector<int> colour(const std::vector<std::pair<int, int>>& iv, int* n_colou
 
 }  // namespace
 
+// ------------------------------------------------------------------ conv nets
+void check_layers(const std::vector<LayerSpec>& layers) {
+  bool seen_linear = false;
+  int64_t prev_out = -1;
+  for (size_t i = 0; i < layers.size(); ++i) {
+    const LayerSpec& l = layers[i];
+    const std::string at = "layer " + std::to_string(i) + ": ";
+    if (l.in < 1 || l.out < 1) throw std::invalid_argument(at + "empty layer");
+    if (l.act < 0 || l.act > 3) throw std::invalid_argument(at + "bad activation");
+    if (l.kind == LayerKind::conv3x3) {
+      if (seen_linear) throw std::invalid_argument(at + "conv layers must precede linear layers");
+      if (l.h < 1 || l.w < 1) throw std::invalid_argument(at + "conv needs an image size");
+      if (l.out % 64 != 0) throw std::invalid_argument(at + "conv output channels % 64");
+      if (i == 0 ? (l.in % 64 != 0 && 9 * l.in > 72) : l.in % 64 != 0)
+        throw std::invalid_argument(at + "conv input channels % 64 (first layer: <= 8)");
+      if (l.pool && (l.h % 2 != 0 || l.w % 2 != 0))
+        throw std::invalid_argument(at + "pooling needs an even image size");
+      if (l.pool && l.act != 0 && l.act != 1)
+        throw std::invalid_argument(at + "pooling follows a linear or ReLU activation");
+    } else {
+      seen_linear = true;
+      if (l.pool) throw std::invalid_argument(at + "linear layers do not pool");
+    }
+    if (prev_out >= 0 && l.in_elems() != prev_out)
+      throw std::invalid_argument(at + "input size " + std::to_string(l.in_elems()) +
+                                  " != previous output " + std::to_string(prev_out));
+    prev_out = l.out_elems();
+  }
+  if (layers.empty() || layers.back().kind != LayerKind::linear)
+    throw std::invalid_argument("a conv network ends with a linear layer");
+}
+
+std::vector<int> partition_by_flops(const std::vector<LayerSpec>& layers, int W) {
+  const int L = static_cast<int>(layers.size());
+  if (W < 1 || W > L)
+    throw pipesim::domain_error("workers", "cannot split " + std::to_string(L) +
+                                               " layers into " + std::to_string(W) + " stages");
+  std::vector<double> pre(L + 1, 0.0);
+  for (int i = 0; i < L; ++i) pre[i + 1] = pre[i] + layers[i].flops();
+  const double inf = 1e300;
+  // best[k][i]: smallest max-stage cost of the first i layers in k stages
+  std::vector<std::vector<double>> best(W + 1, std::vector<double>(L + 1, inf));
+  std::vector<std::vector<int>> cut(W + 1, std::vector<int>(L + 1, 0));
+  best[0][0] = 0.0;
+  for (int k = 1; k <= W; ++k)
+    for (int i = k; i <= L; ++i)
+      for (int j = k - 1; j < i; ++j) {
+        const double v = std::max(best[k - 1][j], pre[i] - pre[j]);
+        if (v < best[k][i]) {
+          best[k][i] = v;
+          cut[k][i] = j;
+        }
+      }
+  std::vector<int> n(W);
+  for (int k = W, i = L; k >= 1; --k) {
+    n[k - 1] = i - cut[k][i];
+    i = cut[k][i];
+  }
+  return n;
+}
+
 // ------------------------------------------------------------------ Impl
 struct Session::Impl {
   struct LayerDev {
+    // weights: out x in (in = GEMM K, the fan-in), rows of ld_in elements
     int in = 0, out = 0, act = 0;
     int ld_in = 0, ld_out = 0;
+    // conv layers (LayerSpec): channels, input image, pooling; the network's
+    // first conv reads an im2col of the input (first_conv)
+    bool conv = false, pool = false, first_conv = false;
+    int cin = 0, h = 0, w = 0;
+    // per-sample elements of the layer's input / (pooled) output: the
+    // activation rows (= ld_in / ld_out for a Linear layer)
+    int ain = 0, aout = 0;
+    int64_t pre_elems = 0;  // pooled conv: per-sample conv output before pooling
     float* w32[2] = {nullptr, nullptr};  // fp32 masters by version parity
     uint16_t* lo[2] = {nullptr, nullptr};  // split masters: residuals by parity
     float* b32[2] = {nullptr, nullptr};
@@ -74,6 +145,8 @@ struct Session::Impl {
   };
   struct ActSlot {
     std::vector<__nv_bfloat16*> out16;  // per layer (null for the logits layer)
+    std::vector<__nv_bfloat16*> pre16;  // per layer: pooled conv output before pooling
+    __nv_bfloat16* cols16 = nullptr;     // first conv: im2col of the input rows
     float* out32 = nullptr;              // last stage: logits / final output
     __nv_bfloat16* dzin = nullptr;       // delta into this stage's top layer
     // cross-GPU boundary buffers (only on a rank's first stage when the
@@ -88,6 +161,10 @@ struct Session::Impl {
     std::vector<PoolSlot> pool;
     std::vector<ActSlot> acts;
     std::vector<__nv_bfloat16*> scratch_dz;  // per layer < L-1
+    std::vector<__nv_bfloat16*> scratch_pre;  // per pooled conv layer: dZ before pooling
+    float* wg_ws = nullptr;    // conv wgrad split-K partial slabs (side stream)
+    float* bias_ws = nullptr;  // conv bias-gradient row-block partials (bias stream)
+    size_t wg_floats = 0, bias_floats = 0;
     std::vector<int> version_colour;         // [M+1]
     std::vector<int> mini_act;               // [M+1]
     int* cur_version = nullptr;
@@ -108,7 +185,9 @@ struct Session::Impl {
   };
 
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
-                      send, recv, mark, ktime, xwait, digest };
+                      send, recv, mark, ktime, xwait, digest,
+                      // conv stages
+                      im2col, pool_fwd, pool_bwd, wgrad_partial, reduce_sgd, colsum };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kDigest = -6;  // in-epoch params digests
@@ -147,6 +226,18 @@ struct Session::Impl {
     int value = 0;
     // send / recv
     int peer = 0, dir = 0;
+    // conv stages: images / size / channels (im2col, pooling), partial slabs
+    // (reduce_sgd: S slabs of `slab` floats, rows x cols, lds)
+    int n = 0, h = 0, w = 0, ch = 0;
+    const __nv_bfloat16* in16 = nullptr;
+    const __nv_bfloat16* aux16 = nullptr;
+    __nv_bfloat16* out16 = nullptr;
+    float* f32 = nullptr;
+    const float* w_cur = nullptr;
+    float* w_new = nullptr;
+    int ldw = 0, ld16 = 0, S = 0;
+    long long slab = 0;
+    bool f32dz = false;  // bias: dz holds fp32 partial sums
   };
 
   const SessionConfig& cfg;
@@ -367,6 +458,18 @@ struct Session::Impl {
 // ------------------------------------------------------------------ ctor
 Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   SessionConfig& c = cfg_;
+  const bool convnet = !c.layers.empty();
+  if (convnet) {  // widths / acts of a layer list (per-sample elements)
+    check_layers(c.layers);
+    if (c.verify_fp32) throw std::invalid_argument("conv networks: bf16 precision only");
+    c.widths.clear();
+    c.acts.clear();
+    for (const LayerSpec& l : c.layers) {
+      c.widths.push_back(static_cast<int>(l.in_elems()));
+      c.acts.push_back(l.act);
+    }
+    c.widths.push_back(static_cast<int>(c.layers.back().out_elems()));
+  }
   if (c.widths.size() < 2 || c.acts.size() + 1 != c.widths.size())
     throw std::invalid_argument("bad network description");
   if (c.stage_hi == 0) c.stage_hi = c.W;
@@ -420,8 +523,32 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   net.widths = c.widths;
   for (int a : c.acts) net.activations.push_back(static_cast<pipesim::activation_kind>(a));
   net.loss = c.loss == 0 ? pipesim::loss_kind::mse : pipesim::loss_kind::softmax_cross_entropy;
-  const std::vector<pipesim::stage_model> part = pipesim::partition_model(net, W);
-  total_params_ = net.param_count();
+  // stage s: layers [part_first[s], part_first[s] + part_count[s])
+  std::vector<int> part_first(W), part_count(W);
+  if (convnet) {
+    std::vector<int> cnt = c.stage_layers.empty() ? partition_by_flops(c.layers, W) : c.stage_layers;
+    if (static_cast<int>(cnt.size()) != W)
+      throw std::invalid_argument("stage_layers must have one entry per stage");
+    int f = 0;
+    for (int s = 0; s < W; ++s) {
+      if (cnt[s] < 1) throw std::invalid_argument("every stage needs at least one layer");
+      part_first[s] = f;
+      part_count[s] = cnt[s];
+      f += cnt[s];
+    }
+    if (f != static_cast<int>(c.layers.size()))
+      throw std::invalid_argument("stage_layers must cover the layers");
+    total_params_ = 0;
+    for (const LayerSpec& l : c.layers)
+      total_params_ += static_cast<int64_t>(l.out) * l.fan_in() + l.out;
+  } else {
+    const std::vector<pipesim::stage_model> part = pipesim::partition_model(net, W);
+    for (int s = 0; s < W; ++s) {
+      part_first[s] = part[s].first_layer;
+      part_count[s] = static_cast<int>(part[s].layers.size());
+    }
+    total_params_ = net.param_count();
+  }
 
   // ---------------- plan
   // Per stage: ordered tasks (slot numbers) and the pins / prop versions.
@@ -527,8 +654,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   for (int s = 0; s < W; ++s) {
     Impl::Stage& st = I.stages[s];
     st.id = s + 1;
-    st.first_layer = part[s].first_layer;
-    st.L = static_cast<int>(part[s].layers.size());
+    st.first_layer = part_first[s];
+    st.L = part_count[s];
     st.version_colour = colour(version_iv[s], &pool_n[s], /*half_open=*/true);
     std::vector<int> ac = colour(act_iv[s], &act_n[s], /*half_open=*/false);
     st.mini_act.assign(M + 1, 0);
@@ -538,11 +665,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   // ---------------- split masters: every local layer's wgrad+SGD must run the
   // pair kernel's TMA epilogue (the verify precision and per-slot snapshots
   // keep fp32 masters)
-  I.split = !I.v32 && !c.snapshots;
+  I.split = !I.v32 && !c.snapshots && !convnet;
   for (int s = 0; s < W && I.split; ++s) {
     if (!I.local(s)) continue;
-    for (int gl = part[s].first_layer;
-         gl < part[s].first_layer + static_cast<int>(part[s].layers.size()); ++gl)
+    for (int gl = part_first[s]; gl < part_first[s] + part_count[s]; ++gl)
       if (!split_master_eligible(c.widths[gl + 1], c.widths[gl], ld8(c.widths[gl])))
         I.split = false;
   }
@@ -565,6 +691,26 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       d.act = c.acts[gl];
       d.ld_in = ld8(d.in);
       d.ld_out = ld8(d.out);
+      d.ain = d.ld_in;
+      d.aout = d.ld_out;
+      if (convnet) {
+        const LayerSpec& ls = c.layers[gl];
+        d.in = ls.fan_in();
+        d.out = ls.out;
+        d.ld_in = ld8(d.in);
+        d.ld_out = ld8(d.out);
+        d.ain = static_cast<int>(ls.in_elems());
+        d.aout = static_cast<int>(ls.out_elems());
+        if (ls.kind == LayerKind::conv3x3) {
+          d.conv = true;
+          d.pool = ls.pool;
+          d.cin = ls.in;
+          d.h = ls.h;
+          d.w = ls.w;
+          d.first_conv = gl == 0 && ls.in % 64 != 0;
+          d.pre_elems = d.pool ? static_cast<int64_t>(ls.h) * ls.w * ls.out : 0;
+        }
+      }
       st.layers.push_back(d);
       st.param_count += static_cast<int64_t>(d.in) * d.out + d.out;
       if (!I.local(s)) continue;
@@ -572,15 +718,26 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                           : bytes_of(static_cast<size_t>(d.in) * d.out, 4)) +
                  bytes_of(d.out, 4));
       wb += pool_n[s] * (bytes_of(static_cast<size_t>(d.out) * d.ld_in, 2 * I.sc) + bytes_of(d.out, 4));
-      ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
-      if (l + 1 < st.L) ab += bytes_of(static_cast<size_t>(c.B) * d.ld_out, 2 * I.sc);
+      ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.aout, 2 * I.sc);
+      if (l + 1 < st.L) ab += bytes_of(static_cast<size_t>(c.B) * d.aout, 2 * I.sc);
+      if (d.pool)  // conv output before pooling (slots) + its delta (scratch)
+        ab += (act_n[s] + 1) * bytes_of(static_cast<size_t>(c.B) * d.pre_elems, 2);
+      if (d.first_conv)
+        ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.h * d.w * d.ld_in, 2);
+      if (d.conv) {
+        int lds = 0;
+        const size_t f = wgrad_partial_floats(d.out, d.ld_in, c.B * d.h * d.w, &lds);
+        st.wg_floats = std::max(st.wg_floats, f);
+        st.bias_floats = std::max(st.bias_floats, static_cast<size_t>(kColsumChunks) * d.out);
+      }
     }
     off += st.param_count;
     if (!I.local(s)) continue;
+    wb += bytes_of(st.wg_floats, 4) + bytes_of(st.bias_floats, 4);
     if (s > 0 && !I.local(s - 1))  // boundary buffers: received input + outgoing delta
-      ab += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ld_in, 2 * I.sc);
+      ab += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ain, 2 * I.sc);
     wb += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
-    ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().ld_out, 2 * I.sc);
+    ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.back().aout, 2 * I.sc);
     if (s == W - 1) ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * I.n_out, 4);
     st.bytes_weights = static_cast<int64_t>(wb);
     st.bytes_acts = static_cast<int64_t>(ab);
@@ -628,21 +785,33 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     st.acts.resize(act_n[s]);
     for (auto& as : st.acts) {
       for (int l = 0; l < st.L; ++l) {
+        const auto& d = st.layers[l];
         const bool logits = (s == W - 1) && (l == st.L - 1);
         as.out16.push_back(logits ? nullptr
                                   : I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * I.sc *
-                                                           st.layers[l].ld_out));
+                                                           d.aout));
+        as.pre16.push_back(d.pool ? I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * d.pre_elems)
+                                  : nullptr);
+        if (d.first_conv)
+          as.cols16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * d.h * d.w * d.ld_in);
       }
       if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out);
-      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().ld_out * I.sc);
+      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().aout * I.sc);
       if (s > 0 && !I.local(s - 1)) {
-        as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in * I.sc);
-        as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ld_in * I.sc);
+        as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ain * I.sc);
+        as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ain * I.sc);
       }
     }
     for (int l = 0; l + 1 < st.L; ++l)
       st.scratch_dz.push_back(
-          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].ld_out * I.sc));
+          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].aout * I.sc));
+    for (int l = 0; l < st.L; ++l)
+      st.scratch_pre.push_back(
+          st.layers[l].pool
+              ? I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].pre_elems)
+              : nullptr);
+    if (st.wg_floats) st.wg_ws = I.carve<float>(st.wg_floats);
+    if (st.bias_floats) st.bias_ws = I.carve<float>(st.bias_floats);
   }
   I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x * I.sc);
   I.y32 = I.carve<float>(rows * I.n_out);
@@ -984,11 +1153,12 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     if (!I.local(s - 1)) {  // received over the network into this stage's slot
       const Impl::Stage& me = I.stages[s];
       const auto& fl = me.layers.front();
-      return Mat16{me.acts[me.mini_act[k]].in16, c.B, fl.in, fl.ld_in};
+      return Mat16{me.acts[me.mini_act[k]].in16, c.B, fl.conv ? fl.ain : fl.in, fl.ain};
     }
     const Impl::Stage& pv = I.stages[s - 1];
     const auto& pl = pv.layers.back();
-    return Mat16{pv.acts[pv.mini_act[k]].out16.back(), c.B, pl.out, pl.ld_out};
+    return Mat16{pv.acts[pv.mini_act[k]].out16.back(), c.B, pl.conv ? pl.aout : pl.out,
+                 pl.aout};
   };
 
   // Cross-GPU plumbing.  Previous occupant of each activation slot (slot reuse
@@ -1074,8 +1244,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           const auto& fl = st.layers.front();
           Impl::Op rv{OK::recv};
           rv.stream = Impl::kFwdRecv;
-          rv.dst = as.in16 + static_cast<size_t>(up.jj0) * I.Rm * fl.ld_in * I.sc;
-          rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ld_in * 2 * I.sc;
+          rv.dst = as.in16 + static_cast<size_t>(up.jj0) * I.Rm * fl.ain * I.sc;
+          rv.bytes = static_cast<size_t>(up.jj1 - up.jj0 + 1) * I.Rm * fl.ain * 2 * I.sc;
           rv.peer = I.owner[up.s];
           rv.dir = 0;
           rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
@@ -1090,7 +1260,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         Impl::Op rv{OK::recv};
         rv.stream = Impl::kBwdRecv;
         rv.dst = as.dzin;
-        rv.bytes = static_cast<size_t>(c.B) * st.layers.back().ld_out * 2 * I.sc;
+        rv.bytes = static_cast<size_t>(c.B) * st.layers.back().aout * 2 * I.sc;
         rv.peer = I.owner[up.s];
         rv.dir = 1;
         rv.value = I.add_msg(false, rv.dir, rv.peer, rv.bytes, nullptr, rv.dst);
@@ -1126,17 +1296,44 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         if (l == 0) {
           x = stage_input(s, tk.k, &in_off);
         } else {
-          x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
+          x = Mat16{as.out16[l - 1], c.B, d.conv ? d.ain : d.in, d.ain};
         }
         const bool logits = (s == last_s) && (l == st.L - 1);
         Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
         Impl::Op o{OK::fwd};
         o.stream = ns;
-        if (!c.plan_only)
-        o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
-                       logits ? nullptr : as.out16[l], d.ld_out,
-                       logits ? as.out32 : nullptr, I.n_out, r0,
-                       /*allow_split=*/split_fwd && !I.v32, /*verify=*/I.v32);
+        // a pooled conv writes its pre-pooling output, then pools it
+        __nv_bfloat16* y16 = d.pool ? as.pre16[l] : as.out16[l];
+        const int hw = d.h * d.w;
+        if (d.first_conv) {
+          // the network input's im2col (3-channel images: too narrow for an
+          // im2col TMA box), then a plain GEMM over it
+          Impl::Op ic{OK::im2col};
+          ic.stream = ns;
+          ic.in16 = x.ptr + static_cast<size_t>(in_off + r0) * x.ld;
+          ic.ld = x.ld;
+          ic.n = rows;
+          ic.h = d.h;
+          ic.w = d.w;
+          ic.ch = d.cin;
+          ic.out16 = as.cols16 + static_cast<size_t>(r0) * hw * d.ld_in;
+          ic.ld16 = d.ld_in;
+          push(ic);
+          ++kernels_per_epoch_;
+          if (!c.plan_only)
+            o.g = plan_fwd(Mat16{as.cols16, c.B * hw, d.ld_in, d.ld_in}, r0 * hw, rows * hw, w,
+                           ps.b32[l], d.act, y16, d.out, nullptr, 0, r0 * hw,
+                           /*allow_split=*/false);
+        } else if (d.conv) {
+          if (!c.plan_only)
+            o.g = plan_conv_fwd(Nhwc{x.ptr, x.rows, d.h, d.w, d.cin}, in_off + r0, rows, w,
+                                ps.b32[l], d.act, y16, r0 * hw);
+        } else if (!c.plan_only) {
+          o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
+                         logits ? nullptr : as.out16[l], d.ld_out,
+                         logits ? as.out32 : nullptr, I.n_out, r0,
+                         /*allow_split=*/split_fwd && !I.v32, /*verify=*/I.v32);
+        }
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
           o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
@@ -1145,6 +1342,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         }
         push(o);
         ++kernels_per_epoch_;
+        if (d.pool) {
+          Impl::Op pf{OK::pool_fwd};
+          pf.stream = ns;
+          pf.in16 = as.pre16[l] + static_cast<size_t>(r0) * d.pre_elems;
+          pf.out16 = as.out16[l] + static_cast<size_t>(r0) * d.aout;
+          pf.n = rows;
+          pf.h = d.h;
+          pf.w = d.w;
+          pf.ch = d.out;
+          push(pf);
+          ++kernels_per_epoch_;
+        }
       }
     } else {
       // ---------------- backward of mini k on stage s
@@ -1190,10 +1399,35 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         if (l == 0)
           x = stage_input(s, tk.k, &x_off);
         else
-          x = Mat16{as.out16[l - 1], c.B, d.in, d.ld_in};
-        Mat16 mdz{dz, c.B, d.out, d.ld_out};
+          x = Mat16{as.out16[l - 1], c.B, d.conv ? d.ain : d.in, d.ain};
+        const int hw = d.h * d.w;
+        // a pooled conv's delta arrives pooled (already gated by act' of the
+        // pooled activation, which equals act' at each window's maximum);
+        // route it to the first maximum of every window
+        if (d.pool) {
+          Impl::Op pb{OK::pool_bwd};
+          pb.stream = ns;
+          pb.in16 = dz;
+          pb.aux16 = as.pre16[l];
+          pb.dz = as.out16[l];
+          pb.out16 = st.scratch_pre[l];
+          pb.n = c.B;
+          pb.h = d.h;
+          pb.w = d.w;
+          pb.ch = d.out;
+          push(pb);
+          ++kernels_per_epoch_;
+          dz = st.scratch_pre[l];
+          if (c.side_streams) {
+            cudaEvent_t ev = record_on(ns);
+            wait_on(side, ev);
+            if (bstr != side) wait_on(bstr, ev);
+          }
+        }
+        // conv: dz has one row per output pixel
+        Mat16 mdz = d.conv ? Mat16{dz, c.B * hw, d.out, d.out} : Mat16{dz, c.B, d.out, d.ld_out};
         // dgrad: delta for the layer below (or the previous stage)
-        if (l > 0 || s > 0) {
+        if ((l > 0 || s > 0) && !d.first_conv) {
           __nv_bfloat16* dst;
           int act_prev;
           if (l > 0) {
@@ -1212,9 +1446,14 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld * I.sc;
           Impl::Op o{OK::dgrad};
           o.stream = ns;
-          if (!c.plan_only)
-          o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld, act_prev,
-                           dst, d.ld_in, I.v32);
+          if (!c.plan_only) {
+            if (d.conv)
+              o.g = plan_conv_dgrad(Nhwc{dz, c.B, d.h, d.w, d.out}, prop.w16[l], d.cin, d.ld_in,
+                                    xin, act_prev, dst);
+            else
+              o.g = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin, x.ld,
+                               act_prev, dst, d.ld_in, I.v32);
+          }
           push(o);
           ++kernels_per_epoch_;
         }
@@ -1222,7 +1461,39 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         // made ready before this iteration (dZ_{L-1}: task start; dZ_l: the
         // previous iteration's dgrad, signalled below)
         // wgrad + SGD into the new version (trainer.cpp:244-249, :484-488)
-        {
+        if (d.conv) {
+          // conv: split-K fp32 partial slabs over the pixels, then their
+          // in-order reduction fused with the SGD update and the bf16 copy
+          Impl::Op o{OK::wgrad_partial};
+          o.stream = side;
+          int S = 1;
+          if (!c.plan_only) {
+            if (d.first_conv)
+              o.g = plan_wgrad_partial(mdz, Mat16{as.cols16, c.B * hw, d.ld_in, d.ld_in},
+                                       st.wg_ws, d.ld_in, &S);
+            else
+              o.g = plan_conv_wgrad_partial(mdz, Nhwc{x.ptr, x.rows, d.h, d.w, d.cin}, x_off,
+                                            st.wg_ws, d.ld_in, &S);
+          }
+          push(o);
+          ++kernels_per_epoch_;
+          Impl::Op r{OK::reduce_sgd};
+          r.stream = side;
+          r.f32 = st.wg_ws;
+          r.S = S;
+          r.slab = static_cast<long long>(d.out) * d.ld_in;
+          r.rows = d.out;
+          r.cols = d.in;
+          r.ld = d.ld_in;
+          r.w_cur = d.w32[cur];
+          r.w_new = d.w32[nxt];
+          r.ldw = d.in;
+          r.out16 = next.w16[l];
+          r.ld16 = d.ld_in;
+          r.lr = static_cast<float>(c.lr);
+          push(r);
+          ++kernels_per_epoch_;
+        } else {
           Impl::Op o{OK::wgrad};
           o.stream = side;
           if (!c.plan_only) {
@@ -1238,7 +1509,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           push(o);
           ++kernels_per_epoch_;
         }
-        // bias gradient + SGD; the last one stamps the commit
+        // bias gradient + SGD; the last one stamps the commit.  Conv: column
+        // sums of row blocks of dZ first (one pass over all its pixel rows
+        // on the whole GPU), then the same kernel over the fp32 partials.
         {
           Impl::Op o{OK::bias};
           o.stream = bstr;
@@ -1246,6 +1519,21 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           o.rows = c.B;
           o.cols = d.out;
           o.ld = d.ld_out;
+          if (d.conv) {
+            Impl::Op cs{OK::colsum};
+            cs.stream = bstr;
+            cs.dz = dz;
+            cs.rows = c.B * hw;
+            cs.cols = d.out;
+            cs.ld = d.out;
+            cs.f32 = st.bias_ws;
+            push(cs);
+            ++kernels_per_epoch_;
+            o.dz = reinterpret_cast<const __nv_bfloat16*>(st.bias_ws);
+            o.rows = colsum_chunks(c.B * hw);
+            o.ld = d.out;
+            o.f32dz = true;
+          }
           o.b_cur = d.b32[cur];
           o.b_new = d.b32[nxt];
           o.b_copy = next.b32[l];
@@ -1306,8 +1594,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       wait_on(Impl::kFwdSend, node.done);
       Impl::Op sd{OK::send};
       sd.stream = Impl::kFwdSend;
-      sd.src = as.out16.back() + static_cast<size_t>(node.jj0) * I.Rm * ll.ld_out * I.sc;
-      sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.ld_out * 2 * I.sc;
+      sd.src = as.out16.back() + static_cast<size_t>(node.jj0) * I.Rm * ll.aout * I.sc;
+      sd.bytes = static_cast<size_t>(node.jj1 - node.jj0 + 1) * I.Rm * ll.aout * 2 * I.sc;
       sd.peer = I.owner[s + 1];
       sd.dir = 0;
       sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
@@ -1318,7 +1606,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       Impl::Op sd{OK::send};
       sd.stream = Impl::kBwdSend;
       sd.src = as.dzsend;
-      sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ld_in * 2 * I.sc;
+      sd.bytes = static_cast<size_t>(c.B) * st.layers.front().ain * 2 * I.sc;
       sd.peer = I.owner[s - 1];
       sd.dir = 1;
       sd.value = I.add_msg(true, sd.dir, sd.peer, sd.bytes, sd.src, nullptr);
@@ -1361,6 +1649,8 @@ std::vector<Transfer> Session::transfers() const {
 }
 
 int64_t Session::stage_param_count(int s) const { return impl_->stages.at(s - 1).param_count; }
+int Session::stage_first_layer(int s) const { return impl_->stages.at(s - 1).first_layer; }
+int Session::stage_layer_count(int s) const { return impl_->stages.at(s - 1).L; }
 int64_t Session::stage_param_offset(int s) const {
   return impl_->stages.at(s - 1).param_offset;
 }
@@ -1650,7 +1940,25 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::wgrad: launch_wgrad(o.g, s); break;
       case OK::bias:
         launch_bias_sgd(s, o.dz, o.rows, o.cols, o.ld, o.b_cur, o.b_new, o.b_copy, o.lr,
-                        o.tag_slot, o.cur_version, o.version, o.trace_src, o.trace_dst, I.v32);
+                        o.tag_slot, o.cur_version, o.version, o.trace_src, o.trace_dst,
+                        I.v32 || o.f32dz);
+        break;
+      case OK::im2col:
+        launch_im2col_first(s, o.in16, o.ld, o.n, o.h, o.w, o.ch, o.out16, o.ld16);
+        break;
+      case OK::pool_fwd:
+        launch_maxpool2_fwd(s, o.in16, o.n, o.h, o.w, o.ch, o.out16);
+        break;
+      case OK::pool_bwd:  // in16 = d_out (pooled), aux16 = conv output, dz = pooled output
+        launch_maxpool2_bwd(s, o.in16, o.aux16, o.dz, o.n, o.h, o.w, o.ch, o.out16);
+        break;
+      case OK::wgrad_partial: launch_wgrad_partial(o.g, s); break;
+      case OK::reduce_sgd:
+        launch_reduce_sgd(s, o.f32, o.S, o.slab, o.rows, o.cols, o.ld, o.w_cur, o.w_new, o.ldw,
+                          o.out16, o.ld16, o.lr);
+        break;
+      case OK::colsum:
+        launch_colsum_partial(s, o.dz, o.rows, o.cols, o.ld, o.f32);
         break;
       case OK::loss:
         launch_loss(s, o.y, o.rows, o.cols, o.ld, o.t, o.ld_t, o.loss, o.act_last, o.denom,

@@ -40,9 +40,55 @@ enum class RunMode { timeprest = 0, pipedream = 1, sequential = 2 };
 // copied straight into the device layout, no conversion kernel)
 enum class HostDType { f64 = 0, f32 = 1, labels_i32 = 2, bf16 = 3 };
 
+// One layer of a convolutional network (VGG-style stages, BASELINE
+// configs[3]; the reference has only Linear layers).
+//  linear: in -> out features.
+//  conv3x3: in -> out channels on h x w NHWC images, pad 1, stride 1, then
+//  the activation, then (pool) 2x2 / stride-2 max pooling.  Weights are
+//  [out][9 * in] with K = (3r + s) * in + c (tap-major), then b[out].
+// A network is conv layers followed by linear layers; the first linear layer
+// reads the last conv output flattened in NHWC order.  The first layer may be
+// a narrow conv (in * 9 <= 72: the network input, im2col'd), every other conv
+// has in, out % 64 == 0.
+enum class LayerKind { linear = 0, conv3x3 = 1 };
+struct LayerSpec {
+  LayerKind kind = LayerKind::linear;
+  int in = 0, out = 0;
+  int h = 0, w = 0;  // conv: input image size
+  bool pool = false;
+  int act = 0;
+  // per-sample element counts of the layer's input and (pooled) output
+  int64_t in_elems() const {
+    return kind == LayerKind::linear ? in : static_cast<int64_t>(h) * w * in;
+  }
+  int64_t out_elems() const {
+    if (kind == LayerKind::linear) return out;
+    return pool ? static_cast<int64_t>(h / 2) * (w / 2) * out : static_cast<int64_t>(h) * w * out;
+  }
+  // GEMM K of the weights (fan-in) and forward flops per sample
+  int fan_in() const { return kind == LayerKind::linear ? in : 9 * in; }
+  double flops() const {
+    return 2.0 * out * fan_in() * (kind == LayerKind::linear ? 1.0 : static_cast<double>(h) * w);
+  }
+};
+
+// Contiguous partition of a layer list into W stages minimising the largest
+// stage's forward flops (the reference's partition_model balances parameter
+// counts, trainer.cpp:104-135, which for a CNN would put every conv layer on
+// one stage).  Returns n_layers per stage.
+std::vector<int> partition_by_flops(const std::vector<LayerSpec>& layers, int W);
+// Validates a conv network description (throws std::invalid_argument).
+void check_layers(const std::vector<LayerSpec>& layers);
+
 struct SessionConfig {
   std::vector<int> widths;
   std::vector<int> acts;
+  // convolutional network (empty: the MLP given by widths / acts).  When set,
+  // widths / acts are derived (widths[l] = per-sample input elements of
+  // layer l, widths.back() = classes) and the stages are a flop-balanced
+  // partition (stage_layers overrides it).
+  std::vector<LayerSpec> layers;
+  std::vector<int> stage_layers;
   int loss = 1;
   int W = 2, N = 2, B = 20, M = 10;
   double lr = 0.05;
@@ -130,6 +176,8 @@ class Session {
   int64_t param_count() const { return total_params_; }
   int64_t stage_param_count(int s) const;  // 1-based
   int64_t stage_param_offset(int s) const;
+  int stage_first_layer(int s) const;  // 1-based stage; 0-based layer
+  int stage_layer_count(int s) const;
 
   // Installs a flat whole-network parameter vector as version 0.
   void load_params(const double* flat);

@@ -609,7 +609,10 @@ class Session:
                               int(digests))
         spec = net._c()
         h = C.c_void_p()
-        if world > 1:
+        if getattr(net, "layer_net", False):  # convnet.ConvNetSpec
+            N.check(_L().pb_session_create_layers(C.byref(spec), C.byref(cfg), rank, world,
+                                                  bytes(nccl_ids), len(nccl_ids), C.byref(h)))
+        elif world > 1:
             N.check(_L().pb_session_create_dist(C.byref(spec), C.byref(cfg), rank, world,
                                                 bytes(nccl_ids), len(nccl_ids), C.byref(h)))
         else:
