@@ -228,17 +228,16 @@ int pb_conv_bwd_dw_sgd(void* stream, const uint16_t* dz, int n, int h, int w, in
                        int ld_w32, uint16_t* w16, int ld_w16, float lr) {
   PB_GUARD_BEGIN
   const int pixels = n * h * w;
-  int lds = 0;
-  const size_t floats = pb::wgrad_partial_floats(cout, 9 * cin, pixels, &lds);
+  const size_t floats = pb::conv_wgrad_floats(cout, cin, pixels);
   float* ws = nullptr;
   cudaStream_t st = as_stream(stream);
   PB_CUDA(cudaMallocAsync(&ws, floats * 4, st));
-  int S = 0;
+  pb::ConvWgradInfo info;
   pb::Mat16 mdz{bf(dz), pixels, cout, cout};
-  pb::GemmLaunch g = pb::plan_conv_wgrad_partial(mdz, pb::Nhwc{bf(x), n, h, w, cin}, 0, ws, lds, &S);
+  pb::GemmLaunch g = pb::plan_conv_wgrad_partial(mdz, pb::Nhwc{bf(x), n, h, w, cin}, 0, ws, &info);
   pb::launch_wgrad_partial(g, st);
-  pb::launch_reduce_sgd(st, ws, S, static_cast<long long>(cout) * lds, cout, 9 * cin, lds, w_cur,
-                        w_new, ld_w32, bfm(w16), ld_w16, lr);
+  pb::launch_reduce_sgd(st, ws, info.splits, info.slab, cout, 9 * cin, info.lds, w_cur, w_new,
+                        ld_w32, bfm(w16), ld_w16, lr, info.transposed);
   PB_CUDA(cudaFreeAsync(ws, st));
   PB_GUARD_END
 }

@@ -27,9 +27,12 @@ inline int colsum_chunks(int rows) {
 }
 void launch_colsum_partial(cudaStream_t st, const __nv_bfloat16* dz, int rows, int cols, int ld,
                            float* partial);
+// w_new = w_cur - lr * sum_{s < S} slab_s (in split order), w16 = bf16(w_new)
+// (may be null); rows x cols of the weights; transposed: the slabs hold
+// [cols][rows] (rows of lds floats either way)
 void launch_reduce_sgd(cudaStream_t st, const float* slabs, int S, long long slab, int rows,
                        int cols, int lds, const float* w_cur, float* w_new, int ldw,
-                       __nv_bfloat16* w16, int ld16, float lr);
+                       __nv_bfloat16* w16, int ld16, float lr, bool transposed = false);
 
 // --- implicit-GEMM 3x3 / pad 1 / stride 1 convolution GEMMs (layer_ops.cu)
 // NHWC activation tensor: n images of H x W x C, contiguous.
@@ -46,11 +49,19 @@ GemmLaunch plan_conv_fwd(const Nhwc& x, int img0, int imgs, const Mat16& w, cons
 // w = [Cout, ld] with ld >= 9 * Cin, xin / d = [n*H*W, Cin].
 GemmLaunch plan_conv_dgrad(const Nhwc& dz, const __nv_bfloat16* w, int cin, int ld_w,
                            const __nv_bfloat16* xin, int act_prev, __nv_bfloat16* d);
-// Partial weight gradients of a conv: slab s = sum over its pixel range of
-// dz[p, :]^T im2col(x)[p, :] -> ws + s * M * lds (fp32, M = Cout, N = 9*Cin).
-// x images img0 .. img0 + dz pixels / (H*W).  *splits receives S.
+// Partial weight gradients of a conv on the CTA-pair kernel: slab s = the
+// sum over its pixel range of dz[p, :]^T im2col(x)[p, :] (fp32 [Cout][9*Cin],
+// or its transpose [9*Cin][Cout] for Cout < 256), at ws + s * slab with rows
+// of lds floats.  x images img0 .. img0 + dz pixels / (H*W).
+struct ConvWgradInfo {
+  int splits = 1, lds = 0;
+  long long slab = 0;
+  bool transposed = false;
+};
 GemmLaunch plan_conv_wgrad_partial(const Mat16& dz, const Nhwc& x, int img0, float* ws,
-                                   int lds, int* splits);
+                                   ConvWgradInfo* info);
+// workspace floats plan_conv_wgrad_partial needs
+size_t conv_wgrad_floats(int cout, int cin, int pixels);
 // The same for a plain [pixels, K] operand (the network input's im2col).
 GemmLaunch plan_wgrad_partial(const Mat16& dz, const Mat16& x, float* ws, int lds, int* splits);
 // workspace floats plan_*wgrad_partial needs for an M x N gradient

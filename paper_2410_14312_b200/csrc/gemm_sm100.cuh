@@ -1205,6 +1205,21 @@ __device__ __forceinline__ void conv_loads_fd(const GemmShape& sh, const CUtenso
   }
 }
 
+// 64 pixels (K, from k0 + k_off) x 64 channels of tap mn / C of an im2col
+// operand, MN-major (conv wgrad).  Columns past the GEMM extent `ext` load a
+// valid box (tap 0) whose products land outside the stored output.
+template <class Cfg>
+__device__ __forceinline__ void conv_im2col_mn(const GemmShape& sh, const CUtensorMap* map,
+                                               uint32_t fb, uint8_t* dst, int k0, int mn, int ext,
+                                               int k_off) {
+  const int hw = sh.conv_h * sh.conv_w;
+  const int p = k0 + k_off;
+  const int pn = p / hw, ph = (p - pn * hw) / sh.conv_w, pw = p - pn * hw - ph * sh.conv_w;
+  if (mn >= ext) mn = 0;
+  const int tap = mn / sh.conv_c, c0 = mn - tap * sh.conv_c;
+  ptx::tma_load_im2col_pair(dst, map, fb, c0, pw - 1, ph - 1, pn, tap % 3, tap / 3);
+}
+
 // wgrad: B = im2col(x), 64 pixels (K) x 64 channels of tap n / C (N) for
 // every 64 output columns, MN-major.
 template <class Cfg>
@@ -1257,9 +1272,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int kb_all = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
-  constexpr int S_k = 1;  // the pair kernel never splits K
-  const int kbps = kb_all;
-  const int num_units = num_tiles;
+  // split-K only into partial slabs (conv wgrad): unit = (tile, split)
+  const int S_k = ep.partial_slab ? max(1, sh.splits) : 1;
+  const int kbps = ep.partial_slab && sh.splits > 1 ? sh.kb_per_split : kb_all;
+  const int num_units = num_tiles * S_k;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmap_a);
@@ -1322,6 +1338,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
           }
           if constexpr (!A_MN) {
             ptx::tma_load_2d_pair(a_dst, &tmap_a, fb, k0 + sh.a_k_off, m0 + sh.a_mn_off);
+          } else if (sh.conv == 4) {
+            // transposed conv wgrad: A = im2col(x), 64 pixels (K) x 64
+            // channels of tap m / C (M) per half, MN-major
+#pragma unroll
+            for (int h = 0; h < 2; ++h) conv_im2col_mn<Cfg>(sh, &tmap_a, fb, a_dst + h * 8192, k0,
+                                                            m0 + h * 64, sh.M, sh.a_k_off);
           } else {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -1334,7 +1356,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             const int nbj = tn * BN + j * Cfg::kMmaN + static_cast<int>(rank) * (Cfg::kMmaN / 2);
             uint8_t* bj = b_dst + j * Cfg::kBSub;
             if (B_MN && sh.conv == 2) {
-              conv_wgrad_b<Cfg>(sh, &tmap_b, fb, bj, k0, nbj);
+#pragma unroll
+              for (int h = 0; h < Cfg::kMmaN / 128; ++h)
+                conv_im2col_mn<Cfg>(sh, &tmap_b, fb, bj + h * 8192, k0, nbj + h * 64, sh.N,
+                                    sh.b_k_off);
               continue;
             }
             if constexpr (!B_MN) {
@@ -1438,7 +1463,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && split == 0 && rank == 0 &&
           e == 0 && lane == 0 && ep.tag_src && ep.tag_dst)
         write_tags(ep);
-      if (ep.dbg_skip & 1) {
+      if (ep.partial_slab) {
+        // split-K into partial slabs (conv wgrad): this split's own fp32
+        // slab, plain stores; an in-order reduction consumes the slabs
+        if constexpr (EPI == kEpiFwd) {
+          EpiParams epp = ep;
+          epp.y32 = ep.y32 + static_cast<size_t>(split) * ep.partial_slab;
+          epilogue_warp_vec<EPI, kLinear>(epp, sh, row_base, tn * BN + c_off, kColsPerWarp,
+                                          t_row, T);
+        }
+      } else if (ep.dbg_skip & 1) {
       } else if (EPI == kEpiWgradSgd && ep.rowwise == 3) {
         if constexpr (EPI == kEpiWgradSgd) {
           int next_row = -1, next_col = 0;

@@ -25,8 +25,11 @@ struct GemmShape {
   //             B = W viewed [Cout][9][Cin] (3-D map, MN-major)
   //  2 wgrad:   A = dz [pixels, Cout] (MN-major), B = im2col(x) (MN-major,
   //             64-pixel columns)
+  //  4 wgrad, transposed (dW^T, for Cout < 256): A = im2col(x) (MN-major,
+  //             M = 9*C), B = dz (MN-major, N = Cout)
   // conv_h / conv_w: image size; conv_c: channels of the im2col'd tensor.
-  // a_mn_off (modes 1, 3) / b_k_off (mode 2) are pixel offsets.
+  // a_mn_off (modes 1, 3) / b_k_off (mode 2) / a_k_off (mode 4) are pixel
+  // offsets.
   int conv = 0, conv_h = 0, conv_w = 0, conv_c = 0;
 };
 

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -125,7 +126,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
       return e ? std::max(1, std::atoi(e)) : 1;
     }();
     if (EPI != kEpiWgradSgd && tpp > 1) cap = std::min(cap, (tiles + tpp - 1) / tpp);
-    const int pairs = std::min(tiles, std::max(1, cap));
+    const int units = tiles * (g.ep.partial_slab ? std::max(1, g.sh.splits) : 1);
+    const int pairs = std::min(units, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
   } else if constexpr (BN <= 256) {
@@ -590,10 +592,33 @@ CUtensorMap make_w3d_tmap(const __nv_bfloat16* w, int cout, int cin, int ld) {
 }
 
 // split count of a partial-slab wgrad: about two waves of 128 x bn tiles
+// Split count of a split-K partial-slab GEMM with `tiles` output tiles on
+// `slots` persistent CTAs (pairs) or SMs: the smallest S whose tiles * S units
+// fill the slots in whole waves best (at most four waves, at least 8
+// k-blocks per unit), so no slot idles through a final partial wave.
+int balanced_splits(int tiles, int kb, int slots) {
+  const int s_max = std::max(1, std::min(std::max(1, kb / 8), (4 * slots + tiles - 1) / tiles));
+  int best = 1;
+  double best_eff = -1.0;
+  for (int S = 1; S <= s_max; ++S) {
+    const int kbps = (kb + S - 1) / S;
+    const int s_real = (kb + kbps - 1) / kbps;
+    const int units = tiles * s_real;
+    const int waves = (units + slots - 1) / slots;
+    // useful work / slot time, the last split's shorter K included
+    const double eff = static_cast<double>(kb) * tiles / (static_cast<double>(waves) * slots * kbps);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = S;
+    }
+  }
+  return best;
+}
+
 int partial_splits(int M, int N, int K, int bn, int* kbps) {
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int kb = (K + 63) / 64;
-  int S = std::max(1, std::min(kb, (2 * sm_count() + tiles - 1) / tiles));
+  const int S = balanced_splits(tiles, kb, sm_count());
   *kbps = (kb + S - 1) / S;
   return (kb + *kbps - 1) / *kbps;
 }
@@ -672,17 +697,101 @@ GemmLaunch partial_common(const Mat16& dz, int N, float* ws, int lds, int* split
   if (lds % 4 != 0 || !al(ws, 16)) throw std::invalid_argument("partial slabs: 16-byte rows");
   return g;
 }
+
+// CTA-pair conv wgrad (256-row tiles, split-K over the pixels into partial
+// slabs, about two units per pair): Cout >= 256 computes dW = dz^T im2col(x)
+// (M = Cout), narrower layers the transposed dW^T = im2col(x)^T dz
+// (M = 9*Cin, N = Cout), so the 256-row tile is never mostly empty.
+struct PairWgradShape {
+  bool transposed;
+  int M, N, bn, S, kbps, lds;
+};
+PairWgradShape pair_wgrad_shape(int cout, int cin, int pixels, bool transposed) {
+  PairWgradShape p;
+  p.transposed = transposed;
+  p.M = p.transposed ? 9 * cin : cout;
+  p.N = p.transposed ? cout : 9 * cin;
+  p.bn = p.N >= 256 ? 256 : 128;
+  const int tiles = ((p.M + 255) / 256) * ((p.N + p.bn - 1) / p.bn);
+  const int kb = (pixels + 63) / 64;
+  const int S = balanced_splits(tiles, kb, sm_count() / 2);
+  p.kbps = (kb + S - 1) / S;
+  p.S = (kb + p.kbps - 1) / p.kbps;
+  p.lds = (p.N + 7) / 8 * 8;
+  return p;
+}
 }  // namespace
 
-GemmLaunch plan_conv_wgrad_partial(const Mat16& dz, const Nhwc& x, int img0, float* ws, int lds,
-                                   int* splits) {
-  GemmLaunch g = partial_common(dz, 9 * x.c, ws, lds, splits);
-  g.tb = make_im2col_tmap(x, 64);
-  g.sh.b_k_off = img0 * x.h * x.w;
-  g.sh.conv = 2;
+size_t conv_wgrad_floats(int cout, int cin, int pixels) {
+  int lds = 0;
+  const size_t single = wgrad_partial_floats(cout, 9 * cin, pixels, &lds);
+  size_t pair = 0;
+  for (bool t : {false, true}) {
+    const PairWgradShape p = pair_wgrad_shape(cout, cin, pixels, t);
+    pair = std::max(pair, static_cast<size_t>(p.S) * p.M * p.lds);
+  }
+  return std::max(single, pair);
+}
+
+// PIPESIM_CONV_WGRAD=pair|single|transposed (default: pair for Cout >= 256,
+// else the single-CTA kernel; the transposed pair form measured slower)
+int conv_wgrad_mode(int cout) {
+  static const int env = [] {
+    const char* e = std::getenv("PIPESIM_CONV_WGRAD");
+    if (!e) return -1;
+    return std::strcmp(e, "single") == 0 ? 0 : std::strcmp(e, "pair") == 0 ? 1 : 2;
+  }();
+  if (env >= 0) return env == 1 && cout < 256 ? 0 : env;
+  return cout >= 256 ? 1 : 0;
+}
+
+GemmLaunch plan_conv_wgrad_partial(const Mat16& dz, const Nhwc& x, int img0, float* ws,
+                                   ConvWgradInfo* info) {
+  const int cout = dz.cols, pixels = dz.rows;
+  const int mode = conv_wgrad_mode(cout);
+  if (mode == 0) {  // single-CTA 128-row tiles, dW = dz^T im2col(x)
+    int lds = 0;
+    wgrad_partial_floats(cout, 9 * x.c, pixels, &lds);
+    GemmLaunch g = partial_common(dz, 9 * x.c, ws, lds, &info->splits);
+    g.tb = make_im2col_tmap(x, 64);
+    g.sh.b_k_off = img0 * x.h * x.w;
+    g.sh.conv = 2;
+    g.sh.conv_h = x.h;
+    g.sh.conv_w = x.w;
+    g.sh.conv_c = x.c;
+    info->lds = lds;
+    info->slab = static_cast<long long>(cout) * lds;
+    info->transposed = false;
+    return g;
+  }
+  const PairWgradShape p = pair_wgrad_shape(cout, x.c, pixels, mode == 2);
+  GemmLaunch g;
+  g.pair = true;
+  g.bn = p.bn;
+  const CUtensorMap im = make_im2col_tmap(x, 64);
+  const CUtensorMap dm = make_operand_tmap(dz, /*k_major=*/false, 64);
+  g.ta = p.transposed ? im : dm;
+  g.tb = p.transposed ? dm : im;
+  g.sh = GemmShape{p.M, p.N, pixels, 0, 0, 0, 0, p.S, p.kbps};
+  g.sh.conv = p.transposed ? 4 : 2;
+  if (p.transposed)
+    g.sh.a_k_off = img0 * x.h * x.w;
+  else
+    g.sh.b_k_off = img0 * x.h * x.w;
   g.sh.conv_h = x.h;
   g.sh.conv_w = x.w;
   g.sh.conv_c = x.c;
+  g.ep = empty_epi(kEpiFwd);
+  g.ep.act = kLinear;
+  g.ep.y32 = ws;
+  g.ep.ld_y32 = p.lds;
+  g.ep.partial_slab = static_cast<long long>(p.M) * p.lds;
+  g.ep.rowwise = 2;
+  if (!al(ws, 16)) throw std::invalid_argument("partial slabs: 16-byte aligned workspace");
+  info->splits = p.S;
+  info->lds = p.lds;
+  info->slab = static_cast<long long>(p.M) * p.lds;
+  info->transposed = p.transposed;
   return g;
 }
 

@@ -726,7 +726,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.h * d.w * d.ld_in, 2);
       if (d.conv) {
         int lds = 0;
-        const size_t f = wgrad_partial_floats(d.out, d.ld_in, c.B * d.h * d.w, &lds);
+        const size_t f = d.first_conv ? wgrad_partial_floats(d.out, d.ld_in, c.B * d.h * d.w, &lds)
+                                      : conv_wgrad_floats(d.out, d.cin, c.B * d.h * d.w);
         st.wg_floats = std::max(st.wg_floats, f);
         st.bias_floats = std::max(st.bias_floats, static_cast<size_t>(kColsumChunks) * d.out);
       }
@@ -1466,25 +1467,28 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           // in-order reduction fused with the SGD update and the bf16 copy
           Impl::Op o{OK::wgrad_partial};
           o.stream = side;
-          int S = 1;
+          ConvWgradInfo wi;
+          wi.lds = d.ld_in;
+          wi.slab = static_cast<long long>(d.out) * d.ld_in;
           if (!c.plan_only) {
             if (d.first_conv)
               o.g = plan_wgrad_partial(mdz, Mat16{as.cols16, c.B * hw, d.ld_in, d.ld_in},
-                                       st.wg_ws, d.ld_in, &S);
+                                       st.wg_ws, d.ld_in, &wi.splits);
             else
               o.g = plan_conv_wgrad_partial(mdz, Nhwc{x.ptr, x.rows, d.h, d.w, d.cin}, x_off,
-                                            st.wg_ws, d.ld_in, &S);
+                                            st.wg_ws, &wi);
           }
           push(o);
           ++kernels_per_epoch_;
           Impl::Op r{OK::reduce_sgd};
           r.stream = side;
           r.f32 = st.wg_ws;
-          r.S = S;
-          r.slab = static_cast<long long>(d.out) * d.ld_in;
+          r.S = wi.splits;
+          r.slab = wi.slab;
+          r.value = wi.transposed ? 1 : 0;
           r.rows = d.out;
           r.cols = d.in;
-          r.ld = d.ld_in;
+          r.ld = wi.lds;
           r.w_cur = d.w32[cur];
           r.w_new = d.w32[nxt];
           r.ldw = d.in;
@@ -1955,7 +1959,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
       case OK::wgrad_partial: launch_wgrad_partial(o.g, s); break;
       case OK::reduce_sgd:
         launch_reduce_sgd(s, o.f32, o.S, o.slab, o.rows, o.cols, o.ld, o.w_cur, o.w_new, o.ldw,
-                          o.out16, o.ld16, o.lr);
+                          o.out16, o.ld16, o.lr, o.value != 0);
         break;
       case OK::colsum:
         launch_colsum_partial(s, o.dz, o.rows, o.cols, o.ld, o.f32);
