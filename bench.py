@@ -261,10 +261,8 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    # the executor runs an 8-stage pipeline on one GPU without split-K
-    # forwards (throughput over latency, session.cu); the standalone per-shape
-    # timings below use the same kernels
-    os.environ.setdefault("PIPESIM_SPLITK", "0")
+    # split-K forwards follow the session's own policy (on only when a process
+    # holds <= 2 stages, i.e. one stage per GPU: latency over throughput)
     import torch
     import torch.distributed as dist
 
@@ -386,6 +384,39 @@ def main():
         e2e_step_ms = float(t.item())
     e2e_value = jobs * rows / (e2e_step_ms / 1000.0)
 
+    # ---- N > 1: pipeline-boundary traffic (the program's own transfer list)
+    # and per-stage busy time / bubble from one node-timed epoch
+    pipeline = None
+    if split:
+        xfers = P.plan_transfers(net, W, Nm, B, M, "timeprest", rank=rank, world=world)
+        sent = {}
+        for kind, d, peer, nbytes in xfers:
+            if kind == "send":
+                key = f"{min(rank, peer)}-{max(rank, peer)}:{'act' if d == 0 else 'delta'}"
+                sent[key] = sent.get(key, 0) + nbytes
+        prof = sess.profile_epoch()["profile"]
+        mine = {"rank": rank, "sent": sent, "makespan_ms": prof["makespan_ms"],
+                "busy_ms": [b for b in prof["busy_ms"] if b >= 0]}
+        allp = [None] * world
+        dist.all_gather_object(allp, mine)
+        if rank == 0:
+            bytes_per_boundary = {}
+            for m in allp:
+                for k, v in m["sent"].items():
+                    bytes_per_boundary[k] = bytes_per_boundary.get(k, 0) + v
+            busy = [b for m in allp for b in m["busy_ms"]]
+            mk = max(m["makespan_ms"] for m in allp)
+            pipeline = {
+                "boundary_bytes_per_step": bytes_per_boundary,
+                "boundary_GBps_at_step_rate": {k: v / (ms_step / 1000.0) / 1e9
+                                               for k, v in bytes_per_boundary.items()},
+                "transport": transport + ("" if transport == "ipc" else " (unverified on hardware)"),
+                "stage_busy_ms": busy, "profile_makespan_ms": mk,
+                "bubble": 1.0 - sum(busy) / (len(busy) * mk) if mk > 0 else None,
+                "note": ("busy / bubble from one epoch timed per node without the graph "
+                         "(Session.profile_epoch); bytes from the program's transfer list"),
+            }
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -430,6 +461,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": M * 4 * B + M * 8, "ms_per_step": e2e_step_ms},
         "gpu_launches": kernels_per_step,
+        "pipeline": pipeline,
         "other_configs": other_configs(P) if world == 1 else None,
         "e2e_dropin": dropin_e2e() if world == 1 and not args.no_dropin else None,
         "clocks": clocks.summary(),
