@@ -126,9 +126,22 @@ int pb_linear_fwd(void* stream, const uint16_t* x, int rows, int in, int ld_x,
   PB_GUARD_BEGIN
   pb::Mat16 mx{bf(x), rows, in, ld_x};
   pb::Mat16 mw{bf(w), out, in, ld_w};
+  cudaStream_t st = as_stream(stream);
+  // a skinny forward splits K on CTA pairs with the in-kernel fixup: its
+  // workspace and (zeroed) tile counters live for this call only
+  const size_t fix_floats = pb::fwd_fix_floats(rows, out, in);
+  float* ws = nullptr;
+  int* cnt = nullptr;
+  if (fix_floats) {
+    const size_t nc = static_cast<size_t>(pb::fwd_fix_counters(rows, out));
+    PB_CUDA(cudaMallocAsync(&ws, fix_floats * 4 + nc * 4, st));
+    cnt = reinterpret_cast<int*>(ws + fix_floats);
+    PB_CUDA(cudaMemsetAsync(cnt, 0, nc * 4, st));
+  }
   pb::GemmLaunch g = pb::plan_fwd(mx, 0, rows, mw, bias, act, bfm(y16), ld_y16,
-                                  y32, ld_y32, 0);
-  pb::launch_fwd(g, as_stream(stream));
+                                  y32, ld_y32, 0, true, false, ws, cnt);
+  pb::launch_fwd(g, st);
+  if (ws) PB_CUDA(cudaFreeAsync(ws, st));
   PB_GUARD_END
 }
 

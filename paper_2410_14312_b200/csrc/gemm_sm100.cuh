@@ -455,10 +455,11 @@ __device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const Ge
 constexpr int kVecLd = 32;  // staging row stride (floats)
 __device__ __forceinline__ int vec_slot(int row, int chunk) { return (chunk ^ (row & 7)) * 4; }
 
-template <int EPI, int ACT>
+template <int EPI, int ACT, bool FIX = false>
 __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const GemmShape& sh,
                                                   int row_base, int n_base, int n_cols,
-                                                  uint32_t t_row, float* T) {
+                                                  uint32_t t_row, float* T,
+                                                  const FixSrc& fix = FixSrc{}) {
   const int lane = threadIdx.x % 32;
   const int sub_r = lane >> 3;
   const int c4 = (lane & 7) * 4;
@@ -501,6 +502,32 @@ __device__ __forceinline__ void epilogue_warp_vec(const EpiParams& ep, const Gem
       uint32_t r[32];
       ptx::tmem_ld32(t_row + c, r);
       ptx::tmem_ld_wait();
+      if constexpr (FIX) {
+        // split-K fixup: the S partials of these 32 columns in split order,
+        // this unit's own from TMEM, the others from their warp-blocked slots
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int sp = 0; sp < fix.S; ++sp) {
+          if (sp == fix.self) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] += __uint_as_float(r[j]);
+          } else {
+            const float4* p = reinterpret_cast<const float4*>(
+                fix.base + sp * fix.stride + (c / 32) * 1024 + lane * 4);
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 v = __ldcg(p + j4 * 32);
+              acc[4 * j4] += v.x;
+              acc[4 * j4 + 1] += v.y;
+              acc[4 * j4 + 2] += v.z;
+              acc[4 * j4 + 3] += v.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(acc[j]);
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         *reinterpret_cast<float4*>(T + lane * kVecLd + vec_slot(lane, j)) =
@@ -1258,6 +1285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   uint64_t* sgd_bar = tempty_bar + 2;    // [kSgdBufs per epilogue warp] (TMA SGD epilogue)
   // (own 16-byte slot, apart from the barriers thread 0 initialises)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::kBarOff + 496);
+  volatile int* fix_last = reinterpret_cast<volatile int*>(smem + Cfg::kBarOff + 500);
   static_assert(sizeof(uint64_t) * (2 * Cfg::kStages + 4 +
                                     (EPI == kEpiWgradSgd ? Cfg::kSgdBufs * Cfg::kEpiWarps : 0)) <=
                     496,
@@ -1272,9 +1300,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int kb_all = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
-  // split-K only into partial slabs (conv wgrad): unit = (tile, split)
-  const int S_k = ep.partial_slab ? max(1, sh.splits) : 1;
-  const int kbps = ep.partial_slab && sh.splits > 1 ? sh.kb_per_split : kb_all;
+  // split-K into partial slabs (conv wgrad) or with the in-kernel fixup
+  // (forward): unit = (tile, split)
+  // (only forward-epilogue launches split: the other kernels fold S_k = 1)
+  const bool splitk = EPI == kEpiFwd && (ep.partial_slab || ep.fix_cnt) && sh.splits > 1;
+  const int S_k = splitk ? sh.splits : 1;
+  const int kbps = splitk ? sh.kb_per_split : kb_all;
   const int num_units = num_tiles * S_k;
 
   if (threadIdx.x == 0) {
@@ -1463,7 +1494,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && split == 0 && rank == 0 &&
           e == 0 && lane == 0 && ep.tag_src && ep.tag_dst)
         write_tags(ep);
-      if (ep.partial_slab) {
+      if (EPI == kEpiFwd && ep.fix_cnt && S_k > 1) {
+        // split-K fixup: store this split's partial (warp-blocked: each
+        // store instruction writes 512 contiguous bytes), publish it, count
+        // the arrival; the last split of the tile half reduces and finishes
+        if constexpr (EPI == kEpiFwd) {
+          const long long blk = 32LL * kColsPerWarp;
+          const long long stride = 2LL * Cfg::kEpiWarps * blk;  // between splits
+          float* base = ep.fix_ws + (static_cast<long long>(tile) * S_k * 2 + rank) *
+                                        Cfg::kEpiWarps * blk + e * blk;
+          float* mine = base + split * stride;
+          const int n0 = tn * BN + c_off;
+#pragma unroll 1
+          for (int c = 0; c < kColsPerWarp; c += 32) {
+            if (n0 + c >= sh.N) break;  // warp-uniform
+            uint32_t r[32];
+            ptx::tmem_ld32(t_row + c, r);
+            ptx::tmem_ld_wait();
+            float4* p = reinterpret_cast<float4*>(mine + (c / 32) * 1024 + lane * 4);
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4)
+              __stcg(p + j4 * 32, make_float4(__uint_as_float(r[4 * j4]),
+                                              __uint_as_float(r[4 * j4 + 1]),
+                                              __uint_as_float(r[4 * j4 + 2]),
+                                              __uint_as_float(r[4 * j4 + 3])));
+          }
+          __threadfence();
+          ptx::named_bar_sync(1, 32 * Cfg::kEpiWarps);
+          if (e == 0 && lane == 0) {
+            int* cnt = ep.fix_cnt + tile * 2 + rank;
+            const int last = atomicAdd(cnt, 1) == S_k - 1;
+            if (last) *cnt = 0;  // every split has arrived: ready for the next launch
+            *fix_last = last;
+          }
+          ptx::named_bar_sync(1, 32 * Cfg::kEpiWarps);
+          if (*fix_last) {
+            __threadfence();
+            FixSrc fx;
+            fx.base = base;
+            fx.stride = stride;
+            fx.S = S_k;
+            fx.self = split;
+            with_act<EPI>(ep, [&](auto A) {
+              epilogue_warp_vec<EPI, decltype(A)::value, true>(ep, sh, row_base, n0,
+                                                               kColsPerWarp, t_row, T, fx);
+            });
+          }
+        }
+      } else if (ep.partial_slab) {
         // split-K into partial slabs (conv wgrad): this split's own fp32
         // slab, plain stores; an in-order reduction consumes the slabs
         if constexpr (EPI == kEpiFwd) {

@@ -87,6 +87,20 @@ struct EpiParams {
   // without bias / activation): split z writes y32 + z * partial_slab; a
   // separate in-order reduction consumes them (conv wgrad, conv_ops.cu)
   long long partial_slab;
+  // split-K with an in-kernel fixup (forward, pair kernel): every split of a
+  // tile stores its fp32 partial to fix_ws (its own slot, warp-blocked), then
+  // bumps fix_cnt[tile * 2 + CTA rank]; the last to arrive sums the S
+  // partials in split order (its own from TMEM) and runs the epilogue.  The
+  // last arriver resets the counter, so it is zero between launches.
+  float* fix_ws;
+  int* fix_cnt;
+};
+
+// Where the fixup epilogue finds the partials of its tile (see EpiParams).
+struct FixSrc {
+  const float* base = nullptr;  // split 0's block of this warp
+  long long stride = 0;         // floats between splits
+  int S = 0, self = 0;
 };
 
 }  // namespace pb

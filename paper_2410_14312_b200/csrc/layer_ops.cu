@@ -126,7 +126,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
       return e ? std::max(1, std::atoi(e)) : 1;
     }();
     if (EPI != kEpiWgradSgd && tpp > 1) cap = std::min(cap, (tiles + tpp - 1) / tpp);
-    const int units = tiles * (g.ep.partial_slab ? std::max(1, g.sh.splits) : 1);
+    const int units =
+        tiles * ((g.ep.partial_slab || g.ep.fix_cnt) ? std::max(1, g.sh.splits) : 1);
     const int pairs = std::min(units, std::max(1, cap));
     kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
                                                                       g.maps);
@@ -296,9 +297,52 @@ int fwd_splits(int rows, int N, int K) {
   return std::max(1, s);
 }
 
+// Pair forward with the in-kernel split-K fixup (EpiParams::fix_cnt): the
+// tile width the forward would use and the split count that makes its tiles
+// fill one wave of CTA pairs (>= 8 k-blocks per split); 1 = no split.
+// Opt-in (PIPESIM_FWD_FIX=1 automatic split count, =<n> forces n > 1): the
+// last arriver's partial reads are latency-bound (26.7 us for a 256 x 4096 x
+// 4096 forward against 18 us for the single-CTA cluster split), so the
+// cluster split stays the default.
+namespace {
+int fix_env() {
+  static const int v = [] {
+    const char* e = std::getenv("PIPESIM_FWD_FIX");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+int fix_bn(int rows, int N) {
+  int bn = N > 128 ? 256 : 128;
+  if (rows > 128 && wide_tiles(rows, N)) bn = 512;
+  return bn;
+}
+int fix_splits(int rows, int N, int K, int bn) {
+  if (!pair_allowed() || splitk_env() == 0) return 1;
+  const int tiles = ((rows + 255) / 256) * ((N + bn - 1) / bn);
+  const int kb = (K + 63) / 64;
+  const int pairs = sm_count() / 2;
+  if (fix_env() < 1) return 1;
+  int S = fix_env() > 1 ? fix_env() : (tiles * 4 >= pairs * 3 ? 1 : pairs / tiles);
+  S = std::max(1, std::min(S, kb / 8));
+  const int kbps = (kb + S - 1) / S;
+  return (kb + kbps - 1) / kbps;
+}
+}  // namespace
+
+size_t fwd_fix_floats(int rows, int N, int K) {
+  const int bn = fix_bn(rows, N);
+  const int S = fix_splits(rows, N, K, bn);
+  if (S <= 1) return 0;
+  return static_cast<size_t>(S) * ((rows + 255) / 256) * 256 * (((N + bn - 1) / bn) * bn);
+}
+
+int fwd_fix_counters(int rows, int N) { return 2 * ((rows + 255) / 256) * ((N + 127) / 128); }
+
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
-                    float* y32, int ld_y32, int y_row_off, bool allow_split, bool verify) {
+                    float* y32, int ld_y32, int y_row_off, bool allow_split, bool verify,
+                    float* fix_ws, int* fix_cnt) {
   GemmLaunch g;
   if (verify) {
     g.simt = true;
@@ -316,6 +360,34 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
     g.ep.ld_y32 = ld_y32;
     g.ep.y_row_off = y_row_off;
     return g;
+  }
+  // one stage per GPU (latency): CTA-pair split-K with the in-kernel fixup
+  // when a workspace is given, else the single-CTA cluster split
+  int fix = 1;
+  const int fbn = fix_bn(rows, w.rows);
+  if (allow_split && fix_ws && fix_cnt) fix = fix_splits(rows, w.rows, x.cols, fbn);
+  if (fix > 1) {
+    g.bn = fbn;
+    g.pair = true;
+    g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
+    g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
+    g.sh = GemmShape{rows, w.rows, x.cols, x_row_off, 0, 0, 0, fix, 0};
+    const int kb = (x.cols + 63) / 64;
+    g.sh.kb_per_split = (kb + fix - 1) / fix;
+    g.ep = empty_epi(kEpiFwd);
+    g.ep.bias = bias;
+    g.ep.act = act;
+    g.ep.y16 = y16;
+    g.ep.ld_y16 = ld_y16;
+    g.ep.y32 = y32;
+    g.ep.ld_y32 = ld_y32;
+    g.ep.y_row_off = y_row_off;
+    vec_or_fallback(g.ep, kEpiFwd);
+    if (g.ep.rowwise == 2 && !g.ep.dbg_skip) {  // the fixup runs the vector epilogue
+      g.ep.fix_ws = fix_ws;
+      g.ep.fix_cnt = fix_cnt;
+      return g;
+    }
   }
   const int splits = allow_split || splitk_env() > 0 ? fwd_splits(rows, w.rows, x.cols) : 1;
   if (splits > 1) {  // single-CTA 128 x 128 tiles, one cluster of `splits` per tile
@@ -1135,8 +1207,12 @@ void launch_convert_f32_bf16(cudaStream_t st, const float* src, int rows,
                              int ld_dst) {
   if (rows <= 0 || cols <= 0) return;
   if ((ld_dst % 2) != 0) throw std::invalid_argument("bf16 rows must be 4-byte aligned");
-  to_bf16_kernel<float><<<std::min(rows, 148 * 4), 256, 0, st>>>(src, rows, cols, ld_src, dst,
-                                                                 ld_dst);
+  static const int grid_cap = [] {
+    const char* e = std::getenv("PIPESIM_CONV_GRID");
+    return e ? std::max(1, std::atoi(e)) : 148 * 4;
+  }();
+  to_bf16_kernel<float><<<std::min(rows, grid_cap), 256, 0, st>>>(src, rows, cols, ld_src, dst,
+                                                                  ld_dst);
   PB_CUDA(cudaGetLastError());
 }
 

@@ -48,11 +48,17 @@ struct GemmLaunch {
 // (plan_fwd's allow_split).
 int fwd_splits(int rows, int N, int K);
 
-// forward: out = act(x[rows, in] * w[out, in]^T + b)
+// forward: out = act(x[rows, in] * w[out, in]^T + b).  allow_split: a
+// skinny forward may split K (latency over SM-time): with fix_ws / fix_cnt
+// (fwd_fix_floats / fwd_fix_counters, counters zeroed once) on the CTA-pair
+// kernel with an in-kernel fixup, else on single-CTA clusters.
 GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
                     const float* bias, int act, __nv_bfloat16* y16, int ld_y16,
                     float* y32, int ld_y32, int y_row_off, bool allow_split = true,
-                    bool verify = false);
+                    bool verify = false, float* fix_ws = nullptr, int* fix_cnt = nullptr);
+// workspace floats / counters a split forward of this shape needs (0: no split)
+size_t fwd_fix_floats(int rows, int N, int K);
+int fwd_fix_counters(int rows, int N);
 // dgrad: d[rows, in] = (dz[rows,out] * w[out,in]) .* act'(xin)
 GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
                       int ld_xin, int act_prev, __nv_bfloat16* d, int ld_d,

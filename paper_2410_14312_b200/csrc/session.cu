@@ -165,6 +165,12 @@ struct Session::Impl {
     float* wg_ws = nullptr;    // conv wgrad split-K partial slabs (side stream)
     float* bias_ws = nullptr;  // conv bias-gradient row-block partials (bias stream)
     size_t wg_floats = 0, bias_floats = 0;
+    // split-K forwards (one stage per GPU): fixup partials + tile counters
+    // of the forward stream (its launches run one at a time)
+    float* fix_ws = nullptr;
+    int* fix_cnt = nullptr;
+    size_t fix_floats = 0;
+    int fix_counters = 0;
     std::vector<int> version_colour;         // [M+1]
     std::vector<int> mini_act;               // [M+1]
     int* cur_version = nullptr;
@@ -673,6 +679,12 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         I.split = false;
   }
 
+  // Skinny forwards split K (lower latency, more SM-time) when this process
+  // keeps few stages in flight; PIPESIM_SESSION_SPLIT=0/1 overrides.
+  bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
+  if (const char* e = std::getenv("PIPESIM_SESSION_SPLIT")) split_fwd = std::atoi(e) != 0;
+  if (I.v32) split_fwd = false;
+
   // ---------------- sizes
   I.n_out = c.widths.back();
   I.ld_x = ld8(c.widths.front());
@@ -724,6 +736,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         ab += (act_n[s] + 1) * bytes_of(static_cast<size_t>(c.B) * d.pre_elems, 2);
       if (d.first_conv)
         ab += act_n[s] * bytes_of(static_cast<size_t>(c.B) * d.h * d.w * d.ld_in, 2);
+      if (split_fwd && !d.conv) {
+        for (int j = 1; j <= U; ++j)
+          st.fix_floats = std::max(st.fix_floats, fwd_fix_floats(j * I.Rm, d.out, d.in));
+        st.fix_counters = std::max(st.fix_counters, fwd_fix_counters(c.B, d.out));
+      }
       if (d.conv) {
         int lds = 0;
         const size_t f = d.first_conv ? wgrad_partial_floats(d.out, d.ld_in, c.B * d.h * d.w, &lds)
@@ -735,6 +752,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     off += st.param_count;
     if (!I.local(s)) continue;
     wb += bytes_of(st.wg_floats, 4) + bytes_of(st.bias_floats, 4);
+    if (st.fix_floats) ab += bytes_of(st.fix_floats, 4) + bytes_of(st.fix_counters, 4);
     if (s > 0 && !I.local(s - 1))  // boundary buffers: received input + outgoing delta
       ab += 2 * act_n[s] * bytes_of(static_cast<size_t>(c.B) * st.layers.front().ain, 2 * I.sc);
     wb += pool_n[s] * bytes_of(1, 4) + bytes_of(1, 4);
@@ -812,6 +830,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
               ? I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].pre_elems)
               : nullptr);
     if (st.wg_floats) st.wg_ws = I.carve<float>(st.wg_floats);
+    if (st.fix_floats) {  // the arena is zeroed: counters start at 0
+      st.fix_ws = I.carve<float>(st.fix_floats);
+      st.fix_cnt = I.carve<int>(st.fix_counters);
+    }
     if (st.bias_floats) st.bias_ws = I.carve<float>(st.bias_floats);
   }
   I.x16 = I.carve<__nv_bfloat16>(rows * I.ld_x * I.sc);
@@ -953,10 +975,6 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     }
   }
 
-  // Skinny forwards split K (lower latency, more SM-time) when this process
-  // keeps few stages in flight; PIPESIM_SESSION_SPLIT=0/1 overrides.
-  bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
-  if (const char* e = std::getenv("PIPESIM_SESSION_SPLIT")) split_fwd = std::atoi(e) != 0;
 
   // per stage: pool colour of every version; previous occupant of each
   // mini-batch's activation slot (0: none)
@@ -1275,6 +1293,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       Impl::Op xw{OK::xwait};
       xw.stream = ns;
       xw.value = tk.k;
+      xw.dir = node.fwd ? 1 : 0;  // the forward converts the rows, the loss reads labels
       push(xw);
     }
     const int node_idx = static_cast<int>(I.node_meta.size());
@@ -1333,7 +1352,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           o.g = plan_fwd(x, in_off + r0, rows, w, ps.b32[l], d.act,
                          logits ? nullptr : as.out16[l], d.ld_out,
                          logits ? as.out32 : nullptr, I.n_out, r0,
-                         /*allow_split=*/split_fwd && !I.v32, /*verify=*/I.v32);
+                         /*allow_split=*/split_fwd, /*verify=*/I.v32, st.fix_ws, st.fix_cnt);
         }
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
@@ -1813,7 +1832,9 @@ void Session::read_stage_master(int stage, int version, double* out) {
 namespace {
 void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType xt,
                  const void* y, HostDType yt, cudaStream_t st, cudaStream_t conv = nullptr,
-                 cudaEvent_t copied = nullptr);
+                 cudaEvent_t copied = nullptr, bool skip_convert = false);
+void convert_rows(Session::Impl& I, size_t r0, size_t n, HostDType xt, HostDType yt,
+                  cudaStream_t cs, bool do_x = true, bool do_y = true);
 }  // namespace
 
 void Session::upload(const void* x, HostDType xt, const void* y, HostDType yt,
@@ -1849,7 +1870,7 @@ namespace {
 // to back on the copy engine and never wait for SMs).
 void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType xt,
                  const void* y, HostDType yt, cudaStream_t st, cudaStream_t conv,
-                 cudaEvent_t copied) {
+                 cudaEvent_t copied, bool skip_convert) {
   const int in = I.cfg.widths.front();
   const size_t rows = static_cast<size_t>(I.M) * I.B;
   char* xs = static_cast<char*>(I.stage_buf);
@@ -1882,25 +1903,42 @@ void upload_rows(Session::Impl& I, size_t r0, size_t n, const void* x, HostDType
     throw std::invalid_argument("y must be f64, f32 or int32 labels");
   }
   I.use_labels = yt == HostDType::labels_i32;
+  if (copied) PB_CUDA(cudaEventRecord(copied, st));
+  if (skip_convert) return;
   // ---- conversions
   cudaStream_t cs = st;
   if (conv && conv != st) {
-    PB_CUDA(cudaEventRecord(copied, st));
     PB_CUDA(cudaStreamWaitEvent(conv, copied, 0));
     cs = conv;
   }
-  if (xt == HostDType::f64 || xt == HostDType::f32) {
+  convert_rows(I, r0, n, xt, yt, cs);
+}
+
+// Conversion of rows [r0, r0 + n) from the staging buffer into the device
+// layout (f64 / f32 x -> the bf16 operand or fp32 verify rows; f64 y -> fp32).
+void convert_rows(Session::Impl& I, size_t r0, size_t n, HostDType xt, HostDType yt,
+                  cudaStream_t cs, bool do_x, bool do_y) {
+  const int in = I.cfg.widths.front();
+  const size_t rows = static_cast<size_t>(I.M) * I.B;
+  char* xs = static_cast<char*>(I.stage_buf);
+  char* ys = xs + rows * in * 8;
+  __nv_bfloat16* xdst = I.x16 + r0 * I.ld_x * I.sc;
+  float* ydst = I.y32 + r0 * I.n_out;
+  const size_t xes = xt == HostDType::f64 ? 8 : xt == HostDType::f32 ? 4 : 2;
+  char* xb = xs + r0 * in * xes;
+  char* yb = ys + r0 * I.n_out * 8;
+  if (do_x && (xt == HostDType::f64 || xt == HostDType::f32)) {
     if (I.v32)
       launch_rows_to_f32(cs, xb, xt == HostDType::f64, static_cast<int>(n), in, in,
                          reinterpret_cast<float*>(xdst), I.ld_x);
     else if (xt == HostDType::f64)
       launch_convert_f64_bf16(cs, reinterpret_cast<const double*>(xb), static_cast<int>(n), in,
                               in, xdst, I.ld_x);
-    else
+    else if (!std::getenv("PIPESIM_H2D_DBG"))  // timing experiment: skip (wrong numerics)
       launch_convert_f32_bf16(cs, reinterpret_cast<const float*>(xb), static_cast<int>(n), in,
                               in, xdst, I.ld_x);
   }
-  if (yt == HostDType::f64)
+  if (do_y && yt == HostDType::f64)
     launch_convert_f64_f32(cs, reinterpret_cast<const double*>(yb), ydst, n * I.n_out);
 }
 
@@ -1928,11 +1966,18 @@ void issue(Session::Impl& I, cudaStream_t origin) {
   cudaEvent_t fork = I.fork_ev;
   PB_CUDA(cudaEventRecord(fork, origin));
   for (cudaStream_t st : streams) PB_CUDA(cudaStreamWaitEvent(st, fork, 0));
-  if (I.streaming)  // mini-batch k's rows: H2D + conversion, then x_ready[k]
+  // mini-batch k's rows: the H2D copies run back to back on the copy engine
+  // (copy_ev[k]); the conversion of x (f32 / f64 hosts) runs on stage 1's
+  // forward stream right before its first forward of mini k (xwait), where
+  // the rows are needed -- a conversion kernel on a side stream cost ~7 ms
+  // per 16 x 4096 step (measured), against ~0.25 ms of conversion work.
+  // PIPESIM_H2D_SIDE=1 restores the side-stream conversion (x_ready[k]).
+  const bool side_conv = std::getenv("PIPESIM_H2D_SIDE") != nullptr;
+  if (I.streaming)
     for (int k = 1; k <= I.M; ++k) {
       upload_rows(I, static_cast<size_t>(k - 1) * I.B, I.B, I.host_in.x, I.host_in.xt,
-                  I.host_in.y, I.host_in.yt, I.h2d, I.h2dc, I.copy_ev[k]);
-      PB_CUDA(cudaEventRecord(I.x_ready[k], I.h2dc));
+                  I.host_in.y, I.host_in.yt, I.h2d, I.h2dc, I.copy_ev[k], !side_conv);
+      if (side_conv) PB_CUDA(cudaEventRecord(I.x_ready[k], I.h2dc));
     }
   for (const auto& o : I.ops) {
     cudaStream_t s = I.stream_of(o.stream);
@@ -1993,7 +2038,17 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         if (I.profiling) PB_CUDA(cudaEventRecord(I.mark_ev[o.value], s));
         break;
       case OK::xwait:
-        if (I.streaming) PB_CUDA(cudaStreamWaitEvent(s, I.x_ready[o.value], 0));
+        if (I.streaming) {
+          if (std::getenv("PIPESIM_H2D_SIDE")) {
+            PB_CUDA(cudaStreamWaitEvent(s, I.x_ready[o.value], 0));
+          } else {
+            PB_CUDA(cudaStreamWaitEvent(s, I.copy_ev[o.value], 0));
+            // stage 1's first forward of mini k converts its x rows, the loss
+            // its (f64) targets
+            convert_rows(I, static_cast<size_t>(o.value - 1) * I.B, I.B, I.host_in.xt,
+                         I.host_in.yt, s, o.dir == 1, o.dir == 0);
+          }
+        }
         break;
       case OK::digest:
         I.digest->enqueue(I.dplans[o.value], I.d_digest + o.value, s);
@@ -2081,7 +2136,9 @@ EpochResult Session::train_epoch_host(const void* x, HostDType xt, const void* y
     int lo = 0, hi = 0;
     PB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     PB_CUDA(cudaStreamCreateWithFlags(&I.h2d, cudaStreamNonBlocking));
-    PB_CUDA(cudaStreamCreateWithPriority(&I.h2dc, cudaStreamNonBlocking, hi));
+    const char* pe = std::getenv("PIPESIM_H2D_PRIO");
+    PB_CUDA(cudaStreamCreateWithPriority(&I.h2dc, cudaStreamNonBlocking,
+                                         pe && std::atoi(pe) == 0 ? lo : hi));
     I.x_ready.assign(cfg_.M + 1, nullptr);
     I.copy_ev.assign(cfg_.M + 1, nullptr);
     for (int k = 1; k <= cfg_.M; ++k) {

@@ -215,3 +215,26 @@ def test_split_k_cluster_forward_deterministic(rows, inn, out):
     assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
     ref = torch.relu(x.float() @ w.float().T + b)
     assert _rel(ys[0], ref) < 2e-5
+
+
+@pytest.mark.parametrize("rows", [128, 256, 768, 1024])
+def test_linear_fwd_split_fixup_deterministic(rows):
+    """Skinny forwards split K over CTA pairs with the in-kernel fixup (the
+    last split of a tile sums the partials in split order): the result is
+    run-to-run bit-identical and matches fp32 torch (opt-in path:
+    PIPESIM_FWD_FIX=1; with the default the cluster split runs here)."""
+    inn = out = 4096
+    x = K.padded_bf16(rows, inn)
+    x.copy_(torch.rand(rows, inn, device="cuda"))
+    w = K.padded_bf16(out, inn)
+    w.copy_((torch.rand(out, inn, device="cuda") * 2 - 1) / inn ** 0.5)
+    b = torch.rand(out, device="cuda") - 0.5
+    ys = []
+    for _ in range(3):
+        y32 = torch.zeros(rows, out, device="cuda")
+        K.linear_fwd(x, w, b, "relu", y32=y32)
+        ys.append(y32)
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    ref = torch.relu(x.float() @ w.float().T + b)
+    assert _rel(ys[0], ref) < 2e-5

@@ -3,7 +3,8 @@ sys.path.insert(0, "/root/repo")
 from paper_2410_14312_b200 import pipesim as P
 net = P.NetworkSpec([4096] * 17, ["relu"] * 15 + ["linear"], "softmax_cross_entropy")
 W, N, B, M = 8, 8, 1024, 32
-s = P.Session(net, W, N, B, M, 0.05, "timeprest")
+import os
+s = P.Session(net, W, N, B, M, 0.05, "timeprest", use_graph=os.environ.get("NOGRAPH") is None)
 s.load_params(P.init_network_params(net, 1))
 x, lab = P.make_classification_task(M * B, 4096, 4096, seed=7, as_labels=True, dtype=np.float32)
 xh = torch.from_numpy(x).pin_memory(); yh = torch.from_numpy(lab).pin_memory()
