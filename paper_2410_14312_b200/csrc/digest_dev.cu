@@ -42,6 +42,14 @@ __device__ __forceinline__ uint32_t apply(uint64_t f, uint32_t n) {
   return static_cast<uint32_t>(f >> (4 * n)) & 15u;
 }
 
+// byte j (compile-time after unrolling) of a 32-byte slot held in registers
+__device__ __forceinline__ uint32_t slot_byte(const uint4 (&q)[2], int j) {
+  const uint4 v = q[j >> 4];
+  const int w = (j >> 2) & 3;
+  const uint32_t x = w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+  return (x >> (8 * (j & 3))) & 0xFFu;
+}
+
 __device__ __forceinline__ float fetch(const DigestSpan& sp, int64_t off) {
   if (sp.f32) return __ldg(sp.f32 + off);
   const uint32_t h = __bfloat16_as_ushort(sp.hi[off]);
@@ -103,7 +111,9 @@ __device__ uint32_t block_incoming(uint64_t m, uint32_t block_in, uint64_t* sh, 
   return r;
 }
 
-// (A) format + low-nibble maps
+// (A) format + low-nibble maps (R values per thread: 16, or 4 for small
+// segments so that they still fill the SMs)
+template <int R>
 __global__ void __launch_bounds__(kT) dg_format_lo(const DigestSpan* __restrict__ spans,
                                                    int nspans, int64_t seg0, int64_t segn,
                                                    char* __restrict__ slots,
@@ -112,10 +122,10 @@ __global__ void __launch_bounds__(kT) dg_format_lo(const DigestSpan* __restrict_
                                                    uint64_t* __restrict__ bmap) {
   __shared__ uint64_t sh[kT / 32];
   const int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
-  const int64_t a = t * kR;
+  const int64_t a = t * R;
   uint64_t S = kIdent;
   if (a < segn) {
-    const int64_t b = min(segn, a + kR);
+    const int64_t b = min(segn, a + R);
     int si = find_span(spans, nspans, seg0 + a);
     DigestSpan sp = spans[si];
     int64_t local = seg0 + a - sp.start;
@@ -141,8 +151,11 @@ __global__ void __launch_bounds__(kT) dg_format_lo(const DigestSpan* __restrict_
       dst[0] = buf.q[0];
       dst[1] = buf.q[1];
       lens[i] = static_cast<uint8_t>(n);
-      for (int j = 0; j < n; ++j) {
-        const uint64_t x = S ^ (static_cast<uint64_t>(static_cast<uint8_t>(buf.ch[j]) & 15u) * kRep);
+      const uint4 q[2] = {buf.q[0], buf.q[1]};
+#pragma unroll
+      for (int j = 0; j < kSlot; ++j) {  // registers only (no dynamic indexing)
+        if (j >= n) break;
+        const uint64_t x = S ^ (static_cast<uint64_t>(slot_byte(q, j) & 15u) * kRep);
         S = nib_mul3(x);
       }
     }
@@ -165,14 +178,19 @@ __global__ void __launch_bounds__(1024) dg_chain(const uint64_t* __restrict__ bm
   for (int b = b0; b < b1; ++b) m = compose(m, bmap[b]);
   g[threadIdx.x] = m;
   __syncthreads();
-  // serial chain over the 1024 group maps (applications only: cheap)
-  if (threadIdx.x == 0) {
-    uint32_t n = static_cast<uint32_t>(*state >> shift) & 15u;
-    for (int i = 0; i < 1024; ++i) {
-      gn[i] = n;
-      n = apply(g[i], n);
-    }
+  // exclusive scan of the 1024 group maps in order (Hillis-Steele: 10
+  // compose steps instead of a 1024-long serial chain), then each group's
+  // incoming nibble is its prefix applied to the segment's incoming nibble
+  uint64_t inc = m;
+  for (int d = 1; d < 1024; d <<= 1) {
+    const uint64_t prev = threadIdx.x >= d ? g[threadIdx.x - d] : kIdent;
+    __syncthreads();
+    inc = compose(prev, inc);
+    g[threadIdx.x] = inc;
+    __syncthreads();
   }
+  const uint32_t n0 = static_cast<uint32_t>(*state >> shift) & 15u;
+  gn[threadIdx.x] = threadIdx.x == 0 ? n0 : apply(g[threadIdx.x - 1], n0);
   __syncthreads();
   uint32_t n = gn[threadIdx.x];
   for (int b = b0; b < b1; ++b) {
@@ -182,6 +200,7 @@ __global__ void __launch_bounds__(1024) dg_chain(const uint64_t* __restrict__ bm
 }
 
 // (B) high-nibble maps given the low-nibble trajectory
+template <int R>
 __global__ void __launch_bounds__(kT) dg_hi(const char* __restrict__ slots,
                                             const uint8_t* __restrict__ lens, int64_t segn,
                                             uint64_t* __restrict__ tmap,
@@ -193,22 +212,19 @@ __global__ void __launch_bounds__(kT) dg_hi(const char* __restrict__ slots,
   const int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   const uint32_t lo_in = block_incoming(tmap[t], bin[blockIdx.x], sh, shn);
   tlo[t] = static_cast<uint8_t>(lo_in);
-  const int64_t a = t * kR;
+  const int64_t a = t * R;
   uint64_t H = kIdent;
   if (a < segn) {
-    const int64_t b = min(segn, a + kR);
+    const int64_t b = min(segn, a + R);
     uint32_t lo = lo_in;
     for (int64_t i = a; i < b; ++i) {
       const int n = lens[i];
       const uint4* src = reinterpret_cast<const uint4*>(slots + i * kSlot);
-      union {
-        char ch[kSlot];
-        uint4 q[2];
-      } buf;
-      buf.q[0] = src[0];
-      buf.q[1] = src[1];
-      for (int j = 0; j < n; ++j) {
-        const uint32_t c = static_cast<uint8_t>(buf.ch[j]);
+      const uint4 q[2] = {src[0], src[1]};
+#pragma unroll
+      for (int j = 0; j < kSlot; ++j) {
+        if (j >= n) break;
+        const uint32_t c = slot_byte(q, j);
         const uint32_t xl = (lo ^ c) & 15u;
         const uint32_t K = (11u * xl + ((3u * xl) >> 4)) & 15u;
         const uint64_t x = H ^ (static_cast<uint64_t>(c >> 4) * kRep);
@@ -223,6 +239,7 @@ __global__ void __launch_bounds__(kT) dg_hi(const char* __restrict__ slots,
 }
 
 // (C) exact fold from the known low byte: affine map h_out = c + m * h_in
+template <int R>
 __global__ void __launch_bounds__(kT) dg_exact(const char* __restrict__ slots,
                                                const uint8_t* __restrict__ lens, int64_t segn,
                                                const uint64_t* __restrict__ tmap,
@@ -236,20 +253,17 @@ __global__ void __launch_bounds__(kT) dg_exact(const char* __restrict__ slots,
   const uint32_t hi_in = block_incoming(tmap[t], bin[blockIdx.x], sh, shn);
   const uint64_t l_in = (hi_in << 4) | tlo[t];
   uint64_t h = l_in, m = 1;
-  const int64_t a = t * kR;
+  const int64_t a = t * R;
   if (a < segn) {
-    const int64_t b = min(segn, a + kR);
+    const int64_t b = min(segn, a + R);
     for (int64_t i = a; i < b; ++i) {
       const int n = lens[i];
       const uint4* src = reinterpret_cast<const uint4*>(slots + i * kSlot);
-      union {
-        char ch[kSlot];
-        uint4 q[2];
-      } buf;
-      buf.q[0] = src[0];
-      buf.q[1] = src[1];
-      for (int j = 0; j < n; ++j) {
-        h = (h ^ static_cast<uint8_t>(buf.ch[j])) * kP;
+      const uint4 q[2] = {src[0], src[1]};
+#pragma unroll
+      for (int j = 0; j < kSlot; ++j) {
+        if (j >= n) break;
+        h = (h ^ slot_byte(q, j)) * kP;
         m *= kP;
       }
     }
@@ -368,12 +382,24 @@ void DeviceDigest::enqueue(const Plan& p, uint64_t* d_state, cudaStream_t st) {
   PB_CUDA(cudaGetLastError());
   for (int64_t s0 = 0; s0 < p.total; s0 += seg_) {
     const int64_t n = std::min(seg_, p.total - s0);
-    const int nb = static_cast<int>((n + kVB - 1) / kVB);
-    dg_format_lo<<<nb, kT, 0, st>>>(p.d_spans, p.nspans, s0, n, slots_, lens_, tmap_, bmap_);
-    dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 0, bin_);
-    dg_hi<<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, bmap_);
-    dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 4, bin_);
-    dg_exact<<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, baff_);
+    // small segments: 4 values per thread (4x the blocks; fits the scratch
+    // sized for 16 per thread when n <= seg / 4)
+    const bool small = n * 4 <= seg_;
+    const int64_t vb = small ? kT * 4 : kVB;
+    const int nb = static_cast<int>((n + vb - 1) / vb);
+    if (small) {
+      dg_format_lo<4><<<nb, kT, 0, st>>>(p.d_spans, p.nspans, s0, n, slots_, lens_, tmap_, bmap_);
+      dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 0, bin_);
+      dg_hi<4><<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, bmap_);
+      dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 4, bin_);
+      dg_exact<4><<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, baff_);
+    } else {
+      dg_format_lo<kR><<<nb, kT, 0, st>>>(p.d_spans, p.nspans, s0, n, slots_, lens_, tmap_, bmap_);
+      dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 0, bin_);
+      dg_hi<kR><<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, bmap_);
+      dg_chain<<<1, 1024, 0, st>>>(bmap_, nb, d_state, 4, bin_);
+      dg_exact<kR><<<nb, kT, 0, st>>>(slots_, lens_, n, tmap_, tlo_, bin_, baff_);
+    }
     dg_finish<<<1, 1024, 0, st>>>(baff_, nb, d_state);
     PB_CUDA(cudaGetLastError());
   }
