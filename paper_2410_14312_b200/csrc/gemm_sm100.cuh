@@ -1202,6 +1202,11 @@ struct Gemm2Cfg {
   static_assert(kSmem <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
+template <class Cfg>
+__device__ __forceinline__ void conv_loads_b(const GemmShape& sh, const CUtensorMap* tb,
+                                             uint32_t fb, uint8_t* b_dst, int k0, int tap, int c0,
+                                             int n_tile, uint32_t rank);
+
 // Operand loads of one k-block of an implicit-GEMM 3x3 convolution (pad 1,
 // stride 1, NHWC; GemmShape::conv).  K is tap-major: k = tap * C + channel,
 // tap = 3 * r + s, so a 64-wide k-block is one tap and 64 channels.
@@ -1216,6 +1221,16 @@ __device__ __forceinline__ void conv_loads_fd(const GemmShape& sh, const CUtenso
   // reads dz at window offset t and pairs it with the weights of tap 8 - t
   const int tap = k0 / sh.conv_c, c0 = k0 - tap * sh.conv_c;
   ptx::tma_load_im2col_pair(a_dst, ta, fb, c0, px_w - 1, px_h - 1, px_n, tap % 3, tap / 3);
+  conv_loads_b<Cfg>(sh, tb, fb, b_dst, k0, tap, c0, n_tile, rank);
+}
+
+// The B operand of k-block (tap, channel chunk c0) of a conv forward (W
+// [Cout, 9C], K-major) or dgrad (W viewed [Cout][9][Cin], flipped tap,
+// MN-major).
+template <class Cfg>
+__device__ __forceinline__ void conv_loads_b(const GemmShape& sh, const CUtensorMap* tb,
+                                             uint32_t fb, uint8_t* b_dst, int k0, int tap, int c0,
+                                             int n_tile, uint32_t rank) {
 #pragma unroll
   for (int j = 0; j < Cfg::kSub; ++j) {
     const int nbj = n_tile + j * Cfg::kMmaN + static_cast<int>(rank) * (Cfg::kMmaN / 2);
@@ -1287,7 +1302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Cfg::kBarOff + 496);
   volatile int* fix_last = reinterpret_cast<volatile int*>(smem + Cfg::kBarOff + 500);
   static_assert(sizeof(uint64_t) * (2 * Cfg::kStages + 4 +
-                                    (EPI == kEpiWgradSgd ? Cfg::kSgdBufs * Cfg::kEpiWarps : 0)) <=
+                                    (EPI == kEpiWgradSgd ? Cfg::kSgdBufs * Cfg::kEpiWarps : 4)) <=
                     496,
                 "barrier region overlaps the TMEM address slot");
 
@@ -1296,7 +1311,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   const uint32_t rank = ptx::cluster_ctarank();
   const int pair = blockIdx.x / 2;
   const int num_pairs = gridDim.x / 2;
-  const int tiles_m = (sh.M + 255) / 256;
+  // halo conv tiles (GemmShape::halo_tw): strips of tw pixels, two per pair
+  // tile; the operand ring becomes two patch buffers + S_h B-only stages
+  const bool halo = EPI != kEpiWgradSgd && (sh.conv == 1 || sh.conv == 3) && sh.halo_tw > 0;
+  const int tw = sh.halo_tw;
+  const int n_strips = halo ? sh.M / tw : 0;
+  constexpr int kPatchBuf = 48 * 1024;  // {64 ch, <= 128 px, 3 rows} + over-read rows
+  constexpr int S_h = (S * Cfg::kStageBytes - 2 * kPatchBuf) / Cfg::kBHalf < S
+                          ? (S * Cfg::kStageBytes - 2 * kPatchBuf) / Cfg::kBHalf
+                          : S;
+  uint8_t* patch0 = smem;
+  uint8_t* sBh = smem + 2 * kPatchBuf;
+  uint64_t* pbar = tempty_bar + 2;  // [0..1] patch full, [2..3] patch empty (not SGD)
+  const int tiles_m = halo ? (n_strips + 1) / 2 : (sh.M + 255) / 256;
   const int tiles_n = (sh.N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int kb_all = (sh.K + Cfg::kBK - 1) / Cfg::kBK;
@@ -1319,6 +1346,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], 2);  // one arrival per CTA of the pair
     }
+    if (halo)
+      for (int i = 0; i < 4; ++i) ptx::mbar_init(&pbar[i], 1);
     if constexpr (EPI == kEpiWgradSgd)
       if (ep.rowwise == 3) {
         for (int i = 0; i < Cfg::kSgdBufs * Cfg::kEpiWarps; ++i) ptx::mbar_init(&sgd_bar[i], 1);
@@ -1339,10 +1368,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs), completion on the leader's barrier
-      int it = 0;
+      int it = 0, pit = 0;
       for (int u = pair; u < num_units; u += num_pairs) {
         const int tile = u / S_k, split = u % S_k;
         const int tm = tile / tiles_n, tn = tile % tiles_n;
+        if (halo) {
+          // this CTA's strip (the second strip of an odd last tile loads
+          // strip 0: its rows are never stored)
+          const int strip = 2 * tm + static_cast<int>(rank);
+          const int hw = sh.conv_h * sh.conv_w;
+          const int p = (strip < n_strips ? strip : 0) * tw + sh.a_mn_off;
+          const int img = p / hw, hh = (p - img * hw) / sh.conv_w;
+          const int w0 = p - img * hw - hh * sh.conv_w;
+          const uint32_t patch_bytes = 128u * static_cast<uint32_t>(tw + 2) * 3u;
+          for (int c0 = 0; c0 < sh.conv_c; c0 += 64) {
+            const int pb = pit & 1;
+            if (pit >= 2) ptx::mbar_wait(&pbar[2 + pb], ((pit >> 1) - 1) & 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&pbar[pb], 2 * patch_bytes);
+            ptx::tma_load_4d_pair(patch0 + pb * kPatchBuf, &tmap_a, ptx::map_to_rank(&pbar[pb], 0),
+                                  c0, w0 - 1, hh - 1, img);
+            ++pit;
+            for (int tap = 0; tap < 9; ++tap, ++it) {
+              const int s = it % S_h;
+              if (it >= S_h) ptx::mbar_wait(&empty_bar[s], ((it / S_h) - 1) & 1);
+              const uint32_t fb = ptx::map_to_rank(&full_bar[s], 0);
+              if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * Cfg::kBHalf);
+              conv_loads_b<Cfg>(sh, &tmap_b, fb, sBh + s * Cfg::kBHalf, tap * sh.conv_c + c0, tap,
+                                c0, tn * BN, rank);
+            }
+          }
+          continue;
+        }
         const int m0 = tm * 256 + static_cast<int>(rank) * 128;
         const int kb_lo = split * kbps, kb_hi = min(kb_all, kb_lo + kbps);
         // implicit-GEMM conv, A = im2col: this CTA's first output pixel
@@ -1409,7 +1465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
     if (rank == 0 && lane == 0) {
       // ---------------- MMA issuer (leader only)
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, Cfg::kMmaN, A_MN, B_MN);
-      int it = 0, local = 0;
+      int it = 0, local = 0, pit = 0;
       for (int u = pair; u < num_units; u += num_pairs, ++local) {
         const int split = u % S_k;
         const int num_kb = min(kb_all, (split + 1) * kbps) - split * kbps;
@@ -1418,6 +1474,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
         ptx::mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        if (halo) {
+          // per channel chunk: the patch, then the 9 taps as shifted views of
+          // it (tap t = (r, s) starts at patch row r * (tw + 2) + s)
+          for (int c0 = 0; c0 < sh.conv_c; c0 += 64, ++pit) {
+            const int pb = pit & 1;
+            ptx::mbar_wait(&pbar[pb], (pit >> 1) & 1);
+            ptx::tc_fence_after();
+            const uint32_t pa = ptx::smem_u32(patch0 + pb * kPatchBuf);
+            for (int tap = 0; tap < 9; ++tap, ++it) {
+              const int s = it % S_h;
+              ptx::mbar_wait(&full_bar[s], (it / S_h) & 1);
+              ptx::tc_fence_after();
+              const uint32_t a_row = pa + static_cast<uint32_t>((tap / 3) * (tw + 2) + tap % 3) * 128u;
+              const uint32_t b_addr = ptx::smem_u32(sBh + s * Cfg::kBHalf);
+#pragma unroll
+              for (int kk = 0; kk < Cfg::kBK / 16; ++kk) {
+                const uint64_t a_desc = ptx::smem_desc_sw128(a_row + kk * 32, 16, 1024);
+#pragma unroll
+                for (int j = 0; j < Cfg::kSub; ++j) {
+                  const uint32_t bj = b_addr + j * Cfg::kBSub;
+                  const uint64_t b_desc =
+                      B_MN ? ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024)
+                           : ptx::smem_desc_sw128(bj + kk * 32, 16, 1024);
+                  ptx::mma_bf16_pair(d_tmem + j * Cfg::kMmaN, a_desc, b_desc, idesc,
+                                     (c0 | tap | kk) != 0);
+                }
+              }
+              ptx::mma_commit_pair(&empty_bar[s], 0x3);
+            }
+            ptx::mma_commit_pair(&pbar[2 + pb], 0x3);
+          }
+          ptx::mma_commit_pair(&tfull_bar[acc], 0x3);
+          continue;
+        }
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % S;
           ptx::mbar_wait(&full_bar[s], (it / S) & 1);
@@ -1488,7 +1578,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       prefetch_master(u + num_pairs);
       ptx::mbar_wait(&tfull_bar[acc], use & 1);
       ptx::tc_fence_after();
-      const int row_base = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
+      // halo strips: this CTA's rows are its strip's tw pixels
+      GemmShape she = sh;
+      int row_base = tm * 256 + static_cast<int>(rank) * 128 + q * 32;
+      if (halo) {
+        const int strip = 2 * tm + static_cast<int>(rank);
+        row_base = strip * tw + q * 32;
+        she.M = min(sh.M, strip * tw + tw);
+      }
       const uint32_t t_row =
           tmem_base + acc * BN + c_off + (static_cast<uint32_t>(q * 32) << 16);
       if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && split == 0 && rank == 0 &&
@@ -1536,7 +1633,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             fx.S = S_k;
             fx.self = split;
             with_act<EPI>(ep, [&](auto A) {
-              epilogue_warp_vec<EPI, decltype(A)::value, true>(ep, sh, row_base, n0,
+              epilogue_warp_vec<EPI, decltype(A)::value, true>(ep, she, row_base, n0,
                                                                kColsPerWarp, t_row, T, fx);
             });
           }
@@ -1547,7 +1644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
         if constexpr (EPI == kEpiFwd) {
           EpiParams epp = ep;
           epp.y32 = ep.y32 + static_cast<size_t>(split) * ep.partial_slab;
-          epilogue_warp_vec<EPI, kLinear>(epp, sh, row_base, tn * BN + c_off, kColsPerWarp,
+          epilogue_warp_vec<EPI, kLinear>(epp, she, row_base, tn * BN + c_off, kColsPerWarp,
                                           t_row, T);
         }
       } else if (ep.dbg_skip & 1) {
@@ -1570,17 +1667,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
         }
       } else if (ep.rowwise == 2) {
         with_act<EPI>(ep, [&](auto A) {
-          epilogue_warp_vec<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+          epilogue_warp_vec<EPI, decltype(A)::value>(ep, she, row_base, tn * BN + c_off,
                                                      kColsPerWarp, t_row, T);
         });
       } else if (ep.rowwise) {
         with_act<EPI>(ep, [&](auto A) {
-          epilogue_warp_rows<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+          epilogue_warp_rows<EPI, decltype(A)::value>(ep, she, row_base, tn * BN + c_off,
                                                       kColsPerWarp, t_row);
         });
       } else {
         with_act<EPI>(ep, [&](auto A) {
-          epilogue_warp_tile<EPI, decltype(A)::value>(ep, sh, row_base, tn * BN + c_off,
+          epilogue_warp_tile<EPI, decltype(A)::value>(ep, she, row_base, tn * BN + c_off,
                                                       kColsPerWarp, t_row, T);
         });
       }

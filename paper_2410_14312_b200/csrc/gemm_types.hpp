@@ -31,6 +31,15 @@ struct GemmShape {
   // a_mn_off (modes 1, 3) / b_k_off (mode 2) / a_k_off (mode 4) are pixel
   // offsets.
   int conv = 0, conv_h = 0, conv_w = 0, conv_c = 0;
+  // Halo tiles (modes 1 and 3, image width a multiple of halo_tw): a CTA
+  // covers halo_tw consecutive pixels of one image row (a strip); per
+  // 64-channel chunk one TMA load brings the strip's 3-row halo patch
+  // {64 ch, halo_tw + 2 px, 3 rows} (tensor map `ta`, 4-D tiled) and the 9
+  // taps are 9 shifted views of it (the UMMA descriptor starts at any 128-byte
+  // row of the swizzled patch: tools/umma_shift_probe.cu).  Strip g = GEMM
+  // rows [g * halo_tw, (g + 1) * halo_tw); CTA rank r of pair tile t takes
+  // strip 2t + r.  0 = im2col loads, one per tap.
+  int halo_tw = 0;
 };
 
 // Tensor maps of the TMA epilogue of wgrad+SGD (EpiParams::rowwise == 3).

@@ -115,7 +115,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
   if (g.pair) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>;
     constexpr int smem = Gemm2Cfg<BN, EPI>::kSmem;
-    const int tiles = ((g.sh.M + 255) / 256) * ((g.sh.N + BN - 1) / BN);
+    const int tiles_m = g.sh.halo_tw ? (g.sh.M / g.sh.halo_tw + 1) / 2 : (g.sh.M + 255) / 256;
+    const int tiles = tiles_m * ((g.sh.N + BN - 1) / BN);
     int cap = sm_count() / 2;
     if (const char* e = std::getenv("PIPESIM_MAXPAIRS")) cap = std::min(cap, std::atoi(e));
     // PIPESIM_TILES_PER_PAIR=t (fwd/dgrad): at least t tiles per CTA pair,
@@ -645,6 +646,46 @@ CUtensorMap make_im2col_tmap(const Nhwc& t, int pixels_per_column) {
   return map;
 }
 
+// Halo strip width of a 3x3 conv over images `w` pixels wide (GemmShape::
+// halo_tw): whole strips of one image row that nearly fill a 128-row CTA
+// tile; 0 = per-tap im2col loads.  Opt-in (PIPESIM_CONV_HALO=1): it cuts the
+// operand bytes per output pixel by 40% but the narrow VGG layers turned out
+// to be bound per k-block by the N <= 128 MMAs' shared-memory operand reads,
+// not by L2->SM bytes, so the 112-of-128-row strips only add tiles (layer 1
+// forward 547 -> 626 us; aligned views measured the same).
+int halo_width(int w) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_CONV_HALO");
+    return e && std::string(e) == "1";
+  }();
+  if (!on) return 0;
+  for (int tw = 126; tw >= 96; --tw)
+    if (w % tw == 0) return tw;
+  return 0;
+}
+
+// {64 ch, tw + 2 px, 3 rows, 1 image} halo patches of an NHWC tensor
+// (coordinates {c, w - 1, h - 1, n}; out-of-image positions read zeros)
+CUtensorMap make_patch_tmap(const Nhwc& t, int tw) {
+  if (t.c % 64 != 0) throw std::invalid_argument("halo operand: channels must be a multiple of 64");
+  CUtensorMap map;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(t.c), static_cast<cuuint64_t>(t.w),
+                        static_cast<cuuint64_t>(t.h), static_cast<cuuint64_t>(t.n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(t.c) * 2,
+                           static_cast<cuuint64_t>(t.c) * 2 * t.w,
+                           static_cast<cuuint64_t>(t.c) * 2 * t.w * t.h};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(tw + 2), 3, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                           const_cast<void*>(static_cast<const void*>(t.ptr)), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeTiled (halo patch) failed (code " +
+                       std::to_string(static_cast<int>(r)) + ")");
+  return map;
+}
+
 // conv weights [Cout][ld] viewed as [Cout][9][Cin]: box 64 Cin x 1 tap x 64 Cout
 CUtensorMap make_w3d_tmap(const __nv_bfloat16* w, int cout, int cin, int ld) {
   if (cin % 64 != 0 || ld % 8 != 0) throw std::invalid_argument("conv weights: Cin % 64, ld % 8");
@@ -702,10 +743,12 @@ GemmLaunch plan_conv_fwd(const Nhwc& x, int img0, int imgs, const Mat16& w, cons
   GemmLaunch g;
   g.pair = true;
   g.bn = w.rows > 128 ? 256 : 128;
-  g.ta = make_im2col_tmap(x, 128);
+  const int tw = halo_width(x.w);
+  g.ta = tw ? make_patch_tmap(x, tw) : make_im2col_tmap(x, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
   g.sh = GemmShape{imgs * hw, w.rows, 9 * x.c, img0 * hw, 0, 0, 0, 1, 0};
   g.sh.conv = 1;
+  g.sh.halo_tw = tw;
   g.sh.conv_h = x.h;
   g.sh.conv_w = x.w;
   g.sh.conv_c = x.c;
@@ -724,10 +767,12 @@ GemmLaunch plan_conv_dgrad(const Nhwc& dz, const __nv_bfloat16* w, int cin, int 
   GemmLaunch g;
   g.pair = true;
   g.bn = cin > 128 ? 256 : 128;
-  g.ta = make_im2col_tmap(dz, 128);
+  const int tw = halo_width(dz.w);
+  g.ta = tw ? make_patch_tmap(dz, tw) : make_im2col_tmap(dz, 128);
   g.tb = make_w3d_tmap(w, dz.c, cin, ld_w);
   g.sh = GemmShape{dz.n * dz.h * dz.w, cin, 9 * dz.c, 0, 0, 0, 0, 1, 0};
   g.sh.conv = 3;
+  g.sh.halo_tw = tw;
   g.sh.conv_h = dz.h;
   g.sh.conv_w = dz.w;
   g.sh.conv_c = dz.c;

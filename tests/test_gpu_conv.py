@@ -25,7 +25,10 @@ def _nchw(x):
 
 
 SHAPES = [(2, 8, 8, 64, 64), (3, 14, 14, 64, 128), (2, 7, 9, 128, 256), (4, 28, 28, 64, 64),
-          (1, 56, 56, 128, 128)]
+          (1, 56, 56, 128, 128),
+          # image widths 112 / 224 (the opt-in halo strips, PIPESIM_CONV_HALO=1:
+          # an odd strip count, two strips per image row, two patches per tile)
+          (1, 3, 112, 64, 64), (2, 5, 224, 64, 128), (1, 12, 112, 128, 64)]
 
 
 @pytest.mark.parametrize("n,h,w,cin,cout", SHAPES)
