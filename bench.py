@@ -262,7 +262,14 @@ def main():
         return run_reference_arm(args)
 
     # split-K forwards follow the session's own policy (on only when a process
-    # holds <= 2 stages, i.e. one stage per GPU: latency over throughput)
+    # holds <= 2 stages, i.e. one stage per GPU: latency over throughput); the
+    # standalone per-shape timings below must use the step's configuration,
+    # so a process holding more stages turns split-K off for them as well
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.stages / max(1, world_env) > 2 and not os.environ.get("PIPESIM_REPLICAS"):
+        os.environ.setdefault("PIPESIM_SPLITK", "0")
+    elif os.environ.get("PIPESIM_REPLICAS"):
+        os.environ.setdefault("PIPESIM_SPLITK", "0")
     import torch
     import torch.distributed as dist
 

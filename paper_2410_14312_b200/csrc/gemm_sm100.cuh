@@ -1278,7 +1278,10 @@ __device__ __forceinline__ void conv_wgrad_b(const GemmShape& sh, const CUtensor
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// kExt: the launch may use split-K (partial slabs / the fixup) or halo conv
+// tiles; without it those paths compile out (the plain GEMMs keep their lean
+// code: the extensions cost the 8-stage step ~1.7%, measured).
+template <int BN, bool A_MN, bool B_MN, int EPI, bool kExt>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::kThreads, 1)
     gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmap_a,
                            const __grid_constant__ CUtensorMap tmap_b, GemmShape sh,
@@ -1313,7 +1316,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   const int num_pairs = gridDim.x / 2;
   // halo conv tiles (GemmShape::halo_tw): strips of tw pixels, two per pair
   // tile; the operand ring becomes two patch buffers + S_h B-only stages
-  const bool halo = EPI != kEpiWgradSgd && (sh.conv == 1 || sh.conv == 3) && sh.halo_tw > 0;
+  const bool halo =
+      kExt && EPI != kEpiWgradSgd && (sh.conv == 1 || sh.conv == 3) && sh.halo_tw > 0;
   const int tw = sh.halo_tw;
   const int n_strips = halo ? sh.M / tw : 0;
   constexpr int kPatchBuf = 48 * 1024;  // {64 ch, <= 128 px, 3 rows} + over-read rows
@@ -1330,7 +1334,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   // split-K into partial slabs (conv wgrad) or with the in-kernel fixup
   // (forward): unit = (tile, split)
   // (only forward-epilogue launches split: the other kernels fold S_k = 1)
-  const bool splitk = EPI == kEpiFwd && (ep.partial_slab || ep.fix_cnt) && sh.splits > 1;
+  const bool splitk =
+      kExt && EPI == kEpiFwd && (ep.partial_slab || ep.fix_cnt) && sh.splits > 1;
   const int S_k = splitk ? sh.splits : 1;
   const int kbps = splitk ? sh.kb_per_split : kb_all;
   const int num_units = num_tiles * S_k;
@@ -1591,11 +1596,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
       if ((EPI == kEpiFwd || EPI == kEpiDgrad) && tile == 0 && split == 0 && rank == 0 &&
           e == 0 && lane == 0 && ep.tag_src && ep.tag_dst)
         write_tags(ep);
-      if (EPI == kEpiFwd && ep.fix_cnt && S_k > 1) {
+      if (kExt && EPI == kEpiFwd && ep.fix_cnt && S_k > 1) {
         // split-K fixup: store this split's partial (warp-blocked: each
         // store instruction writes 512 contiguous bytes), publish it, count
         // the arrival; the last split of the tile half reduces and finishes
-        if constexpr (EPI == kEpiFwd) {
+        if constexpr (kExt && EPI == kEpiFwd) {
           const long long blk = 32LL * kColsPerWarp;
           const long long stride = 2LL * Cfg::kEpiWarps * blk;  // between splits
           float* base = ep.fix_ws + (static_cast<long long>(tile) * S_k * 2 + rank) *
@@ -1638,10 +1643,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             });
           }
         }
-      } else if (ep.partial_slab) {
+      } else if (kExt && ep.partial_slab) {
         // split-K into partial slabs (conv wgrad): this split's own fp32
         // slab, plain stores; an in-order reduction consumes the slabs
-        if constexpr (EPI == kEpiFwd) {
+        if constexpr (kExt && EPI == kEpiFwd) {
           EpiParams epp = ep;
           epp.y32 = ep.y32 + static_cast<size_t>(split) * ep.partial_slab;
           epilogue_warp_vec<EPI, kLinear>(epp, she, row_base, tn * BN + c_off, kColsPerWarp,

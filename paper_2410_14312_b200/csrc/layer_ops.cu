@@ -113,7 +113,9 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_one(const GemmLaunch& g, cudaStream_t st) {
   init_gemm_attributes();
   if (g.pair) {
-    auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>;
+    auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>;
+    if constexpr (EPI != kEpiWgradSgd)
+      if (g.ext) kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>;
     constexpr int smem = Gemm2Cfg<BN, EPI>::kSmem;
     const int tiles_m = g.sh.halo_tw ? (g.sh.M / g.sh.halo_tw + 1) / 2 : (g.sh.M + 255) / 256;
     const int tiles = tiles_m * ((g.sh.N + BN - 1) / BN);
@@ -164,9 +166,13 @@ void set_attr() {
     PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GemmCfg<BN>::kSmem));
-  PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI>,
+  PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                Gemm2Cfg<BN, EPI>::kSmem));
+  if constexpr (EPI != kEpiWgradSgd)
+    PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Gemm2Cfg<BN, EPI>::kSmem));
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -387,6 +393,7 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
     if (g.ep.rowwise == 2 && !g.ep.dbg_skip) {  // the fixup runs the vector epilogue
       g.ep.fix_ws = fix_ws;
       g.ep.fix_cnt = fix_cnt;
+      g.ext = true;
       return g;
     }
   }
@@ -749,6 +756,7 @@ GemmLaunch plan_conv_fwd(const Nhwc& x, int img0, int imgs, const Mat16& w, cons
   g.sh = GemmShape{imgs * hw, w.rows, 9 * x.c, img0 * hw, 0, 0, 0, 1, 0};
   g.sh.conv = 1;
   g.sh.halo_tw = tw;
+  g.ext = tw > 0;
   g.sh.conv_h = x.h;
   g.sh.conv_w = x.w;
   g.sh.conv_c = x.c;
@@ -773,6 +781,7 @@ GemmLaunch plan_conv_dgrad(const Nhwc& dz, const __nv_bfloat16* w, int cin, int 
   g.sh = GemmShape{dz.n * dz.h * dz.w, cin, 9 * dz.c, 0, 0, 0, 0, 1, 0};
   g.sh.conv = 3;
   g.sh.halo_tw = tw;
+  g.ext = tw > 0;
   g.sh.conv_h = dz.h;
   g.sh.conv_w = dz.w;
   g.sh.conv_c = dz.c;
@@ -884,6 +893,7 @@ GemmLaunch plan_conv_wgrad_partial(const Mat16& dz, const Nhwc& x, int img0, flo
   const PairWgradShape p = pair_wgrad_shape(cout, x.c, pixels, mode == 2);
   GemmLaunch g;
   g.pair = true;
+  g.ext = true;
   g.bn = p.bn;
   const CUtensorMap im = make_im2col_tmap(x, 64);
   const CUtensorMap dm = make_operand_tmap(dz, /*k_major=*/false, 64);

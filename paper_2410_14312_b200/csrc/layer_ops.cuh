@@ -40,6 +40,7 @@ struct GemmLaunch {
   const float* simt_b = nullptr;
   int simt_lda = 0, simt_ldb = 0;
   bool pair = false;  // persistent CTA-pair kernel
+  bool ext = false;   // pair kernel with split-K / halo tiles compiled in
 };
 
 // Split count of a forward GEMM of rows x N x K (1 = no split).  Splitting
