@@ -5,6 +5,7 @@
 #include "host_xfer.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -403,14 +404,50 @@ struct Session::Impl {
 
   explicit Impl(const SessionConfig& c) : cfg(c) {}
 
+  // PIPESIM_GUARD=1 (debugging): a 4 KB canary after every carve, checked
+  // after each epoch (check_guards) -- finds kernels writing past a buffer
+  // inside the one arena allocation, where compute-sanitizer cannot see it
+  static constexpr size_t kGuard = 4096;
+  bool guard = false;
+  struct Carve {
+    size_t off, bytes;
+    std::string label;
+  };
+  std::vector<Carve> carves;
   template <typename T>
-  T* carve(size_t count) {
+  T* carve(size_t count, const char* label = "") {
     size_t bytes = (count * sizeof(T) + kAlign - 1) / kAlign * kAlign;
     if (bytes == 0) bytes = kAlign;
-    if (arena_used + bytes > arena_cap) throw std::runtime_error("arena overflow");
+    if (arena_used + bytes + (guard ? kGuard : 0) > arena_cap)
+      throw std::runtime_error("arena overflow");
     T* p = reinterpret_cast<T*>(arena + arena_used);
-    arena_used += bytes;
+    if (guard) carves.push_back(Carve{arena_used, bytes, label});
+    arena_used += bytes + (guard ? kGuard : 0);
     return p;
+  }
+  void fill_guards() {
+    for (const Carve& c : carves)
+      PB_CUDA(cudaMemset(arena + c.off + c.bytes, 0xA5, kGuard));
+  }
+  // returns the number of buffers written past (messages on stderr)
+  int check_guards() {
+    int hits = 0;
+    std::vector<unsigned char> h(kGuard);
+    for (const Carve& c : carves) {
+      PB_CUDA(cudaMemcpy(h.data(), arena + c.off + c.bytes, kGuard, cudaMemcpyDeviceToHost));
+      size_t bad = 0, first = kGuard;
+      for (size_t i = 0; i < kGuard; ++i)
+        if (h[i] != 0xA5) {
+          ++bad;
+          first = std::min(first, i);
+        }
+      if (bad) {
+        ++hits;
+        std::fprintf(stderr, "PIPESIM_GUARD: %zu bytes written past '%s' (offset %zu, %zu bytes), "
+                             "first at +%zu\n", bad, c.label.c_str(), c.off, c.bytes, first);
+      }
+    }
+    return hits;
   }
 
   ~Impl() {
@@ -711,8 +748,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         d.out = ls.out;
         d.ld_in = ld8(d.in);
         d.ld_out = ld8(d.out);
-        d.ain = static_cast<int>(ls.in_elems());
-        d.aout = static_cast<int>(ls.out_elems());
+        // activation rows: exact NHWC elements for conv layers (channels are
+        // multiples of 64), the 8-aligned leading dimensions for linear ones
+        // (their kernels address rows with ld_in / ld_out)
+        d.ain = ls.kind == LayerKind::linear ? d.ld_in : static_cast<int>(ls.in_elems());
+        d.aout = ls.kind == LayerKind::linear ? d.ld_out : static_cast<int>(ls.out_elems());
         if (ls.kind == LayerKind::conv3x3) {
           d.conv = true;
           d.pool = ls.pool;
@@ -772,6 +812,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   need += bytes_of(static_cast<size_t>(M) + 1, 8);
   need += 64 * kAlign;
 
+  if (const char* e = std::getenv("PIPESIM_GUARD")) I.guard = std::atoi(e) != 0 && !c.plan_only;
+  if (I.guard) need += need + (size_t{1} << 26);  // canaries (debugging only)
   if (c.plan_only) {
     I.arena = reinterpret_cast<char*>(uintptr_t{1} << 40);  // addresses only, never touched
   } else {
@@ -787,18 +829,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     for (auto& d : st.layers)
       for (int p = 0; p < 2; ++p) {
         if (I.split)
-          d.lo[p] = I.carve<uint16_t>(static_cast<size_t>(d.out) * d.ld_in);
+          d.lo[p] = I.carve<uint16_t>(static_cast<size_t>(d.out) * d.ld_in, "master lo");
         else
-          d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out);
-        d.b32[p] = I.carve<float>(d.out);
+          d.w32[p] = I.carve<float>(static_cast<size_t>(d.in) * d.out, "master w32");
+        d.b32[p] = I.carve<float>(d.out, "master b32");
       }
     st.pool.resize(pool_n[s]);
     for (auto& ps : st.pool) {
       for (auto& d : st.layers) {
-        ps.w16.push_back(I.carve<__nv_bfloat16>(static_cast<size_t>(d.out) * d.ld_in * I.sc));
-        ps.b32.push_back(I.carve<float>(d.out));
+        ps.w16.push_back(I.carve<__nv_bfloat16>(static_cast<size_t>(d.out) * d.ld_in * I.sc, "pool w16"));
+        ps.b32.push_back(I.carve<float>(d.out, "pool b32"));
       }
-      ps.tag = I.carve<int>(1);
+      ps.tag = I.carve<int>(1, "pool tag");
     }
     st.cur_version = I.carve<int>(1);
     st.acts.resize(act_n[s]);
@@ -808,14 +850,14 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         const bool logits = (s == W - 1) && (l == st.L - 1);
         as.out16.push_back(logits ? nullptr
                                   : I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * I.sc *
-                                                           d.aout));
+                                                           d.aout, "slot out16"));
         as.pre16.push_back(d.pool ? I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * d.pre_elems)
                                   : nullptr);
         if (d.first_conv)
           as.cols16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * d.h * d.w * d.ld_in);
       }
-      if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out);
-      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().aout * I.sc);
+      if (s == W - 1) as.out32 = I.carve<float>(static_cast<size_t>(c.B) * I.n_out, "slot out32");
+      as.dzin = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.back().aout * I.sc, "slot dzin");
       if (s > 0 && !I.local(s - 1)) {
         as.in16 = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ain * I.sc);
         as.dzsend = I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers.front().ain * I.sc);
@@ -823,7 +865,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     }
     for (int l = 0; l + 1 < st.L; ++l)
       st.scratch_dz.push_back(
-          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].aout * I.sc));
+          I.carve<__nv_bfloat16>(static_cast<size_t>(c.B) * st.layers[l].aout * I.sc, "scratch dz"));
     for (int l = 0; l < st.L; ++l)
       st.scratch_pre.push_back(
           st.layers[l].pool
@@ -844,6 +886,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   I.fwd_trace = I.carve<int>(static_cast<size_t>(M) * U * W);
   I.bwd_trace = I.carve<int>(static_cast<size_t>(M) * W);
   I.d_digest = I.carve<uint64_t>(static_cast<size_t>(M) + 1);
+  if (I.guard) I.fill_guards();
 
   if (!c.plan_only) {
   PB_CUDA(cudaStreamCreateWithFlags(&I.origin, cudaStreamNonBlocking));
@@ -2099,6 +2142,8 @@ EpochResult Session::run_epoch() {
   }
   PB_CUDA(cudaEventRecord(I.t1, I.origin));
   PB_CUDA(cudaEventSynchronize(I.t1));
+  if (I.guard && I.check_guards() > 0)
+    throw std::logic_error("PIPESIM_GUARD: a kernel wrote past a session buffer (see stderr)");
   return collect_result();
 }
 
@@ -2181,6 +2226,8 @@ EpochResult Session::train_epoch_host(const void* x, HostDType xt, const void* y
   I.streaming = false;
   PB_CUDA(cudaEventRecord(I.t1, I.origin));
   PB_CUDA(cudaEventSynchronize(I.t1));
+  if (I.guard && I.check_guards() > 0)
+    throw std::logic_error("PIPESIM_GUARD: a kernel wrote past a session buffer (see stderr)");
   return collect_result();
 }
 
