@@ -814,6 +814,10 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch: everything above overlaps the previous
+  // kernel of the stream; its outputs are read only after this
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -1369,6 +1373,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic dependent launch (see the single-CTA kernel)
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {

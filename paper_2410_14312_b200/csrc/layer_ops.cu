@@ -99,6 +99,16 @@ static bool use_pair(int M) { return M > 128 && pair_allowed(); }
 
 namespace {
 
+// PIPESIM_PDL=0/1 forces programmatic dependent launch of the GEMMs off /
+// on (else GemmLaunch::pdl, chosen by the executor)
+bool pdl_on(const GemmLaunch& g) {
+  static const int env = [] {
+    const char* e = std::getenv("PIPESIM_PDL");
+    return e ? std::atoi(e) : -1;
+  }();
+  return env >= 0 ? env != 0 : g.pdl;
+}
+
 int sm_count() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -132,30 +142,44 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     const int units =
         tiles * ((g.ep.partial_slab || g.ep.fix_cnt) ? std::max(1, g.sh.splits) : 1);
     const int pairs = std::min(units, std::max(1, cap));
-    kern<<<dim3(2 * pairs), Gemm2Cfg<BN, EPI>::kThreads, smem, st>>>(g.ta, g.tb, g.sh, g.ep,
-                                                                      g.maps);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(Gemm2Cfg<BN, EPI>::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on(g) ? 1 : 0;
+    PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
   } else if constexpr (BN <= 256) {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
     constexpr int smem = GemmCfg<BN>::kSmem;
     const int splits = std::max(1, g.sh.splits);
     dim3 grid((g.sh.N + BN - 1) / BN, (g.sh.M + 127) / 128, splits);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
     if (splits > 1 && !g.ep.partial_slab) {  // the splits of a tile are one cluster (DSMEM reduction)
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = grid;
-      cfg.blockDim = dim3(128);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 1;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = splits;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
-    } else {
-      kern<<<grid, 128, smem, st>>>(g.ta, g.tb, g.sh, g.ep, g.maps);
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = 1;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = splits;
+      ++na;
     }
+    if (pdl_on(g)) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
   }
   PB_CUDA(cudaGetLastError());
 }

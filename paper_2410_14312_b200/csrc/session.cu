@@ -253,6 +253,7 @@ struct Session::Impl {
   // in the same layout; sc = bf16 slots per stored element (1 or 2)
   bool v32 = false;
   int sc = 1;
+  bool pdl = false;  // GEMMs with programmatic dependent launch
   // split fp32 masters (gemm_sm100.cuh): version v's master is its pool
   // slot's bf16 weights (hi) plus lo[v % 2]; no separate fp32 masters
   bool split = false;
@@ -716,6 +717,12 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         I.split = false;
   }
 
+  // Latency-bound networks (every Linear layer at most 1024 wide, no conv):
+  // GEMMs use programmatic dependent launch (GemmLaunch::pdl).
+  bool pdl = !convnet;
+  for (size_t l = 0; l + 1 < c.widths.size() && pdl; ++l)
+    if (c.widths[l] > 1024 || c.widths[l + 1] > 1024) pdl = false;
+  I.pdl = pdl;
   // Skinny forwards split K (lower latency, more SM-time) when this process
   // keeps few stages in flight; PIPESIM_SESSION_SPLIT=0/1 overrides.
   bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
@@ -937,6 +944,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   // ---------------- compile the program into ops
   using OK = Impl::OpKind;
   auto push = [&](Impl::Op op) {
+    op.g.pdl = I.pdl;
     const int kind = op.kind == OK::fwd ? 1 : op.kind == OK::dgrad ? 2 : op.kind == OK::wgrad ? 3 : 0;
     const bool timed = kind != 0 && kind == c.timed_kernel && !c.plan_only;
     if (timed) {

@@ -131,6 +131,19 @@ __device__ __forceinline__ void prefetch_l2(const void* gptr, uint32_t bytes) {
                : "memory");
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// A kernel launched with programmatic stream serialization may start (its
+// prologue: barriers, TMEM, descriptor prefetch) while the previous kernel
+// of its stream finishes; griddepcontrol.wait then blocks until that kernel
+// has completed and its memory is visible.  launch_dependents lets the next
+// such kernel be scheduled early (it still waits for this grid's completion).
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
