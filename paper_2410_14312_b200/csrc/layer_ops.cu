@@ -315,15 +315,20 @@ int splitk_env() {
 
 
 // Split-K for skinny forwards (<= 256 rows): enough 128 x 128 tiles x splits
-// to cover the SMs, >= 8 k-blocks per split, at most kMaxSplits (4).
-// PIPESIM_SPLITK=0 disables it, =<n> forces n (A/B runs).
+// to cover the SMs, >= 8 k-blocks per split (PIPESIM_SPLITK_MINKB; 4 k-blocks
+// made C1's 784-wide forwards split and its mini-batch slower, 58.9 -> 65.4
+// us), at most 4.  PIPESIM_SPLITK=0 disables it, =<n> forces n (A/B runs).
 int fwd_splits(int rows, int N, int K) {
   if (rows > 256 || splitk_env() == 0 || !pair_allowed()) return 1;
   const int kb = (K + 63) / 64;
   const int tiles = ((rows + 127) / 128) * ((N + 127) / 128);
   int s = std::max(1, sm_count() / tiles);
   if (splitk_env() > 0) s = splitk_env();
-  s = std::min(s, std::min(4, kb / 8));
+  static const int min_kb = [] {
+    const char* e = std::getenv("PIPESIM_SPLITK_MINKB");
+    return e ? std::max(1, std::atoi(e)) : 8;
+  }();
+  s = std::min(s, std::min(4, kb / min_kb));
   if (s == 3) s = 2;  // column blocks of the reduction: 128 / s, a multiple of 16
   return std::max(1, s);
 }
