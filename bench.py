@@ -504,7 +504,32 @@ def other_configs(P):
         ms = float(np.median([s.run_epoch()["device_ms"] for _ in range(5)]))
         s.close()
         out[key] = {"samples_per_s": M * B / (ms / 1000.0), "us_per_mini_batch": 1000.0 * ms / M}
+    if os.environ.get("PIPESIM_BENCH_VGG", "1") != "0":
+        out.update(vgg_config(P))
     return out
+
+
+def vgg_config(P):
+    """BASELINE configs[3]: VGG-16 on 224x224x3 synthetic images (1000
+    classes), 8 nF1B stages on this GPU (flop-balanced), B=64, N=4, M=16,
+    bf16 conv stages (implicit-GEMM tcgen05), data resident; images/s and
+    the conv + FC GEMM rate against the sustained bf16 peak."""
+    from paper_2410_14312_b200 import convnet as CN
+    net = CN.vgg16()
+    W, N, B, M = 8, 4, 64, 16
+    s = P.Session(net, W, N, B, M, 1e-4, "timeprest")
+    s.load_params(CN.init_params(net, CFG["seed"]))
+    x, lab = CN.synthetic_images(M * B, net, seed=7)
+    s.upload(x, lab, y_labels=True)
+    for _ in range(2):
+        s.run_epoch()
+    ms = float(np.median([s.run_epoch()["device_ms"] for _ in range(3)]))
+    s.close()
+    rate = M * B / (ms / 1000.0)
+    tflops = net.flops_per_sample() * rate / 1e12
+    return {"C4_vgg16_224_W8_nf1b": {"images_per_s": rate, "ms_per_epoch": ms, "images_per_epoch": M * B,
+                                      "partition": net.partition(W), "gemm_tflops": tflops,
+                                      "frac_of_sustained": tflops / _peaks()["bf16_sus"]}}
 
 
 def in_step_kernels(P, net, W, Nm, B, M, device, main_sess):
