@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <stdexcept>
 
+#include "ryu_f32d.cuh"
 #include "shortest.cuh"
 #include "status.hpp"
 
@@ -141,17 +142,17 @@ __global__ void __launch_bounds__(kT) dg_format_lo(const DigestSpan* __restrict_
       }
       const float v = fetch(sp, r * sp.ld + c);
       if (++c == sp.cols) c = 0, ++r;
-      union {
-        char ch[kSlot];
-        uint4 q[2];
-      } buf;
-      int n = fmt::format_shortest(static_cast<double>(v), buf.ch);
-      buf.ch[n++] = '\n';
+      uint64_t wv[4];
+      int n = fmt::format_shortest_fast(static_cast<double>(v), wv);
+      fmt::text_put(wv, n++, '\n');
+      const uint4 q[2] = {make_uint4(static_cast<uint32_t>(wv[0]), static_cast<uint32_t>(wv[0] >> 32),
+                                     static_cast<uint32_t>(wv[1]), static_cast<uint32_t>(wv[1] >> 32)),
+                          make_uint4(static_cast<uint32_t>(wv[2]), static_cast<uint32_t>(wv[2] >> 32),
+                                     static_cast<uint32_t>(wv[3]), static_cast<uint32_t>(wv[3] >> 32))};
       uint4* dst = reinterpret_cast<uint4*>(slots + i * kSlot);
-      dst[0] = buf.q[0];
-      dst[1] = buf.q[1];
+      dst[0] = q[0];
+      dst[1] = q[1];
       lens[i] = static_cast<uint8_t>(n);
-      const uint4 q[2] = {buf.q[0], buf.q[1]};
 #pragma unroll
       for (int j = 0; j < kSlot; ++j) {  // registers only (no dynamic indexing)
         if (j >= n) break;
@@ -421,16 +422,13 @@ namespace {
 __global__ void dg_format_only(const float* __restrict__ v, int64_t n, char* __restrict__ out) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
-  union {
-    char ch[32];
-    uint4 q[2];
-  } buf;
-  buf.q[0] = make_uint4(0, 0, 0, 0);
-  buf.q[1] = make_uint4(0, 0, 0, 0);
-  pb::fmt::format_shortest(static_cast<double>(v[i]), buf.ch);
+  uint64_t w[4];
+  pb::fmt::format_shortest_fast(static_cast<double>(v[i]), w);
   uint4* dst = reinterpret_cast<uint4*>(out + i * 32);
-  dst[0] = buf.q[0];
-  dst[1] = buf.q[1];
+  dst[0] = make_uint4(static_cast<uint32_t>(w[0]), static_cast<uint32_t>(w[0] >> 32),
+                      static_cast<uint32_t>(w[1]), static_cast<uint32_t>(w[1] >> 32));
+  dst[1] = make_uint4(static_cast<uint32_t>(w[2]), static_cast<uint32_t>(w[2] >> 32),
+                      static_cast<uint32_t>(w[3]), static_cast<uint32_t>(w[3] >> 32));
 }
 }  // namespace
 

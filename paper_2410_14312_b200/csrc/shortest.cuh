@@ -32,7 +32,9 @@ namespace fmt {
 
 // 10^k, k = 0..48, as four little-endian 64-bit limbs
 #if defined(__CUDACC__)
-__device__ __constant__ uint64_t kPow10Dev[49][4] = {
+// (global memory: lanes of a warp index different rows, which the constant
+// cache would serialise)
+__device__ const uint64_t kPow10Dev[49][4] = {
   {0x0000000000000001ull, 0x0000000000000000ull, 0x0000000000000000ull, 0x0000000000000000ull},
   {0x000000000000000aull, 0x0000000000000000ull, 0x0000000000000000ull, 0x0000000000000000ull},
   {0x0000000000000064ull, 0x0000000000000000ull, 0x0000000000000000ull, 0x0000000000000000ull},

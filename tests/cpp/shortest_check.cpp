@@ -9,6 +9,7 @@
 #include <random>
 #include <string>
 #include "shortest.cuh"
+#include "ryu_f32d.cuh"
 int main(int argc, char** argv) {
   long n = argc > 1 ? atol(argv[1]) : 1000000;
   std::mt19937_64 g(1);
@@ -22,6 +23,12 @@ int main(int argc, char** argv) {
     int lb = r.ptr - b;
     if (la != lb || memcmp(a, b, la)) {
       if (bad++ < 20) printf("MISMATCH %.17g: got '%.*s' want '%.*s'\n", v, la, a, lb, b);
+    }
+    uint64_t w[4];
+    const int lf = pb::fmt::format_shortest_fast(v, w);
+    if (lf != lb || memcmp(w, b, lf)) {
+      if (bad++ < 20) printf("FAST MISMATCH %.17g: got '%.*s' want '%.*s'\n", v, lf,
+                             reinterpret_cast<const char*>(w), lb, b);
     }
   };
   for (long i = 0; i < n; ++i) { uint32_t u = g(); float x; memcpy(&x, &u, 4); check(x); }
