@@ -154,10 +154,15 @@ __global__ void __launch_bounds__(kT) dg_format_lo(const DigestSpan* __restrict_
       dst[1] = q[1];
       lens[i] = static_cast<uint8_t>(n);
 #pragma unroll
-      for (int j = 0; j < kSlot; ++j) {  // registers only (no dynamic indexing)
-        if (j >= n) break;
-        const uint64_t x = S ^ (static_cast<uint64_t>(slot_byte(q, j) & 15u) * kRep);
-        S = nib_mul3(x);
+      for (int k = 0; k < 4; ++k) {  // registers only: bytes off the words
+        uint64_t word = wv[k];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (8 * k + b >= n) break;
+          const uint64_t x = S ^ ((word & 15u) * kRep);
+          S = nib_mul3(x);
+          word >>= 8;
+        }
       }
     }
   }
@@ -221,11 +226,12 @@ __global__ void __launch_bounds__(kT) dg_hi(const char* __restrict__ slots,
     for (int64_t i = a; i < b; ++i) {
       const int n = lens[i];
       const uint4* src = reinterpret_cast<const uint4*>(slots + i * kSlot);
-      const uint4 q[2] = {src[0], src[1]};
+      const uint4 q0 = src[0], q1 = src[1];
+      const uint32_t qw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
       for (int j = 0; j < kSlot; ++j) {
         if (j >= n) break;
-        const uint32_t c = slot_byte(q, j);
+        const uint32_t c = (qw[j >> 2] >> (8 * (j & 3))) & 0xFFu;
         const uint32_t xl = (lo ^ c) & 15u;
         const uint32_t K = (11u * xl + ((3u * xl) >> 4)) & 15u;
         const uint64_t x = H ^ (static_cast<uint64_t>(c >> 4) * kRep);
@@ -260,11 +266,12 @@ __global__ void __launch_bounds__(kT) dg_exact(const char* __restrict__ slots,
     for (int64_t i = a; i < b; ++i) {
       const int n = lens[i];
       const uint4* src = reinterpret_cast<const uint4*>(slots + i * kSlot);
-      const uint4 q[2] = {src[0], src[1]};
+      const uint4 q0 = src[0], q1 = src[1];
+      const uint32_t qw[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
       for (int j = 0; j < kSlot; ++j) {
         if (j >= n) break;
-        h = (h ^ slot_byte(q, j)) * kP;
+        h = (h ^ ((qw[j >> 2] >> (8 * (j & 3))) & 0xFFu)) * kP;
         m *= kP;
       }
     }

@@ -404,6 +404,16 @@ PB_FMT_HD void ryu_d2d(uint64_t bits, uint64_t* digits, int* e10out) {
   *e10out = e10 + removed;
 }
 
+// the exact-integer path of format_shortest, kept out of line so that its
+// 256-bit temporaries do not weigh on the fast path's registers
+#if defined(__CUDACC__)
+__host__ __device__ __noinline__ inline int format_shortest_slow(double v, char* out) {
+  return format_shortest(v, out);
+}
+#else
+inline int format_shortest_slow(double v, char* out) { return format_shortest(v, out); }
+#endif
+
 // byte c at position pos of a 32-byte text held in four registers
 PB_FMT_HD void text_put(uint64_t (&w)[4], int pos, uint32_t c) {
   const uint64_t v = static_cast<uint64_t>(c & 0xFF) << (8 * (pos & 7));
@@ -433,7 +443,16 @@ PB_FMT_HD int format_shortest_fast(double v, uint64_t (&w)[4]) {
   ryu_d2d(bits, &dg, &e10);
   // digit count (dg < 10^17)
   int nd = 1;
-  for (uint64_t p = 10; nd < 17 && dg >= p; p *= 10) ++nd;
+  {
+    // digit count: 32-bit compares on the high part when it is non-zero
+    const uint64_t h = dg / 100000000u;
+    uint32_t x = h ? static_cast<uint32_t>(h) : static_cast<uint32_t>(dg);
+    nd = h ? 9 : 1;
+    while (x >= 10) {
+      x /= 10;
+      ++nd;
+    }
+  }
   const int X = e10 + nd - 1;  // v = d1.d2..dn x 10^X
   const int ax = X < 0 ? -X : X;
   const int sci_len = nd + (nd > 1 ? 1 : 0) + 2 + (ax >= 100 ? 3 : 2);
@@ -442,7 +461,7 @@ PB_FMT_HD int format_shortest_fast(double v, uint64_t (&w)[4]) {
   if (fixed && X >= 0 && nd < X + 1) {
     // padded integer digits: the exact integer (rare; the reference path)
     char buf[48];
-    const int m = format_shortest(v, buf);
+    const int m = format_shortest_slow(v, buf);
     w[0] = w[1] = w[2] = w[3] = 0;
     for (int i = 0; i < m && i < 32; ++i) text_put(w, i, static_cast<uint8_t>(buf[i]));
     return m;
@@ -454,11 +473,23 @@ PB_FMT_HD int format_shortest_fast(double v, uint64_t (&w)[4]) {
     if (X < 0) return n + 1 - X + i;                      // 0.000ddd
     return n + (i <= X ? i : i + 1);                      // dd.ddd / ddd
   };
-  uint64_t q = dg;
+  // dg < 10^17: the low 8 digits and the rest as 32-bit numbers (32-bit
+  // divisions by 10 are a multiply-high; 64-bit ones are emulated)
+  const uint64_t hi64 = dg / 100000000u;
+  uint32_t lo = static_cast<uint32_t>(dg - hi64 * 100000000u);
+  uint32_t hi = static_cast<uint32_t>(hi64);
   for (int i = nd - 1; i >= 0; --i) {
-    const uint64_t q10 = q / 10;
-    text_put(w, digit_pos(i), static_cast<uint32_t>('0' + (q - 10 * q10)));
-    q = q10;
+    uint32_t d;
+    if (i >= nd - 8) {
+      const uint32_t l10 = lo / 10;
+      d = lo - 10 * l10;
+      lo = l10;
+    } else {
+      const uint32_t h10 = hi / 10;
+      d = hi - 10 * h10;
+      hi = h10;
+    }
+    text_put(w, digit_pos(i), '0' + d);
   }
   int len;
   if (!fixed) {
