@@ -343,6 +343,37 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
 }
 
 // Row-per-thread epilogue (thread i owns row i; 16-column vector chunks).
+// Softmax cross-entropy of one row of logits (raw accumulators v + bias, a
+// linear head) against its class label, in the forward epilogue: the loss
+// kernel's formulas (max-subtracted, one exp per logit) on registers.
+__device__ __forceinline__ void fused_ce_row(const EpiParams& ep, int row, const float (&v)[16],
+                                             int valid) {
+  const size_t r = static_cast<size_t>(row + ep.y_row_off);
+  float z[16];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    z[i] = i < valid ? v[i] + (ep.bias ? ep.bias[i] : 0.f) : -INFINITY;
+    mx = fmaxf(mx, z[i]);
+  }
+  const int lab = ep.loss_labels[r];
+  float zl = 0.f;  // the label's max-subtracted logit
+  float se = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i == lab) zl = z[i] - mx;
+    z[i] = i < valid ? expf(z[i] - mx) : 0.f;
+    se += z[i];
+  }
+  __nv_bfloat16* d = ep.loss_dz + r * ep.loss_ld_dz;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i >= valid) break;
+    d[i] = __float2bfloat16_rn((z[i] / se - (i == lab ? 1.f : 0.f)) / ep.loss_denom);
+  }
+  ep.loss_row[r] = logf(se) - zl;
+}
+
 template <int EPI, int ACT>
 __device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const GemmShape& sh,
                                                    int row_base, int n_base, int n_cols,
@@ -430,6 +461,8 @@ __device__ __forceinline__ void epilogue_warp_rows(const EpiParams& ep, const Ge
         }
       } else {
         epilogue_chunk<EPI, ACT>(ep, sh, row, n, valid, v);
+        if constexpr (EPI == kEpiFwd)
+          if (ep.loss_dz && n == 0 && sh.N <= 16) fused_ce_row(ep, row, v, valid);
       }
     }
     xa[0] = xb[0];

@@ -103,6 +103,15 @@ struct EpiParams {
   // last arriver resets the counter, so it is zero between launches.
   float* fix_ws;
   int* fix_cnt;
+  // softmax cross-entropy fused into the logits layer's forward epilogue
+  // (class labels, linear head, N <= 16, the row-per-thread epilogue): per
+  // row dz = (softmax - onehot) / loss_denom (bf16, row stride loss_ld_dz)
+  // and the row's loss; rows indexed like y (y_row_off)
+  const int* loss_labels;
+  __nv_bfloat16* loss_dz;
+  int loss_ld_dz;
+  float* loss_row;
+  float loss_denom;
 };
 
 // Where the fixup epilogue finds the partials of its tile (see EpiParams).

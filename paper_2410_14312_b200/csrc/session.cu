@@ -245,6 +245,9 @@ struct Session::Impl {
     int ldw = 0, ld16 = 0, S = 0;
     long long slab = 0;
     bool f32dz = false;  // bias: dz holds fp32 partial sums
+    // logits forward with the softmax-CE fused into its epilogue, and the
+    // loss op it replaces (both only when the targets are class labels)
+    bool loss_fused = false;
   };
 
   const SessionConfig& cfg;
@@ -728,6 +731,11 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
   if (const char* e = std::getenv("PIPESIM_SESSION_SPLIT")) split_fwd = std::atoi(e) != 0;
   if (I.v32) split_fwd = false;
+  // softmax-CE fused into the logits forward (small class counts, linear
+  // head; applied when the targets are class labels): the loss kernel leaves
+  // the backward's critical path.  PIPESIM_LOSS_FUSE=0 disables.
+  bool loss_fuse = !I.v32 && c.loss == 1 && c.acts.back() == kLinear && c.widths.back() <= 16;
+  if (const char* e = std::getenv("PIPESIM_LOSS_FUSE")) loss_fuse = loss_fuse && std::atoi(e) != 0;
 
   // ---------------- sizes
   I.n_out = c.widths.back();
@@ -1405,6 +1413,14 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                          logits ? as.out32 : nullptr, I.n_out, r0,
                          /*allow_split=*/split_fwd, /*verify=*/I.v32, st.fix_ws, st.fix_cnt);
         }
+        if (logits && loss_fuse && !o.g.simt && o.g.sh.splits <= 1) {
+          o.loss_fused = true;
+          o.lab = I.ylab + static_cast<size_t>(tk.k - 1) * c.B;
+          o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
+          o.dz_out = as.dzin;
+          o.ld_dz = d.ld_out;
+          o.denom = static_cast<float>(c.B);
+        }
         if (l == 0) {
           o.g.ep.tag_src = ps.tag;
           o.g.ep.tag_dst = I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
@@ -1445,8 +1461,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         o.dz_out = as.dzin;
         o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
         o.ld_dz = st.layers.back().ld_out;
+        o.loss_fused = loss_fuse;
         push(o);
-        ++kernels_per_epoch_;
+        if (!loss_fuse) ++kernels_per_epoch_;
       }
       const Impl::PoolSlot& prop = st.pool[st.version_colour[tk.version]];
       Impl::PoolSlot& next = st.pool[st.version_colour[tk.k]];
@@ -2035,7 +2052,20 @@ void issue(Session::Impl& I, cudaStream_t origin) {
     switch (o.kind) {
       case OK::wait: PB_CUDA(cudaStreamWaitEvent(s, o.ev, 0)); break;
       case OK::record: PB_CUDA(cudaEventRecord(o.ev, s)); break;
-      case OK::fwd: launch_fwd(o.g, s); break;
+      case OK::fwd:
+        if (o.loss_fused && I.use_labels) {
+          GemmLaunch g = o.g;
+          g.ep.loss_labels = o.lab;
+          g.ep.loss_dz = o.dz_out;
+          g.ep.loss_ld_dz = o.ld_dz;
+          g.ep.loss_row = o.row_loss;
+          g.ep.loss_denom = o.denom;
+          g.ep.rowwise = 1;  // the row-per-thread epilogue holds whole rows
+          launch_fwd(g, s);
+        } else {
+          launch_fwd(o.g, s);
+        }
+        break;
       case OK::dgrad: launch_dgrad(o.g, s); break;
       case OK::wgrad: launch_wgrad(o.g, s); break;
       case OK::bias:
@@ -2061,6 +2091,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         launch_colsum_partial(s, o.dz, o.rows, o.cols, o.ld, o.f32);
         break;
       case OK::loss:
+        if (o.loss_fused && I.use_labels) break;  // done by the logits forward
         launch_loss(s, o.y, o.rows, o.cols, o.ld, o.t, o.ld_t, o.loss, o.act_last, o.denom,
                     o.dz_out, o.ld_dz, o.row_loss, I.v32, I.use_labels ? o.lab : nullptr);
         break;
