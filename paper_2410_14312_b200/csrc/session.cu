@@ -734,6 +734,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   // softmax-CE fused into the logits forward (small class counts, linear
   // head; applied when the targets are class labels): the loss kernel leaves
   // the backward's critical path.  PIPESIM_LOSS_FUSE=0 disables.
+  // backwards wait for the downstream delta, not the downstream updates
+  // (PIPESIM_DELTA_EDGES=0: the whole downstream backward, as before)
+  bool delta_edges = true;
+  if (const char* e = std::getenv("PIPESIM_DELTA_EDGES")) delta_edges = std::atoi(e) != 0;
   bool loss_fuse = !I.v32 && c.loss == 1 && c.acts.back() == kLinear && c.widths.back() <= 16;
   if (const char* e = std::getenv("PIPESIM_LOSS_FUSE")) loss_fuse = loss_fuse && std::atoi(e) != 0;
 
@@ -1061,6 +1065,9 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     int order;                     // position of the first member in issue order
     std::vector<int> deps;         // node ids (same-stage predecessor + cross-stage)
     cudaEvent_t done = nullptr;
+    // backward of a stage s > 0: the delta for stage s-1 is written (its
+    // wgrad / bias work on the side streams may still run)
+    cudaEvent_t delta_done = nullptr;
     int digest = -1;               // >= 0: in-epoch digest node (index into dplans)
   };
   std::vector<Node> nodes;
@@ -1146,6 +1153,22 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           }
         }
       }
+    }
+    // The backward of mini k on stage s waits only for the delta of stage
+    // s+1's backward (delta_done), not for stage s+1's weight / bias updates
+    // still running on its side streams -- they read stage s's activation
+    // slot of mini k (the wgrad operand x), so stage s's reuse of that slot
+    // (its first forward of the slot's next occupant) waits for stage s+1's
+    // whole backward of the previous occupant instead: edge (b').
+    std::map<std::pair<int, int>, int> first_fwd_node;
+    for (int i = 0; i < static_cast<int>(nodes.size()); ++i)
+      if (nodes[i].fwd && !first_fwd_node.count({nodes[i].k, nodes[i].s}))
+        first_fwd_node[{nodes[i].k, nodes[i].s}] = i;
+    for (int i = 0; i < static_cast<int>(nodes.size()); ++i) {
+      Node& n = nodes[i];
+      if (!n.fwd || n.s + 1 >= W || first_fwd_node.at({n.k, n.s}) != i) continue;
+      const int pk = act_prev_occupant[n.s][n.k];
+      if (pk > 0) n.deps.push_back(bwd_node.at({pk, n.s + 1}));  // (b')
     }
     for (Node& n : nodes) {
       if (n.fwd && n.s > 0)
@@ -1308,8 +1331,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     for (int d : node.deps) {
       // same-stage order is the stream order (same kind, or one stream per stage)
       if (nodes[d].s == s && (nodes[d].fwd == node.fwd || !I.split_fb)) continue;
+      // (b') on another GPU: its wgrad reads its own received copy
+      if (node.fwd && !nodes[d].fwd && nodes[d].digest < 0 && nodes[d].s == s + 1 &&
+          !I.local(nodes[d].s))
+        continue;
       if (nodes[d].digest >= 0 || I.local(nodes[d].s)) {
-        wait_on(ns, nodes[d].done);
+        // a backward waits for the downstream stage's delta only
+        const bool delta_edge = !node.fwd && !nodes[d].fwd && nodes[d].digest < 0 &&
+                                nodes[d].s == s + 1 && nodes[d].k == node.k &&
+                                nodes[d].delta_done && delta_edges;
+        wait_on(ns, delta_edge ? nodes[d].delta_done : nodes[d].done);
         continue;
       }
       const Node& up = nodes[d];
@@ -1544,6 +1575,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           }
           push(o);
           ++kernels_per_epoch_;
+          if (l == 0) node.delta_done = record_on(ns);  // stage s-1's delta is written
         }
         // the side stream's work on layer l only reads dZ_l (and x); it was
         // made ready before this iteration (dZ_{L-1}: task start; dZ_l: the
@@ -1693,7 +1725,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       push(sd);
     }
     if (!node.fwd && s > 0 && !I.local(s - 1)) {
-      wait_on(Impl::kBwdSend, node.done);
+      wait_on(Impl::kBwdSend, node.delta_done && delta_edges ? node.delta_done : node.done);
       Impl::Op sd{OK::send};
       sd.stream = Impl::kBwdSend;
       sd.src = as.dzsend;
