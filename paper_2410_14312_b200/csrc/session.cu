@@ -738,6 +738,10 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   // (PIPESIM_DELTA_EDGES=0: the whole downstream backward, as before)
   bool delta_edges = true;
   if (const char* e = std::getenv("PIPESIM_DELTA_EDGES")) delta_edges = std::atoi(e) != 0;
+  // forwards wait for the commit of their pinned version only (not for the
+  // dgrad chain of that backward); PIPESIM_COMMIT_EDGES=0: the whole backward
+  bool commit_edges = !c.snapshots;
+  if (const char* e = std::getenv("PIPESIM_COMMIT_EDGES")) commit_edges = commit_edges && std::atoi(e) != 0;
   bool loss_fuse = !I.v32 && c.loss == 1 && c.acts.back() == kLinear && c.widths.back() <= 16;
   if (const char* e = std::getenv("PIPESIM_LOSS_FUSE")) loss_fuse = loss_fuse && std::atoi(e) != 0;
 
@@ -1064,6 +1068,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     int s, k, version, jj0, jj1;  // s 0-based; forward micro range [jj0, jj1]
     int order;                     // position of the first member in issue order
     std::vector<int> deps;         // node ids (same-stage predecessor + cross-stage)
+    // forward: hazard-(a) deps (the commit of its pinned version: only the
+    // backward's wgrad / bias streams, not its dgrad chain), and the
+    // hazard-(b) dep (slot reuse: the whole backward)
+    std::vector<int> commit_deps;
+    int slot_dep = -1;
+    // backward: events on its wgrad and bias streams after the commit
+    cudaEvent_t commit_side = nullptr, commit_bias = nullptr;
     cudaEvent_t done = nullptr;
     // backward of a stage s > 0: the delta for stage s-1 is written (its
     // wgrad / bias work on the side streams may still run)
@@ -1134,10 +1145,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         Node& n = nodes[i];
         const auto& colour = stage_version_colour[n.s];
         if (n.fwd) {
-          if (n.version >= 1) n.deps.push_back(bwd_node.at({n.version, n.s}));  // (a)
+          if (n.version >= 1) {                                                 // (a)
+            n.deps.push_back(bwd_node.at({n.version, n.s}));
+            n.commit_deps.push_back(n.deps.back());
+          }
           if (first_fwd.at({n.k, n.s}) == i) {                                  // (b)
             const int pk = act_prev_occupant[n.s][n.k];
-            if (pk > 0) n.deps.push_back(bwd_node.at({pk, n.s}));
+            if (pk > 0) {
+              n.deps.push_back(bwd_node.at({pk, n.s}));
+              n.slot_dep = n.deps.back();
+            }
           }
         } else {
           n.deps.push_back(last_fwd_of_mini.at({n.k, n.s}));  // (c)
@@ -1340,6 +1357,19 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         const bool delta_edge = !node.fwd && !nodes[d].fwd && nodes[d].digest < 0 &&
                                 nodes[d].s == s + 1 && nodes[d].k == node.k &&
                                 nodes[d].delta_done && delta_edges;
+        // a forward waits for the commit of its pinned version only (the
+        // wgrad + bias streams of that backward), unless the same backward
+        // also frees the activation slot it writes
+        const bool commit_edge =
+            node.fwd && !nodes[d].fwd && nodes[d].digest < 0 && nodes[d].s == s &&
+            d != node.slot_dep && nodes[d].commit_side && commit_edges &&
+            std::find(node.commit_deps.begin(), node.commit_deps.end(), d) !=
+                node.commit_deps.end();
+        if (commit_edge) {
+          wait_on(ns, nodes[d].commit_side);
+          if (nodes[d].commit_bias) wait_on(ns, nodes[d].commit_bias);
+          continue;
+        }
         wait_on(ns, delta_edge ? nodes[d].delta_done : nodes[d].done);
         continue;
       }
@@ -1679,9 +1709,13 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
           if (bstr != side) wait_on(bstr, ev);
         }
       }
-      if (c.side_streams) {  // join
-        wait_on(ns, record_on(side));
-        if (bstr != side) wait_on(ns, record_on(bstr));
+      if (c.side_streams) {  // join (the two events also mark the commit)
+        node.commit_side = record_on(side);
+        wait_on(ns, node.commit_side);
+        if (bstr != side) {
+          node.commit_bias = record_on(bstr);
+          wait_on(ns, node.commit_bias);
+        }
       }
       if (c.snapshots && !c.plan_only) {
         for (int l = 0, po = 0; l < st.L; ++l) {
