@@ -90,7 +90,19 @@ bool pair_allowed() {
 }  // namespace
 
 int pick_bn(int M, int N) {
-  if (M > 128 && pair_allowed()) return N > 128 ? 256 : 128;
+  if (M > 128 && pair_allowed()) {
+    // a pair GEMM with fewer than 16 256-wide tiles (a small network:
+    // latency-bound) takes 128-wide tiles, twice the SMs -- C1 55.5 -> 47.4
+    // us per mini-batch; the 16 x 4096 shapes have >= 16 tiles
+    // (PIPESIM_SMALL_TILES=N: the threshold, 0 = off)
+    static const int small = [] {
+      const char* e = std::getenv("PIPESIM_SMALL_TILES");
+      return e ? std::atoi(e) : 16;
+    }();
+    const long tiles256 = static_cast<long>((M + 255) / 256) * ((N + 255) / 256);
+    if (N > 128 && tiles256 < small) return 128;
+    return N > 128 ? 256 : 128;
+  }
   const long tiles256 = static_cast<long>((M + 127) / 128) * ((N + 255) / 256);
   return (N > 128 && tiles256 >= 132) ? 256 : 128;
 }
