@@ -104,7 +104,18 @@ int pick_bn(int M, int N) {
     return N > 128 ? 256 : 128;
   }
   const long tiles256 = static_cast<long>((M + 127) / 128) * ((N + 255) / 256);
-  return (N > 128 && tiles256 >= 132) ? 256 : 128;
+  if (N > 128 && tiles256 >= 132) return 256;
+  // a single-CTA GEMM with fewer than PIPESIM_BN64 128-wide tiles (a micro-
+  // batch of <= 128 rows in a small network: latency-bound) takes 64-wide
+  // tiles, twice the SMs, half the B bytes per k-block -- C1 47.2 -> 46.4 us
+  // per mini-batch (tools/gpu/r2_bn64.sh; 0 = off)
+  static const int small64 = [] {
+    const char* e = std::getenv("PIPESIM_BN64");
+    return e ? std::atoi(e) : 8;
+  }();
+  const long tiles128 = static_cast<long>((M + 127) / 128) * ((N + 127) / 128);
+  if (tiles128 < small64) return 64;
+  return 128;
 }
 
 static bool use_pair(int M) { return M > 128 && pair_allowed(); }
@@ -135,6 +146,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_one(const GemmLaunch& g, cudaStream_t st) {
   init_gemm_attributes();
   if (g.pair) {
+    if constexpr (BN >= 128) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>;
     if constexpr (EPI != kEpiWgradSgd)
       if (g.ext) kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>;
@@ -165,6 +177,7 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl_on(g) ? 1 : 0;
     PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
+    }
   } else if constexpr (BN <= 256) {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
     constexpr int smem = GemmCfg<BN>::kSmem;
@@ -202,6 +215,8 @@ void set_attr() {
     PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GemmCfg<BN>::kSmem));
+  if constexpr (BN < 128) return;  // single-CTA only
+  else {
   PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                Gemm2Cfg<BN, EPI>::kSmem));
@@ -209,6 +224,7 @@ void set_attr() {
     PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Gemm2Cfg<BN, EPI>::kSmem));
+  }
 }
 
 template <bool A_MN, bool B_MN, int EPI>
@@ -217,6 +233,8 @@ void launch_bn(const GemmLaunch& g, cudaStream_t st) {
     if (g.bn == 512) return launch_one<512, A_MN, B_MN, EPI>(g, st);
   if (g.bn == 256)
     launch_one<256, A_MN, B_MN, EPI>(g, st);
+  else if (g.bn == 64 && !g.pair)
+    launch_one<64, A_MN, B_MN, EPI>(g, st);
   else
     launch_one<128, A_MN, B_MN, EPI>(g, st);
 }
@@ -232,6 +250,9 @@ void init_gemm_attributes() {
     set_attr<512, false, true, kEpiDgrad>();
     set_attr<128, false, true, kEpiDgrad>();
     set_attr<256, false, true, kEpiDgrad>();
+    set_attr<64, false, false, kEpiFwd>();
+    set_attr<64, false, true, kEpiDgrad>();
+    set_attr<64, true, true, kEpiWgradSgd>();
     set_attr<128, true, true, kEpiWgradSgd>();
     set_attr<256, true, true, kEpiWgradSgd>();
     // conv wgrad: split-K partial slabs (single-CTA, MN / MN operands)
