@@ -120,6 +120,17 @@ int pick_bn(int M, int N) {
 
 static bool use_pair(int M) { return M > 128 && pair_allowed(); }
 
+// A pair forward with at most 64 output columns (VGG's 64-channel convs,
+// the first conv's im2col GEMM) takes 64-wide tiles instead of computing a
+// half-empty 128-wide one (PIPESIM_PAIR_BN64=0: off)
+static bool pair_bn64(int N) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_PAIR_BN64");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && N <= 64;
+}
+
 namespace {
 
 // PIPESIM_PDL=0/1 forces programmatic dependent launch of the GEMMs off /
@@ -146,10 +157,12 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_one(const GemmLaunch& g, cudaStream_t st) {
   init_gemm_attributes();
   if (g.pair) {
-    if constexpr (BN >= 128) {
+    // 64-wide pair tiles: forward (K-major B) only, no split-K / halo
+    if constexpr (BN >= 128 || (BN == 64 && !A_MN && !B_MN && EPI == kEpiFwd)) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>;
-    if constexpr (EPI != kEpiWgradSgd)
+    if constexpr (EPI != kEpiWgradSgd && BN >= 128)
       if (g.ext) kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>;
+    if (BN < 128 && g.ext) throw std::logic_error("64-wide pair tiles: no split-K / halo");
     constexpr int smem = Gemm2Cfg<BN, EPI>::kSmem;
     const int tiles_m = g.sh.halo_tw ? (g.sh.M / g.sh.halo_tw + 1) / 2 : (g.sh.M + 255) / 256;
     const int tiles = tiles_m * ((g.sh.N + BN - 1) / BN);
@@ -177,6 +190,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl_on(g) ? 1 : 0;
     PB_CUDA(cudaLaunchKernelEx(&cfg, kern, g.ta, g.tb, g.sh, g.ep, g.maps));
+    } else {
+      throw std::logic_error("64-wide pair tiles: forward only");
     }
   } else if constexpr (BN <= 256) {
     auto kern = gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>;
@@ -215,8 +230,12 @@ void set_attr() {
     PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GemmCfg<BN>::kSmem));
-  if constexpr (BN < 128) return;  // single-CTA only
-  else {
+  if constexpr (BN < 128) {  // single-CTA, plus the forward pair kernel
+    if constexpr (!A_MN && !B_MN && EPI == kEpiFwd)
+      PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Gemm2Cfg<BN, EPI>::kSmem));
+  } else {
   PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                Gemm2Cfg<BN, EPI>::kSmem));
@@ -233,7 +252,7 @@ void launch_bn(const GemmLaunch& g, cudaStream_t st) {
     if (g.bn == 512) return launch_one<512, A_MN, B_MN, EPI>(g, st);
   if (g.bn == 256)
     launch_one<256, A_MN, B_MN, EPI>(g, st);
-  else if (g.bn == 64 && !g.pair)
+  else if (g.bn == 64)
     launch_one<64, A_MN, B_MN, EPI>(g, st);
   else
     launch_one<128, A_MN, B_MN, EPI>(g, st);
@@ -467,6 +486,7 @@ GemmLaunch plan_fwd(const Mat16& x, int x_row_off, int rows, const Mat16& w,
     g.bn = pick_bn(rows, w.rows);
     g.pair = use_pair(rows);
     if (g.pair && wide_tiles(rows, w.rows)) g.bn = 512;
+    if (g.pair && pair_bn64(w.rows)) g.bn = 64;
   }
   g.ta = make_operand_tmap(x, /*k_major=*/true, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
@@ -811,8 +831,8 @@ GemmLaunch plan_conv_fwd(const Nhwc& x, int img0, int imgs, const Mat16& w, cons
   const int hw = x.h * x.w;
   GemmLaunch g;
   g.pair = true;
-  g.bn = w.rows > 128 ? 256 : 128;
   const int tw = halo_width(x.w);
+  g.bn = w.rows > 128 ? 256 : (pair_bn64(w.rows) && !tw ? 64 : 128);
   g.ta = tw ? make_patch_tmap(x, tw) : make_im2col_tmap(x, 128);
   g.tb = make_operand_tmap(w, /*k_major=*/true, b_box(g));
   g.sh = GemmShape{imgs * hw, w.rows, 9 * x.c, img0 * hw, 0, 0, 0, 1, 0};

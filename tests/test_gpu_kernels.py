@@ -36,6 +36,8 @@ def _rel(got, want):
 FWD_SHAPES = [
     (128, 256, 128), (64, 784, 512), (64, 512, 256), (64, 256, 10), (5, 2, 8),
     (200, 100, 10), (256, 4096, 4096), (128, 4096, 4096), (1000, 136, 392),
+    # 64-wide pair tiles (out <= 64, rows > 128), ragged rows
+    (1000, 136, 64), (300, 72, 40),
     # split-K shapes (K >= 1024): ragged N, ragged last split, partial M tiles
     (1024, 4096, 4096), (512, 1024, 1536), (384, 2048, 1000), (100, 3000, 700),
     # 256 x 512 tiles with a partial last row tile / ragged rows
