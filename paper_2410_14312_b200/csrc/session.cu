@@ -1779,6 +1779,25 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       kernels_per_epoch_ += I.digest->launches_per(I.dplans.back());
     }
   }
+  // PIPESIM_DUMP_OPS=file: the epoch's op program (stream, kind, event) for
+  // reading the dependency chains (works with plan_only, no GPU)
+  if (const char* path = std::getenv("PIPESIM_DUMP_OPS")) {
+    static const char* kNames[] = {"wait", "record", "fwd", "dgrad", "wgrad", "bias", "loss",
+                                   "copy", "memset", "snapshot", "send", "recv", "mark",
+                                   "ktime", "xwait", "digest", "im2col", "pool_fwd",
+                                   "pool_bwd", "wgrad_partial", "reduce_sgd", "colsum"};
+    if (FILE* f = std::fopen(path, "w")) {
+      std::map<cudaEvent_t, int> ev_id;
+      for (size_t i = 0; i < I.ops.size(); ++i) {
+        const Impl::Op& o = I.ops[i];
+        int e = -1;
+        if (o.ev) e = ev_id.emplace(o.ev, static_cast<int>(ev_id.size())).first->second;
+        std::fprintf(f, "%zu %d %s %d %d\n", i, o.stream, kNames[static_cast<int>(o.kind)], e,
+                     o.g.sh.M);
+      }
+      std::fclose(f);
+    }
+  }
 }
 
 Session::~Session() = default;
