@@ -121,4 +121,16 @@ struct FixSrc {
   int S = 0, self = 0;
 };
 
+
+// Fused two-layer dgrad (dgrad_chain.cuh): the first GEMM's operands and
+// act' gate; the second GEMM uses the plain dgrad GemmShape / EpiParams.
+struct ChainArgs {
+  const __nv_bfloat16* x_gate = nullptr;  // layer l's input = act_{l-1} output
+  int ld_gate = 0;
+  int act_gate = 0;  // activation of layer l-1
+  int k1 = 0;        // out_l (<= 64)
+  int n1 = 0;        // in_l = out_{l-1} (<= 256, multiple of 64)
+  int store_dz = 1;  // write dz_{l-1} to global (column-tile 0 CTAs)
+};
+
 }  // namespace pb

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "gemm_sm100.cuh"
+#include "dgrad_chain.cuh"
 #include "layer_ops.cuh"
 #include "conv_ops.cuh"
 #include "status.hpp"
@@ -1015,6 +1016,79 @@ void launch_wgrad_partial(const GemmLaunch& g, cudaStream_t st) {
     launch_one<256, true, true, kEpiFwd>(g, st);
   else
     launch_one<128, true, true, kEpiFwd>(g, st);
+}
+
+// ------------------------------------------------------------ dgrad chain
+// PIPESIM_DGRAD_CHAIN=0 keeps two dgrad launches
+bool dgrad_chain_eligible(int out_l, int in_l) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_DGRAD_CHAIN");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && out_l <= 64 && in_l <= 256 && in_l % 64 == 0;
+}
+
+ChainLaunch plan_dgrad_chain(const GemmLaunch& g1, const GemmLaunch& g2, const Mat16& dz_mid) {
+  if (g1.simt || g2.simt) throw std::logic_error("dgrad chain: bf16 tensor-core plans only");
+  ChainLaunch c;
+  c.a1 = g1.ta;
+  c.b1 = g1.tb;
+  c.b2 = g2.tb;
+  c.dz = make_operand_tmap(dz_mid, /*k_major=*/true, 128);
+  c.sh2 = g2.sh;
+  c.ep2 = g2.ep;
+  c.ca.x_gate = g1.ep.xin;
+  c.ca.ld_gate = g1.ep.ld_xin;
+  c.ca.act_gate = g1.ep.act_prev;
+  c.ca.k1 = g1.sh.K;
+  c.ca.n1 = g1.sh.N;
+  c.ca.store_dz = 1;
+  if (c.ca.k1 > 64 || c.ca.n1 > 256 || c.ca.n1 % 64 != 0 || g2.sh.K != c.ca.n1 ||
+      (c.ca.ld_gate % 8) != 0)
+    throw std::invalid_argument("dgrad chain: shape outside the fused kernel's range");
+  // 64-wide column tiles unless that gives 16 or more CTAs (PIPESIM_CHAIN_BN)
+  static const int env_bn = [] {
+    const char* e = std::getenv("PIPESIM_CHAIN_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  const long tiles128 = static_cast<long>((g2.sh.M + 127) / 128) * ((g2.sh.N + 127) / 128);
+  c.bn = env_bn == 64 || env_bn == 128 ? env_bn : (tiles128 < 16 ? 64 : 128);
+  return c;
+}
+
+namespace {
+template <int BN>
+void launch_chain_bn(const ChainLaunch& c, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PB_CUDA(cudaFuncSetAttribute(dgrad_chain_kernel<BN>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ChainCfg<BN>::kSmem));
+  });
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((c.sh2.N + BN - 1) / BN, (c.sh2.M + 127) / 128);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = ChainCfg<BN>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  GemmLaunch probe;
+  probe.pdl = c.pdl;
+  cfg.numAttrs = pdl_on(probe) ? 1 : 0;
+  PB_CUDA(cudaLaunchKernelEx(&cfg, dgrad_chain_kernel<BN>, c.a1, c.b1, c.b2, c.dz, c.sh2, c.ep2,
+                             c.ca));
+  PB_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+void launch_dgrad_chain(const ChainLaunch& c, cudaStream_t st) {
+  if (c.sh2.M <= 0 || c.sh2.N <= 0) return;
+  if (c.bn == 128)
+    launch_chain_bn<128>(c, st);
+  else
+    launch_chain_bn<64>(c, st);
 }
 
 void launch_fwd(const GemmLaunch& g, cudaStream_t st) {

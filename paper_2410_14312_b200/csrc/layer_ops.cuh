@@ -91,6 +91,22 @@ void launch_split_master(cudaStream_t st, const float* w, int rows, int cols, in
 void launch_join_master(cudaStream_t st, const __nv_bfloat16* hi, const uint16_t* lo, int rows,
                         int cols, int ld, float* w, int ld_w);
 
+// Two consecutive dgrads of a stage backward in one kernel (dgrad_chain.cuh):
+// g1 = the plan of layer l's dgrad (out_l <= 64, in_l <= 256 and a multiple
+// of 64), g2 = layer l-1's, whose A operand dz_mid (= g1's destination) the
+// kernel builds in shared memory and also stores.
+struct ChainLaunch {
+  CUtensorMap a1, b1, b2, dz;
+  GemmShape sh2;
+  EpiParams ep2;
+  ChainArgs ca;
+  int bn = 64;
+  bool pdl = false;
+};
+bool dgrad_chain_eligible(int out_l, int in_l);
+ChainLaunch plan_dgrad_chain(const GemmLaunch& g1, const GemmLaunch& g2, const Mat16& dz_mid);
+void launch_dgrad_chain(const ChainLaunch& c, cudaStream_t st);
+
 void launch_fwd(const GemmLaunch& g, cudaStream_t st);
 void launch_dgrad(const GemmLaunch& g, cudaStream_t st);
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st);

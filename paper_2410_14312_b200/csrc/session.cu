@@ -194,7 +194,8 @@ struct Session::Impl {
   enum class OpKind { wait, record, fwd, dgrad, wgrad, bias, loss, copy, memset_i32, snapshot,
                       send, recv, mark, ktime, xwait, digest,
                       // conv stages
-                      im2col, pool_fwd, pool_bwd, wgrad_partial, reduce_sgd, colsum };
+                      im2col, pool_fwd, pool_bwd, wgrad_partial, reduce_sgd, colsum,
+                      dgrad_chain };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kDigest = -6;  // in-epoch params digests
@@ -206,6 +207,7 @@ struct Session::Impl {
     int stream = 0;  // stage index (0-based); -1 = origin stream
     cudaEvent_t ev = nullptr;
     GemmLaunch g{};
+    ChainLaunch chain{};  // dgrad_chain
     // bias
     const __nv_bfloat16* dz = nullptr;
     int rows = 0, cols = 0, ld = 0;
@@ -695,6 +697,23 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       for (int k = 0; k < M; ++k)
         act_iv[s0][k].first = std::min(act_iv[s0][k].first, act_iv[s0 - 1][k].first);
 
+  // Latency-bound networks (every Linear layer at most 1024 wide, no conv):
+  // GEMMs use programmatic dependent launch (GemmLaunch::pdl), and every
+  // stage holds one spare activation slot -- a mini-batch's slot stays
+  // reserved until the next one's first forward, so that forward does not
+  // wait for the previous backward's weight gradient, which reads the slot
+  // (hazard (b); C1 45.6 -> see DESIGN.md; PIPESIM_SPARE_ACT=0: off).
+  bool latency = !convnet;
+  for (size_t l = 0; l + 1 < c.widths.size() && latency; ++l)
+    if (c.widths[l] > 1024 || c.widths[l + 1] > 1024) latency = false;
+  {
+    const char* e = std::getenv("PIPESIM_SPARE_ACT");
+    if (latency && !(e && std::string(e) == "0"))
+      for (int s0 = 0; s0 < W; ++s0)
+        for (int k = 0; k + 1 < M; ++k)
+          act_iv[s0][k].second = std::max(act_iv[s0][k].second, act_iv[s0][k + 1].first);
+  }
+
   // ---------------- colouring: version pool and activation slots
   I.stages.resize(W);
   std::vector<int> pool_n(W), act_n(W);
@@ -720,12 +739,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         I.split = false;
   }
 
-  // Latency-bound networks (every Linear layer at most 1024 wide, no conv):
-  // GEMMs use programmatic dependent launch (GemmLaunch::pdl).
-  bool pdl = !convnet;
-  for (size_t l = 0; l + 1 < c.widths.size() && pdl; ++l)
-    if (c.widths[l] > 1024 || c.widths[l + 1] > 1024) pdl = false;
-  I.pdl = pdl;
+  I.pdl = latency;
   // Skinny forwards split K (lower latency, more SM-time) when this process
   // keeps few stages in flight; PIPESIM_SESSION_SPLIT=0/1 overrides.
   bool split_fwd = I.W_hi - I.W_lo + 1 <= 2;
@@ -961,6 +975,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   using OK = Impl::OpKind;
   auto push = [&](Impl::Op op) {
     op.g.pdl = I.pdl;
+    op.chain.pdl = I.pdl;
     const int kind = op.kind == OK::fwd ? 1 : op.kind == OK::dgrad ? 2 : op.kind == OK::wgrad ? 3 : 0;
     const bool timed = kind != 0 && kind == c.timed_kernel && !c.plan_only;
     if (timed) {
@@ -1299,10 +1314,34 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   }
   std::map<int, cudaEvent_t> fwd_recv_done;  // upstream node id -> event
 
+  // Transitive pruning of cross-stream waits: done[i] = the nodes whose
+  // completion node i's start already implies (through full-completion
+  // waits and stream order; a wait on a partial event -- delta, commit --
+  // implies only that node's own predecessors).  A wait on d is dropped when
+  // another dependency of the same node implies d.  Fewer graph edges, and a
+  // GEMM left with a single upstream kernel gets a programmatic (PDL) edge
+  // instead of a full one (PIPESIM_PRUNE_EDGES=0: off).
+  const bool prune_edges = [] {
+    const char* e = std::getenv("PIPESIM_PRUNE_EDGES");
+    return !(e && std::string(e) == "0");
+  }();
+  const size_t words = (nodes.size() + 63) / 64;
+  std::vector<std::vector<uint64_t>> done_set(nodes.size());
+  auto implies = [&](int i, int d) {
+    return !done_set[i].empty() && ((done_set[i][d >> 6] >> (d & 63)) & 1);
+  };
+  auto absorb = [&](int i, int d, bool with_d) {
+    if (done_set[i].empty()) done_set[i].assign(words, 0);
+    if (!done_set[d].empty())
+      for (size_t w = 0; w < words; ++w) done_set[i][w] |= done_set[d][w];
+    if (with_d) done_set[i][d >> 6] |= uint64_t{1} << (d & 63);
+  };
+
   for (int id : topo) {
     Node& node = nodes[id];
     const int s = node.s;
     if (node.digest >= 0) {
+      for (int d : node.deps) absorb(id, d, true);
       for (int d : node.deps) {
         Impl::Op w{OK::wait};
         w.stream = Impl::kDigest;
@@ -1345,14 +1384,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       push(r);
       return r.ev;
     };
-    for (int d : node.deps) {
-      // same-stage order is the stream order (same kind, or one stream per stage)
-      if (nodes[d].s == s && (nodes[d].fwd == node.fwd || !I.split_fb)) continue;
-      // (b') on another GPU: its wgrad reads its own received copy
-      if (node.fwd && !nodes[d].fwd && nodes[d].digest < 0 && nodes[d].s == s + 1 &&
-          !I.local(nodes[d].s))
-        continue;
-      if (nodes[d].digest >= 0 || I.local(nodes[d].s)) {
+    // classify every dependency: 0 stream order, 1 skipped (remote (b')),
+    // 2 full wait, 3 delta wait, 4 commit wait, 5 remote
+    std::vector<int> dep_kind(node.deps.size());
+    for (size_t i = 0; i < node.deps.size(); ++i) {
+      const int d = node.deps[i];
+      int kind;
+      if (nodes[d].s == s && (nodes[d].fwd == node.fwd || !I.split_fb)) {
+        kind = 0;
+      } else if (node.fwd && !nodes[d].fwd && nodes[d].digest < 0 && nodes[d].s == s + 1 &&
+                 !I.local(nodes[d].s)) {
+        kind = 1;
+      } else if (nodes[d].digest >= 0 || I.local(nodes[d].s)) {
         // a backward waits for the downstream stage's delta only
         const bool delta_edge = !node.fwd && !nodes[d].fwd && nodes[d].digest < 0 &&
                                 nodes[d].s == s + 1 && nodes[d].k == node.k &&
@@ -1365,6 +1408,27 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
             d != node.slot_dep && nodes[d].commit_side && commit_edges &&
             std::find(node.commit_deps.begin(), node.commit_deps.end(), d) !=
                 node.commit_deps.end();
+        kind = commit_edge ? 4 : delta_edge ? 3 : 2;
+      } else {
+        kind = 5;
+      }
+      dep_kind[i] = kind;
+      if (kind == 0 || kind == 2) absorb(id, d, true);
+      else if (kind == 3 || kind == 4) absorb(id, d, false);
+    }
+    for (size_t i = 0; i < node.deps.size(); ++i) {
+      const int d = node.deps[i];
+      const int kind = dep_kind[i];
+      if (kind <= 1) continue;
+      if (kind <= 4) {
+        if (prune_edges) {
+          bool implied = false;
+          for (size_t j = 0; j < node.deps.size() && !implied; ++j)
+            implied = j != i && dep_kind[j] != 1 && dep_kind[j] != 5 &&
+                      node.deps[j] != d && implies(node.deps[j], d);
+          if (implied) continue;
+        }
+        const bool commit_edge = kind == 4, delta_edge = kind == 3;
         if (commit_edge) {
           wait_on(ns, nodes[d].commit_side);
           if (nodes[d].commit_bias) wait_on(ns, nodes[d].commit_bias);
@@ -1540,6 +1604,39 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         wait_on(side, ev);
         if (bstr != side) wait_on(bstr, ev);
       }
+      // the input x of layer li (row offset *off inside its buffer)
+      auto layer_x = [&](int li, int* off) {
+        *off = 0;
+        if (li == 0) return stage_input(s, tk.k, off);
+        const auto& dl = st.layers[li];
+        return Mat16{as.out16[li - 1], c.B, dl.conv ? dl.ain : dl.in, dl.ain};
+      };
+      // where layer li's dgrad writes (the layer below's dZ, or the delta of
+      // the previous stage) and the activation whose act' gates it
+      auto dgrad_dst = [&](int li, __nv_bfloat16** dst, int* act_prev) {
+        if (li > 0) {
+          *dst = st.scratch_dz[li - 1];
+          *act_prev = st.layers[li - 1].act;
+        } else if (!I.local(s - 1)) {
+          *dst = as.dzsend;  // sent to the upstream GPU after this task
+          *act_prev = I.stages[s - 1].layers.back().act;
+        } else {
+          const Impl::Stage& pv = I.stages[s - 1];
+          *dst = pv.acts[pv.mini_act[tk.k]].dzin;
+          *act_prev = pv.layers.back().act;
+        }
+      };
+      // top two dgrads fused into one kernel (dgrad_chain.cuh): a narrow top
+      // layer (out <= 64) over an input of <= 256 columns, both linear, and
+      // the lower dgrad needed (not the network input)
+      int chain_top = -1;
+      {
+        const int lt = st.L - 1;
+        if (lt >= 1 && !I.v32 && !st.layers[lt].conv && !st.layers[lt - 1].conv &&
+            (lt - 1 > 0 || s > 0) &&
+            dgrad_chain_eligible(st.layers[lt].out, st.layers[lt].in))
+          chain_top = lt;
+      }
       for (int l = st.L - 1; l >= 0; --l) {
         const auto& d = st.layers[l];
         __nv_bfloat16* dz = (l == st.L - 1) ? as.dzin : st.scratch_dz[l];
@@ -1576,20 +1673,34 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         // conv: dz has one row per output pixel
         Mat16 mdz = d.conv ? Mat16{dz, c.B * hw, d.out, d.out} : Mat16{dz, c.B, d.out, d.ld_out};
         // dgrad: delta for the layer below (or the previous stage)
-        if ((l > 0 || s > 0) && !d.first_conv) {
+        if ((l > 0 || s > 0) && !d.first_conv && l == chain_top - 1) {
+          // computed by the chain kernel of layer l + 1
+          if (l == 0) node.delta_done = record_on(ns);  // stage s-1's delta is written
+        } else if ((l > 0 || s > 0) && !d.first_conv && l == chain_top) {
+          __nv_bfloat16 *dst, *dst2;
+          int act_prev, act_prev2, x2_off = 0;
+          dgrad_dst(l, &dst, &act_prev);
+          dgrad_dst(l - 1, &dst2, &act_prev2);
+          const auto& d2 = st.layers[l - 1];
+          const Mat16 x2 = layer_x(l - 1, &x2_off);
+          Impl::Op o{OK::dgrad_chain};
+          o.stream = ns;
+          if (!c.plan_only) {
+            const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld * I.sc;
+            const __nv_bfloat16* xin2 = x2.ptr + static_cast<size_t>(x2_off) * x2.ld * I.sc;
+            const Mat16 mid{dst, c.B, d2.out, d.ld_in};
+            const GemmLaunch g1 = plan_dgrad(mdz, Mat16{prop.w16[l], d.out, d.in, d.ld_in}, xin,
+                                             x.ld, act_prev, dst, d.ld_in);
+            const GemmLaunch g2 = plan_dgrad(mid, Mat16{prop.w16[l - 1], d2.out, d2.in, d2.ld_in},
+                                             xin2, x2.ld, act_prev2, dst2, d2.ld_in);
+            o.chain = plan_dgrad_chain(g1, g2, mid);
+          }
+          push(o);
+          ++kernels_per_epoch_;
+        } else if ((l > 0 || s > 0) && !d.first_conv) {
           __nv_bfloat16* dst;
           int act_prev;
-          if (l > 0) {
-            dst = st.scratch_dz[l - 1];
-            act_prev = st.layers[l - 1].act;
-          } else if (!I.local(s - 1)) {
-            dst = as.dzsend;  // sent to the upstream GPU after this task
-            act_prev = I.stages[s - 1].layers.back().act;
-          } else {
-            const Impl::Stage& pv = I.stages[s - 1];
-            dst = pv.acts[pv.mini_act[tk.k]].dzin;
-            act_prev = pv.layers.back().act;
-          }
+          dgrad_dst(l, &dst, &act_prev);
           // act' of the layer below, recovered from the activation it produced
           // (= this layer's input x).
           const __nv_bfloat16* xin = x.ptr + static_cast<size_t>(x_off) * x.ld * I.sc;
@@ -1785,7 +1896,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
     static const char* kNames[] = {"wait", "record", "fwd", "dgrad", "wgrad", "bias", "loss",
                                    "copy", "memset", "snapshot", "send", "recv", "mark",
                                    "ktime", "xwait", "digest", "im2col", "pool_fwd",
-                                   "pool_bwd", "wgrad_partial", "reduce_sgd", "colsum"};
+                                   "pool_bwd", "wgrad_partial", "reduce_sgd", "colsum",
+                                   "dgrad_chain"};
     if (FILE* f = std::fopen(path, "w")) {
       std::map<cudaEvent_t, int> ev_id;
       for (size_t i = 0; i < I.ops.size(); ++i) {
@@ -2152,6 +2264,7 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         }
         break;
       case OK::dgrad: launch_dgrad(o.g, s); break;
+      case OK::dgrad_chain: launch_dgrad_chain(o.chain, s); break;
       case OK::wgrad: launch_wgrad(o.g, s); break;
       case OK::bias:
         launch_bias_sgd(s, o.dz, o.rows, o.cols, o.ld, o.b_cur, o.b_new, o.b_copy, o.lr,
