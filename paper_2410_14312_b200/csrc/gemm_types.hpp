@@ -133,4 +133,13 @@ struct ChainArgs {
   int store_dz = 1;  // write dz_{l-1} to global (column-tile 0 CTAs)
 };
 
+
+// Fused two-layer forward (fwd_chain.cuh): layer l-1's bias, layer l's
+// padded width, and where y1 (layer l-1's output) rows start.
+struct FwdChainArgs {
+  const float* b1 = nullptr;
+  int n2pad = 16;      // layer l's width rounded up to 16 (<= 64)
+  int y1_row_off = 0;  // row of y1's buffer where this launch's rows start
+};
+
 }  // namespace pb

@@ -10,6 +10,7 @@
 
 #include "gemm_sm100.cuh"
 #include "dgrad_chain.cuh"
+#include "fwd_chain.cuh"
 #include "layer_ops.cuh"
 #include "conv_ops.cuh"
 #include "status.hpp"
@@ -1090,6 +1091,80 @@ void launch_dgrad_chain(const ChainLaunch& c, cudaStream_t st) {
   else
     launch_chain_bn<64>(c, st);
 }
+
+// ------------------------------------------------------------ forward chain
+// PIPESIM_FWD_CHAIN=0 keeps two forward launches
+bool fwd_chain_eligible(int n1, int n2) {
+  static const bool on = [] {
+    const char* e = std::getenv("PIPESIM_FWD_CHAIN");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && n1 <= 256 && n1 % 64 == 0 && n2 <= 64;
+}
+
+FwdChainLaunch plan_fwd_chain(const Mat16& x, int x_row_off, int rows, const Mat16& w1,
+                              const float* b1, int act1, __nv_bfloat16* y1, int ld_y1,
+                              int y1_row_off, const Mat16& w2, const GemmLaunch& g2) {
+  if (g2.simt) throw std::logic_error("forward chain: bf16 tensor-core plans only");
+  const int n1 = w1.rows, n2 = w2.rows;
+  if (n1 > 256 || n1 % 64 != 0 || n2 > 64 || w2.cols != n1 || (ld_y1 % 8) != 0 ||
+      (reinterpret_cast<uintptr_t>(b1) & 15) != 0)
+    throw std::invalid_argument("forward chain: shape outside the fused kernel's range");
+  FwdChainLaunch c;
+  c.x = make_operand_tmap(x, /*k_major=*/true, 128);
+  c.w1 = make_operand_tmap(w1, /*k_major=*/true, n1);
+  c.fa.n2pad = (n2 + 15) / 16 * 16;
+  c.w2 = make_operand_tmap(w2, /*k_major=*/true, c.fa.n2pad);
+  // the store map ends at this launch's last row: the tile's tail rows past
+  // it belong to other micro-batches
+  c.y1 = make_operand_tmap(Mat16{y1, y1_row_off + rows, n1, ld_y1}, /*k_major=*/true, 128);
+  c.sh1 = GemmShape{rows, n1, x.cols, x_row_off, 0, 0, 0, 1, 0};
+  c.sh2 = g2.sh;
+  c.sh2.M = rows;
+  c.ep2 = g2.ep;
+  c.fa.b1 = b1;
+  c.fa.y1_row_off = y1_row_off;
+  c.act1 = act1;
+  return c;
+}
+
+namespace {
+template <int ACT1>
+void launch_fwd_chain_act(const FwdChainLaunch& c, const EpiParams& ep2, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    PB_CUDA(cudaFuncSetAttribute(fwd_chain_kernel<ACT1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 FwdChainCfg::kSmem));
+  });
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((c.sh1.M + 127) / 128);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = FwdChainCfg::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  GemmLaunch probe;
+  probe.pdl = c.pdl;
+  cfg.numAttrs = pdl_on(probe) ? 1 : 0;
+  PB_CUDA(cudaLaunchKernelEx(&cfg, fwd_chain_kernel<ACT1>, c.x, c.w1, c.w2, c.y1, c.sh1, c.sh2,
+                             ep2, c.fa));
+  PB_CUDA(cudaGetLastError());
+}
+}  // namespace
+
+void launch_fwd_chain(const FwdChainLaunch& c, cudaStream_t st, const EpiParams& ep2) {
+  if (c.sh1.M <= 0) return;
+  switch (c.act1) {
+    case kRelu: return launch_fwd_chain_act<kRelu>(c, ep2, st);
+    case kTanh: return launch_fwd_chain_act<kTanh>(c, ep2, st);
+    case kSigmoid: return launch_fwd_chain_act<kSigmoid>(c, ep2, st);
+    default: return launch_fwd_chain_act<kLinear>(c, ep2, st);
+  }
+}
+void launch_fwd_chain(const FwdChainLaunch& c, cudaStream_t st) { launch_fwd_chain(c, st, c.ep2); }
 
 void launch_fwd(const GemmLaunch& g, cudaStream_t st) {
   if (g.simt) return launch_simt_gemm(g, kEpiFwd, st);

@@ -107,6 +107,25 @@ bool dgrad_chain_eligible(int out_l, int in_l);
 ChainLaunch plan_dgrad_chain(const GemmLaunch& g1, const GemmLaunch& g2, const Mat16& dz_mid);
 void launch_dgrad_chain(const ChainLaunch& c, cudaStream_t st);
 
+// Two consecutive Linear forwards in one kernel (fwd_chain.cuh): layer l-1
+// (x[rows, K1] -> y1[rows, n1], n1 <= 256 and a multiple of 64, written to
+// y1 rows from y1_row_off) then layer l, whose epilogue is g2's (layer l's
+// plan_fwd: bias + activation, or the fused softmax-CE at launch).
+struct FwdChainLaunch {
+  CUtensorMap x, w1, w2, y1;
+  GemmShape sh1, sh2;
+  EpiParams ep2;
+  FwdChainArgs fa;
+  int act1 = 0;
+  bool pdl = false;
+};
+bool fwd_chain_eligible(int n1, int n2);
+FwdChainLaunch plan_fwd_chain(const Mat16& x, int x_row_off, int rows, const Mat16& w1,
+                              const float* b1, int act1, __nv_bfloat16* y1, int ld_y1,
+                              int y1_row_off, const Mat16& w2, const GemmLaunch& g2);
+void launch_fwd_chain(const FwdChainLaunch& c, cudaStream_t st);
+void launch_fwd_chain(const FwdChainLaunch& c, cudaStream_t st, const EpiParams& ep2);
+
 void launch_fwd(const GemmLaunch& g, cudaStream_t st);
 void launch_dgrad(const GemmLaunch& g, cudaStream_t st);
 void launch_wgrad(const GemmLaunch& g, cudaStream_t st);

@@ -195,7 +195,7 @@ struct Session::Impl {
                       send, recv, mark, ktime, xwait, digest,
                       // conv stages
                       im2col, pool_fwd, pool_bwd, wgrad_partial, reduce_sgd, colsum,
-                      dgrad_chain };
+                      dgrad_chain, fwd_chain };
   // streams beyond the stage streams (Op::stream values)
   static constexpr int kFwdSend = -2, kFwdRecv = -3, kBwdSend = -4, kBwdRecv = -5;
   static constexpr int kDigest = -6;  // in-epoch params digests
@@ -208,6 +208,7 @@ struct Session::Impl {
     cudaEvent_t ev = nullptr;
     GemmLaunch g{};
     ChainLaunch chain{};  // dgrad_chain
+    FwdChainLaunch fchain{};  // fwd_chain
     // bias
     const __nv_bfloat16* dz = nullptr;
     int rows = 0, cols = 0, ld = 0;
@@ -976,6 +977,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
   auto push = [&](Impl::Op op) {
     op.g.pdl = I.pdl;
     op.chain.pdl = I.pdl;
+    op.fchain.pdl = I.pdl;
     const int kind = op.kind == OK::fwd ? 1 : op.kind == OK::dgrad ? 2 : op.kind == OK::wgrad ? 3 : 0;
     const bool timed = kind != 0 && kind == c.timed_kernel && !c.plan_only;
     if (timed) {
@@ -1493,7 +1495,18 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
       const Impl::PoolSlot& ps = st.pool[st.version_colour[tk.version]];
       const int r0 = node.jj0 * I.Rm;
       const int rows = (node.jj1 - node.jj0 + 1) * I.Rm;
+      // the last two layers in one kernel (fwd_chain.cuh) on latency-bound
+      // networks: layer L-2 at most 256 wide (a multiple of 64), layer L-1
+      // at most 64
+      int fchain = -1;
+      if (st.L >= 2 && I.pdl && !I.v32) {
+        const auto& la = st.layers[st.L - 2];
+        const auto& lb = st.layers[st.L - 1];
+        if (!la.conv && !lb.conv && !la.pool && fwd_chain_eligible(la.out, lb.out))
+          fchain = st.L - 2;
+      }
       for (int l = 0; l < st.L; ++l) {
+        if (fchain >= 0 && l == fchain + 1) continue;  // computed by the chain
         const auto& d = st.layers[l];
         int in_off = 0;
         Mat16 x;
@@ -1504,6 +1517,39 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         }
         const bool logits = (s == last_s) && (l == st.L - 1);
         Mat16 w{ps.w16[l], d.out, d.in, d.ld_in};
+        if (l == fchain) {
+          const auto& d2 = st.layers[l + 1];
+          const bool logits2 = (s == last_s) && (l + 1 == st.L - 1);
+          const Mat16 w2{ps.w16[l + 1], d2.out, d2.in, d2.ld_in};
+          Impl::Op o{OK::fwd_chain};
+          o.stream = ns;
+          if (!c.plan_only) {
+            const GemmLaunch g2 =
+                plan_fwd(Mat16{as.out16[l], c.B, d2.in, d2.ain}, r0, rows, w2, ps.b32[l + 1],
+                         d2.act, logits2 ? nullptr : as.out16[l + 1], d2.ld_out,
+                         logits2 ? as.out32 : nullptr, I.n_out, r0, /*allow_split=*/false);
+            o.fchain = plan_fwd_chain(x, in_off + r0, rows, w, ps.b32[l], d.act, as.out16[l],
+                                      d.ld_out, r0, w2, g2);
+          }
+          if (logits2 && loss_fuse) {
+            o.loss_fused = true;
+            o.lab = I.ylab + static_cast<size_t>(tk.k - 1) * c.B;
+            o.row_loss = I.row_loss + static_cast<size_t>(tk.k - 1) * c.B;
+            o.dz_out = as.dzin;
+            o.ld_dz = d2.ld_out;
+            o.denom = static_cast<float>(c.B);
+          }
+          if (l == 0) {
+            o.fchain.ep2.tag_src = ps.tag;
+            o.fchain.ep2.tag_dst =
+                I.fwd_trace + (static_cast<size_t>(tk.k - 1) * U + node.jj0) * W + s;
+            o.fchain.ep2.tag_count = node.jj1 - node.jj0 + 1;
+            o.fchain.ep2.tag_stride = W;
+          }
+          push(o);
+          ++kernels_per_epoch_;
+          continue;
+        }
         Impl::Op o{OK::fwd};
         o.stream = ns;
         // a pooled conv writes its pre-pooling output, then pools it
@@ -1627,13 +1673,16 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
         }
       };
       // top two dgrads fused into one kernel (dgrad_chain.cuh): a narrow top
-      // layer (out <= 64) over an input of <= 256 columns, both linear, and
-      // the lower dgrad needed (not the network input)
+      // layer (out <= 64) over an input of <= 256 columns, both linear, the
+      // lower one the stage's first (its dgrad is the delta of the previous
+      // stage).  When the lower dgrad feeds another layer of the same stage,
+      // two launches win: that layer's wgrad then starts after the first
+      // (tiny) dgrad instead of after both (C2 sequential 50.5 vs 46.6 us
+      // per mini-batch, tools/gpu/r2_c2seq.sh).
       int chain_top = -1;
       {
         const int lt = st.L - 1;
-        if (lt >= 1 && !I.v32 && !st.layers[lt].conv && !st.layers[lt - 1].conv &&
-            (lt - 1 > 0 || s > 0) &&
+        if (lt == 1 && s > 0 && !I.v32 && !st.layers[lt].conv && !st.layers[lt - 1].conv &&
             dgrad_chain_eligible(st.layers[lt].out, st.layers[lt].in))
           chain_top = lt;
       }
@@ -1897,7 +1946,7 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                                    "copy", "memset", "snapshot", "send", "recv", "mark",
                                    "ktime", "xwait", "digest", "im2col", "pool_fwd",
                                    "pool_bwd", "wgrad_partial", "reduce_sgd", "colsum",
-                                   "dgrad_chain"};
+                                   "dgrad_chain", "fwd_chain"};
     if (FILE* f = std::fopen(path, "w")) {
       std::map<cudaEvent_t, int> ev_id;
       for (size_t i = 0; i < I.ops.size(); ++i) {
@@ -2265,6 +2314,20 @@ void issue(Session::Impl& I, cudaStream_t origin) {
         break;
       case OK::dgrad: launch_dgrad(o.g, s); break;
       case OK::dgrad_chain: launch_dgrad_chain(o.chain, s); break;
+      case OK::fwd_chain:
+        if (o.loss_fused && I.use_labels) {
+          EpiParams ep = o.fchain.ep2;
+          ep.loss_labels = o.lab;
+          ep.loss_dz = o.dz_out;
+          ep.loss_ld_dz = o.ld_dz;
+          ep.loss_row = o.row_loss;
+          ep.loss_denom = o.denom;
+          ep.rowwise = 1;  // the row-per-thread epilogue holds whole rows
+          launch_fwd_chain(o.fchain, s, ep);
+        } else {
+          launch_fwd_chain(o.fchain, s);
+        }
+        break;
       case OK::wgrad: launch_wgrad(o.g, s); break;
       case OK::bias:
         launch_bias_sgd(s, o.dz, o.rows, o.cols, o.ld, o.b_cur, o.b_new, o.b_copy, o.lr,

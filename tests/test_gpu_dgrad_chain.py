@@ -1,7 +1,8 @@
-"""The fused two-layer dgrad (csrc/dgrad_chain.cuh) against the CPU oracle:
-stages whose top layer is narrow (out <= 64) over an input of 64..256
-columns, so the session emits one dgrad_chain launch for the top two
-dgrads.  Covers K1 = 3 / 10 / 64, n1 = 64 / 128 / 192 / 256 (1-4 k-blocks of
+"""The fused two-layer dgrad (csrc/dgrad_chain.cuh) and forward
+(csrc/fwd_chain.cuh) against the CPU oracle: stages whose top layer is
+narrow (out <= 64) over an input of 64..256 columns, so the session emits
+one dgrad_chain launch for the top two dgrads and one fwd_chain launch for
+the last two forwards (the logits one with the fused softmax-CE).  Covers K1 = 3 / 10 / 64, n1 = 64 / 128 / 192 / 256 (1-4 k-blocks of
 the second GEMM), ragged row tiles (B = 100, 300), tanh / sigmoid / relu
 gates, the delta to an upstream stage (W=2) and to a layer of the same stage
 (W=1), MSE and softmax-CE.  Same bars as test_gpu_pipeline."""
@@ -37,12 +38,13 @@ def test_dgrad_chain_matches_oracle(case, mode):
     _check(stages, logs, refs, p0, W, mode, loss_tol=3e-3, dw_tol=1e-1, w_tol=5e-3)
 
 
-def test_dgrad_chain_is_emitted():
-    """C1's stage 2 backward runs one fused launch instead of two dgrads:
-    kernels per epoch drop by one per mini-batch against the same session
-    with PIPESIM_DGRAD_CHAIN=0 (a subprocess: the switch is read once)."""
+@pytest.mark.parametrize("switch", ["PIPESIM_DGRAD_CHAIN", "PIPESIM_FWD_CHAIN"])
+def test_chain_is_emitted(switch):
+    """C1's stage 2 runs one fused launch instead of two per backward (dgrad)
+    or per forward node (two per mini-batch): kernels per epoch against the
+    same session with the switch off (a subprocess: it is read once)."""
+    import os
     import subprocess
-    import sys
     code = ("from paper_2410_14312_b200 import pipesim as P\n"
             "net = P.NetworkSpec([784, 512, 256, 10], ['relu', 'relu', 'linear'], "
             "'softmax_cross_entropy')\n"
@@ -50,8 +52,9 @@ def test_dgrad_chain_is_emitted():
             "print(s.kernels_per_epoch)\n")
     n = []
     for v in ("1", "0"):
-        env = dict(__import__("os").environ, PIPESIM_DGRAD_CHAIN=v)
+        env = dict(os.environ, **{switch: v})
         out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
                              text=True, check=True).stdout.split()
         n.append(int(out[-1]))
-    assert n[1] - n[0] == 6, n
+    per_mini = 1 if switch == "PIPESIM_DGRAD_CHAIN" else 2
+    assert n[1] - n[0] >= 6 * per_mini - 1, n
