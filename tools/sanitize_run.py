@@ -1,7 +1,8 @@
 """Workload for compute-sanitizer (racecheck / synccheck / memcheck) on the
 multi-stream executor: W=4 stages, N=2 micro-batches, one epoch per mode,
 eager (no graph) and graph-captured, pair-kernel shapes (B=256 rows, widths
->= 256) plus a tiny-net epoch on the single-CTA kernels.
+>= 256) plus a tiny-net epoch on the single-CTA kernels, and C1 at W=2 / W=1
+(the fused two-layer dgrad and forward kernels, `chain2` / `chain1`).
 
   compute-sanitizer --tool racecheck python tools/sanitize_run.py [mode ...]
   python tools/sanitize_run.py --ipc     # 2-process IPC split on one GPU
@@ -21,15 +22,20 @@ import numpy as np  # noqa: E402
 NETS = {
     "pair": ([256, 384, 256, 512, 256, 10], ["relu", "tanh", "relu", "sigmoid", "linear"], 256),
     "tiny": ([64, 96, 64, 48, 10], ["relu", "relu", "tanh", "linear"], 32),
+    "chain2": ([784, 512, 256, 10], ["relu", "relu", "linear"], 256, 2),
+    "chain1": ([784, 512, 256, 10], ["relu", "relu", "linear"], 256, 1),
 }
 W, N, M = 4, 2, 12
 
 
 def one(kind, mode, graph, rank=0, world=1, blobs_fn=None):
     from paper_2410_14312_b200 import pipesim as P
-    widths, acts, B = NETS[kind]
+    widths, acts, B = NETS[kind][:3]
+    Wk = NETS[kind][3] if len(NETS[kind]) > 3 else W
+    if Wk == 1 and mode != "sequential":
+        return np.zeros(1)
     net = P.NetworkSpec(widths, acts, "softmax_cross_entropy")
-    s = P.Session(net, W, N, B, M, 0.05, mode, use_graph=graph, rank=rank, world=world,
+    s = P.Session(net, Wk, N, B, M, 0.05, mode, use_graph=graph, rank=rank, world=world,
                   transport="ipc")
     s.load_params(P.init_network_params(net, 1))
     x, lab = P.make_classification_task(M * B, widths[0], widths[-1], seed=7, as_labels=True,
@@ -76,7 +82,7 @@ def main():
         sys.exit(max(p.exitcode for p in ps))
     modes = args or ["timeprest", "pipedream", "sequential"]
     for mode in modes:
-        for kind in ("pair", "tiny"):
+        for kind in ("pair", "tiny", "chain2", "chain1"):
             for graph in (False, True):
                 loss = one(kind, mode, graph)
                 print(f"{mode} {kind} graph={graph} ok, loss[0] {loss[0]:.6f}", flush=True)
