@@ -343,9 +343,10 @@ __device__ __forceinline__ void epilogue_warp_tile(const EpiParams& ep, const Ge
 }
 
 // Row-per-thread epilogue (thread i owns row i; 16-column vector chunks).
-// Softmax cross-entropy of one row of logits (raw accumulators v + bias, a
-// linear head) against its class label, in the forward epilogue: the loss
-// kernel's formulas (max-subtracted, one exp per logit) on registers.
+// Softmax cross-entropy of one row of logits against its class label, in the
+// forward epilogue: the loss kernel's formulas (max-subtracted, one exp per
+// logit) on registers.  v holds the finished logits (epilogue_chunk has
+// added the bias of the linear head in place).
 __device__ __forceinline__ void fused_ce_row(const EpiParams& ep, int row, const float (&v)[16],
                                              int valid) {
   const size_t r = static_cast<size_t>(row + ep.y_row_off);
@@ -353,7 +354,7 @@ __device__ __forceinline__ void fused_ce_row(const EpiParams& ep, int row, const
   float mx = -INFINITY;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    z[i] = i < valid ? v[i] + (ep.bias ? ep.bias[i] : 0.f) : -INFINITY;
+    z[i] = i < valid ? v[i] : -INFINITY;
     mx = fmaxf(mx, z[i]);
   }
   const int lab = ep.loss_labels[r];

@@ -5,13 +5,11 @@ math; the reference itself has no convolution).
 Bars (bf16 operands and activations, fp32 accumulate, fp32 masters):
   * pins, update_source and the device-observed version tags: bit-exact;
   * against the fp64 oracle over whole epochs: per-mini-batch loss relative
-    1e-2, final weights ||W - W_ref|| / ||W_ref|| 1e-3, weight deltas
-    ||dW - dW_ref|| / ||dW_ref|| 1.5e-1 (measured <= 5.1e-3 / 4.3e-4 / 9.6e-2:
+    5e-3, final weights ||W - W_ref|| / ||W_ref|| 1e-3, weight deltas
+    ||dW - dW_ref|| / ||dW_ref|| 1.5e-1 (measured <= 3.4e-3 / 4.3e-4 / 9.6e-2:
     besides operand rounding, 2x2 max pooling routes a window's gradient to
     another pixel whenever bf16 rounding ties or reorders its maximum, and
-    such flips compound over the 20 mini-batches of the two-epoch case --
-    a change of summation order in the softmax moved it from 3.4e-3 to
-    5.1e-3);
+    such flips compound over the 20 mini-batches of the two-epoch case);
   * one SGD step against the oracle with the device's bf16 storage rounding
     (storage="bf16", which routes pooling gradients through the rounded
     windows like the device): loss 1e-5, the Linear layers' updates 1e-4,
@@ -55,7 +53,7 @@ def _run(net, W, N, B, M, lr, mode="timeprest", seed=3, epochs=1, storage="fp64"
     return outs, refs, got, p0
 
 
-def _check(outs, refs, got, p0, W, M, mode, loss_tol=1e-2, w_tol=1e-3, dw_tol=1.5e-1):
+def _check(outs, refs, got, p0, W, M, mode, loss_tol=5e-3, w_tol=1e-3, dw_tol=1.5e-1):
     rels = [np.abs(r["mini_loss"] - ref["losses"]).max() / np.abs(ref["losses"]).max()
             for r, ref in zip(outs, refs)]
     want = refs[-1]["params"]

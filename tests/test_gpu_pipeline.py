@@ -230,6 +230,35 @@ def test_session_resident_epochs_and_labels():
     assert not np.array_equal(outs[0][0], outs[0][1])  # epoch 2 starts from trained weights
 
 
+@pytest.mark.parametrize("widths,W", [([128, 256, 10], 2), ([784, 512, 256, 10], 2),
+                                      ([784, 512, 256, 10], 1)])
+def test_fused_softmax_ce_matches_loss_kernel(widths, W):
+    """Class labels with <= 16 logits take the softmax-CE fused into the
+    logits epilogue (and the fused two-layer forward on C1's shapes); one-hot
+    targets take the separate loss kernel.  Same losses and weights."""
+    acts = ["relu"] * (len(widths) - 2) + ["linear"]
+    net = P.NetworkSpec(widths, acts, "softmax_cross_entropy")
+    p0 = P.init_network_params(net, 1)
+    x, labels = P.make_classification_task(8 * 64, widths[0], widths[-1], seed=7, as_labels=True,
+                                           dtype=np.float32)
+    onehot = np.zeros((len(labels), widths[-1]), np.float32)
+    onehot[np.arange(len(labels)), labels] = 1
+    mode = "timeprest" if W > 1 else "sequential"
+    outs = []
+    for y, lab in ((labels, True), (onehot, False)):
+        s = P.Session(net, W, 4, 64, 8, 0.05, mode)
+        s.load_params(p0)
+        s.upload(x, y, y_labels=lab)
+        r1 = s.run_epoch()
+        r2 = s.run_epoch()
+        outs.append((r1["mini_loss"], r2["mini_loss"], s.read_params()))
+        s.close()
+    for a, b in zip(outs[0][:2], outs[1][:2]):
+        np.testing.assert_allclose(a, b, rtol=1e-5)
+    d = np.linalg.norm(outs[0][2] - outs[1][2]) / np.linalg.norm(outs[1][2] - p0)
+    assert d < 1e-3, d
+
+
 @pytest.mark.parametrize("mode", ["timeprest", "pipedream"])
 def test_forward_coalescing_is_bit_identical(mode):
     """Coalesced forwards (one GEMM over consecutive micro-batches with the same
