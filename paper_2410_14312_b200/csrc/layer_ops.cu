@@ -1112,7 +1112,7 @@ FwdChainLaunch plan_fwd_chain(const Mat16& x, int x_row_off, int rows, const Mat
     throw std::invalid_argument("forward chain: shape outside the fused kernel's range");
   FwdChainLaunch c;
   c.x = make_operand_tmap(x, /*k_major=*/true, 128);
-  c.w1 = make_operand_tmap(w1, /*k_major=*/true, n1);
+  c.w1 = make_operand_tmap(w1, /*k_major=*/true, 64);  // one 64-row slice per cluster CTA
   c.fa.n2pad = (n2 + 15) / 16 * 16;
   c.w2 = make_operand_tmap(w2, /*k_major=*/true, c.fa.n2pad);
   // the store map ends at this launch's last row: the tile's tail rows past
@@ -1137,18 +1137,23 @@ void launch_fwd_chain_act(const FwdChainLaunch& c, const EpiParams& ep2, cudaStr
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  FwdChainCfg::kSmem));
   });
+  const int C = c.sh1.N / 64;  // cluster: one CTA per 64 columns of y1
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((c.sh1.M + 127) / 128);
+  cfg.gridDim = dim3(C, (c.sh1.M + 127) / 128);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = FwdChainCfg::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   GemmLaunch probe;
   probe.pdl = c.pdl;
-  cfg.numAttrs = pdl_on(probe) ? 1 : 0;
+  cfg.numAttrs = pdl_on(probe) ? 2 : 1;
   PB_CUDA(cudaLaunchKernelEx(&cfg, fwd_chain_kernel<ACT1>, c.x, c.w1, c.w2, c.y1, c.sh1, c.sh2,
                              ep2, c.fa));
   PB_CUDA(cudaGetLastError());
