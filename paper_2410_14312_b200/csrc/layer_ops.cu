@@ -549,9 +549,27 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
   return g;
 }
 
+// Latency-bound networks (layers <= 1024 wide): the wgrad+SGD of a layer
+// runs on the single-CTA kernel with 64-wide tiles -- for C1's 512 x 784
+// layer 52 CTAs each updating 8K parameters instead of 14 CTA pairs each
+// updating 32K; the update, not the flops, is the critical path there (C1
+// 41.9 -> 39.1 us per mini-batch, C2 sequential 44.1 -> 39.2 us,
+// tools/gpu/r2_wgsingle.sh).  PIPESIM_WGRAD_SINGLE=0|64|128 overrides.
+int latency_wgrad_bn(int out, int in) {
+  static const int env = [] {
+    const char* e = std::getenv("PIPESIM_WGRAD_SINGLE");
+    return e ? std::atoi(e) : -1;
+  }();
+  (void)out;
+  (void)in;
+  if (env == 0 || env == 64 || env == 128) return env;
+  return 64;
+}
+
 GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           const float* w_cur, float* w_new, int ld_w32,
-                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify) {
+                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify,
+                          int single_bn) {
   GemmLaunch g;
   if (verify) {
     g.simt = true;
@@ -569,8 +587,8 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
     g.ep.lr = lr;
     return g;
   }
-  g.bn = pick_bn(dz.cols, x.cols);
-  g.pair = use_pair(dz.cols);
+  g.bn = single_bn > 0 ? single_bn : pick_bn(dz.cols, x.cols);
+  g.pair = single_bn > 0 ? false : use_pair(dz.cols);
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
   g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};

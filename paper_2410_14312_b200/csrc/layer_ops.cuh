@@ -72,9 +72,15 @@ GemmLaunch plan_dgrad(const Mat16& dz, const Mat16& w, const __nv_bfloat16* xin,
                       bool verify = false);
 // wgrad+SGD: w_new[out,in] = w_cur - lr * dz[rows,out]^T x[rows,in]
 // (x rows start at x_row_off inside its buffer)
+// (single_bn > 0: the single-CTA kernel with single_bn-wide tiles -- more,
+// smaller update tiles for a latency-bound network)
 GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
                           const float* w_cur, float* w_new, int ld_w32,
-                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify = false);
+                          __nv_bfloat16* w16, int ld_w16, float lr, bool verify = false,
+                          int single_bn = 0);
+// single_bn for plan_wgrad_sgd on a latency-bound network (0: the default
+// tiling; PIPESIM_WGRAD_SINGLE=64|128|0 overrides)
+int latency_wgrad_bn(int out, int in);
 
 // wgrad+SGD with split fp32 masters (gemm_sm100.cuh: master = hi << 16 + lo):
 // reads hi/lo of the current version, writes hi (the new version's bf16

@@ -1817,7 +1817,8 @@ Session::Session(const SessionConfig& cfg_in) : cfg_(cfg_in) {
                                          static_cast<float>(c.lr));
             else
               o.g = plan_wgrad_sgd(mdz, x, x_off, d.w32[cur], d.w32[nxt], d.in, next.w16[l],
-                                   d.ld_in, static_cast<float>(c.lr), I.v32);
+                                   d.ld_in, static_cast<float>(c.lr), I.v32,
+                                   I.pdl ? latency_wgrad_bn(d.out, d.in) : 0);
           }
           push(o);
           ++kernels_per_epoch_;

@@ -7,3 +7,4 @@ for rep in 1 2; do timeout 300 python tools/c_timing.py --W 1 --mode sequential 
 timeout 600 python tools/configs.py --out $O/configs_r2.json > $O/configs_r2.md 2> $O/configs.err; echo configs rc=$?
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo bench rc=$?
 python -c "import json;d=json.load(open('$O/bench.json'));print(round(d['value']), round(d['ms_per_step'],2), round(d['e2e']['value']), d['roofline']['frac'], d['clocks'])"
+timeout 600 python tools/vgg_bench.py --W 4 8 --M 16 --profile --out $O/vgg16_bench.json > /dev/null 2> $O/vgg.err; echo vgg rc=$?
