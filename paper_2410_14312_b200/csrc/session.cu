@@ -2435,6 +2435,9 @@ EpochResult Session::run_epoch() {
         throw;
       }
       PB_CUDA(cudaStreamEndCapture(I.origin, &I.graph));
+      // PIPESIM_GRAPH_DOT=file: the captured graph (nodes, edges, edge types)
+      if (const char* dot = std::getenv("PIPESIM_GRAPH_DOT"))
+        cudaGraphDebugDotPrint(I.graph, dot, cudaGraphDebugDotFlagsVerbose);
       PB_CUDA(cudaGraphInstantiate(&I.exec, I.graph, 0));
     }
     PB_CUDA(cudaGraphLaunch(I.exec, I.origin));
