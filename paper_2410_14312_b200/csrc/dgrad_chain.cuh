@@ -5,15 +5,18 @@
 //   dz_{l-1} = (dz_l W_l) . act'_{l-1}        128 x n1, K1 <= 64
 //   delta    = (dz_{l-1} W_{l-1}) . act'_gate   128 x BN tile, K2 = n1 <= 256
 //
-// Each CTA owns 128 rows and one BN-wide column tile of delta.  It computes
-// its rows of dz_{l-1} itself -- one k-block of MMAs into TMEM (256
-// columns), the act' gate on the way out -- and writes them as bf16 straight
-// into shared memory in the 128B-swizzled K-major layout the second GEMM's
-// A operand needs, so dz_{l-1} never makes an L2 round trip before use.  The
-// CTAs of column tile 0 also TMA-store those rows to global memory (the
-// wgrad / bias of layer l-1 read them).  The CTAs of the other column tiles
-// recompute the same 128 x n1 block: one 128 x 256 x 64 MMA, cheaper than a
-// second launch.
+// Each CTA owns 128 rows and one BN-wide column tile of delta.  dz_{l-1}
+// for its rows -- one k-block of MMAs into TMEM, the act' gate on the way
+// out -- is written as bf16 straight into shared memory in the 128B-swizzled
+// K-major layout the second GEMM's A operand needs, so it never makes an L2
+// round trip before use.  With a cluster of C = n1 / 64 CTAs along the
+// column tiles (ChainArgs::cluster), CTA r computes only the 64 columns
+// [64r, 64r + 64) of dz_{l-1} (and TMA-stores them for the wgrad / bias of
+// layer l-1 when it is in the first cluster of the row block), then copies
+// its peers' slices over distributed shared memory into its own A tiles
+// (plain loads and stores, then a proxy fence: the tensor core reads only
+// locally written shared memory).  Without a cluster each CTA computes the
+// whole 128 x n1 block and the column-tile-0 CTAs store it.
 //
 // On the C1 backward (784-512-256-10, stage 2 = [512->256, 256->10]) this
 // replaces the 10-wide L3 dgrad launch on the pipeline's dependency cycle
@@ -63,7 +66,10 @@ __global__ void __launch_bounds__(128, 1)
   const int m0 = blockIdx.y * 128;
   const int n0 = blockIdx.x * BN;
   const int kb2 = (ca.n1 + 63) / 64;
-  const bool store = ca.store_dz && blockIdx.x == 0;
+  const int C = ca.cluster > 1 ? ca.cluster : 1;
+  const int rank = C > 1 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  const int t0 = C > 1 ? rank : 0, t1 = C > 1 ? rank + 1 : kb2;  // dz_{l-1} tiles built here
+  const bool store = ca.store_dz && static_cast<int>(blockIdx.x) < C;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tm_a1);
@@ -83,9 +89,10 @@ __global__ void __launch_bounds__(128, 1)
 
   if (warp == 0 && lane == 0) {
     // operands of both GEMMs at once: at most 1 + 4 + 4 * BN / 64 boxes
-    ptx::mbar_arrive_expect_tx(&bar[0], Cfg::kA1 + kb2 * 8192);
+    ptx::mbar_arrive_expect_tx(&bar[0], Cfg::kA1 + (t1 - t0) * 8192);
     ptx::tma_load_2d(sA1, &tm_a1, &bar[0], 0, m0);
-    for (int h = 0; h < kb2; ++h) ptx::tma_load_2d(sB1 + h * 8192, &tm_b1, &bar[0], h * 64, 0);
+    for (int h = t0; h < t1; ++h)
+      ptx::tma_load_2d(sB1 + (h - t0) * 8192, &tm_b1, &bar[0], h * 64, 0);
     ptx::mbar_arrive_expect_tx(&bar[1], kb2 * Cfg::kB2Blk);
     for (int j = 0; j < kb2; ++j)
 #pragma unroll
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(128, 1)
     // nothing; columns past n1 are never read)
     ptx::mbar_wait(&bar[0], 0);
     ptx::tc_fence_after();
-    constexpr uint32_t idesc1 = ptx::idesc_bf16_f32(128, 256, false, true);
+    const uint32_t idesc1 = ptx::idesc_bf16_f32(128, 64 * (t1 - t0), false, true);
     const uint32_t a = ptx::smem_u32(sA1), b = ptx::smem_u32(sB1);
     const int ksteps = (ca.k1 + 15) / 16;
     for (int kk = 0; kk < ksteps; ++kk)
@@ -114,9 +121,9 @@ __global__ void __launch_bounds__(128, 1)
     const int row = m0 + rl;
     const bool live = row < sh2.M;
     const __nv_bfloat16* xg = ca.x_gate + static_cast<size_t>(live ? row : 0) * ca.ld_gate;
-    for (int c = 0; c < ca.n1; c += 32) {
+    for (int c = 64 * t0; c < 64 * t1; c += 32) {
       uint32_t r[32];
-      ptx::tmem_ld32(acc1 + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
+      ptx::tmem_ld32(acc1 + (static_cast<uint32_t>(warp * 32) << 16) + (c - 64 * t0), r);
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -145,10 +152,27 @@ __global__ void __launch_bounds__(128, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if (C > 1) {
+    // the peers' slices: DSMEM loads into this CTA's own A tiles (16 KB each)
+    ptx::cluster_sync();
+    for (int p = 0; p < C; ++p) {
+      if (p == rank) continue;
+      const uint32_t src = ptx::map_to_rank(sA2 + p * Cfg::kA2Tile, p);
+      float4* dst = reinterpret_cast<float4*>(sA2 + p * Cfg::kA2Tile);
+#pragma unroll
+      for (int i = 0; i < Cfg::kA2Tile / 16 / 128; ++i) {
+        const int e = i * 128 + static_cast<int>(threadIdx.x);
+        dst[e] = ptx::ld_dsmem_f4(src + 16 * e);
+      }
+    }
+    ptx::fence_proxy_async();
+    ptx::cluster_sync();  // every peer's reads of this CTA's slice are done
+    ptx::tc_fence_after();
+  }
 
   if (warp == 0 && lane == 0) {
     if (store) {
-      for (int j = 0; j < kb2; ++j) ptx::tma_store_2d(&tm_dz, sA2 + j * Cfg::kA2Tile, j * 64, m0);
+      for (int j = t0; j < t1; ++j) ptx::tma_store_2d(&tm_dz, sA2 + j * Cfg::kA2Tile, j * 64, m0);
       ptx::bulk_commit_group();
     }
     if (blockIdx.x == 0 && blockIdx.y == 0 && ep2.tag_src && ep2.tag_dst)

@@ -131,6 +131,7 @@ struct ChainArgs {
   int k1 = 0;        // out_l (<= 64)
   int n1 = 0;        // in_l = out_{l-1} (<= 256, multiple of 64)
   int store_dz = 1;  // write dz_{l-1} to global (column-tile 0 CTAs)
+  int cluster = 1;   // CTAs per cluster along the column tiles (n1 / 64, or 1)
 };
 
 

@@ -1072,6 +1072,17 @@ ChainLaunch plan_dgrad_chain(const GemmLaunch& g1, const GemmLaunch& g2, const M
   }();
   const long tiles128 = static_cast<long>((g2.sh.M + 127) / 128) * ((g2.sh.N + 127) / 128);
   c.bn = env_bn == 64 || env_bn == 128 ? env_bn : (tiles128 < 16 ? 64 : 128);
+  // PIPESIM_CHAIN_CLUSTER=1: a cluster of n1 / 64 CTAs along the column
+  // tiles builds dz_{l-1} once per row block.  Off by default: on C1 it is
+  // 0.35 us slower under TiMePReSt (the cluster barriers on the cycle cost
+  // more than the recomputation they save) and 0.7 us faster under 1F1B
+  // (tools/gpu/r2_chain_cluster.sh).
+  static const bool cluster_on = [] {
+    const char* e = std::getenv("PIPESIM_CHAIN_CLUSTER");
+    return e && std::string(e) == "1";
+  }();
+  const int C = c.ca.n1 / 64, tiles_n = (g2.sh.N + c.bn - 1) / c.bn;
+  c.ca.cluster = cluster_on && C > 1 && tiles_n % C == 0 ? C : 1;
   return c;
 }
 
@@ -1089,13 +1100,24 @@ void launch_chain_bn(const ChainLaunch& c, cudaStream_t st) {
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = ChainCfg<BN>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (c.ca.cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = c.ca.cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   GemmLaunch probe;
   probe.pdl = c.pdl;
-  cfg.numAttrs = pdl_on(probe) ? 1 : 0;
+  if (pdl_on(probe)) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
   PB_CUDA(cudaLaunchKernelEx(&cfg, dgrad_chain_kernel<BN>, c.a1, c.b1, c.b2, c.dz, c.sh2, c.ep2,
                              c.ca));
   PB_CUDA(cudaGetLastError());
