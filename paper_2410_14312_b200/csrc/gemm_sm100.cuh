@@ -1277,10 +1277,15 @@ __device__ __forceinline__ void conv_loads_b(const GemmShape& sh, const CUtensor
       ptx::tma_load_2d_pair(bj, tb, fb, k0, nbj);  // W [Cout, 9C], K-major
     } else {
       // W viewed [Cout][9][Cin]: 64 output channels (K) x 64 input channels
-      // (N) of the flipped tap, MN-major
+      // (N) of the flipped tap, MN-major; 64-wide MMAs: 32 input channels per
+      // CTA, one 64-byte-swizzled box
+      if constexpr (Cfg::kMmaN == 64) {
+        ptx::tma_load_3d_pair(bj, tb, fb, nbj, 8 - tap, c0);
+      } else {
 #pragma unroll
-      for (int h = 0; h < Cfg::kMmaN / 128; ++h)
-        ptx::tma_load_3d_pair(bj + h * 8192, tb, fb, nbj + h * 64, 8 - tap, c0);
+        for (int h = 0; h < Cfg::kMmaN / 128; ++h)
+          ptx::tma_load_3d_pair(bj + h * 8192, tb, fb, nbj + h * 64, 8 - tap, c0);
+      }
     }
   }
 }
@@ -1326,6 +1331,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
                            EpiParams ep, const __grid_constant__ EpiMaps maps) {
   using Cfg = Gemm2Cfg<BN, EPI>;
   constexpr int S = Cfg::kStages;
+  // 64-wide MMAs with an MN-major B exist only for the conv dgrad's 64-byte
+  // swizzled weight boxes (the other MN-major loads are 64 columns wide)
+  if constexpr (B_MN && Cfg::kMmaN == 64)
+    if (sh.conv != 3) __trap();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the shared array
   // itself, so every derived pointer stays in the shared address space.
@@ -1541,7 +1550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
                 for (int j = 0; j < Cfg::kSub; ++j) {
                   const uint32_t bj = b_addr + j * Cfg::kBSub;
                   const uint64_t b_desc =
-                      B_MN ? ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024)
+                      B_MN ? (Cfg::kMmaN == 64 ? ptx::smem_desc_sw64(bj + kk * 1024, 4096, 512)
+                                               : ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024))
                            : ptx::smem_desc_sw128(bj + kk * 32, 16, 1024);
                   ptx::mma_bf16_pair(d_tmem + j * Cfg::kMmaN, a_desc, b_desc, idesc,
                                      (c0 | tap | kk) != 0);
@@ -1569,7 +1579,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<BN, EPI>::k
             for (int j = 0; j < Cfg::kSub; ++j) {
               const uint32_t bj = b_addr + j * Cfg::kBSub;
               const uint64_t b_desc =
-                  B_MN ? ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024)
+                  B_MN ? (Cfg::kMmaN == 64 ? ptx::smem_desc_sw64(bj + kk * 1024, 4096, 512)
+                                           : ptx::smem_desc_sw128(bj + kk * 2048, 8192, 1024))
                        : ptx::smem_desc_sw128(bj + kk * 32, 16, 1024);
               ptx::mma_bf16_pair(d_tmem + j * Cfg::kMmaN, a_desc, b_desc, idesc,
                                  (kb | kk) != 0);

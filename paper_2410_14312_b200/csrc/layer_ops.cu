@@ -160,7 +160,8 @@ void launch_one(const GemmLaunch& g, cudaStream_t st) {
   init_gemm_attributes();
   if (g.pair) {
     // 64-wide pair tiles: forward (K-major B) only, no split-K / halo
-    if constexpr (BN >= 128 || (BN == 64 && !A_MN && !B_MN && EPI == kEpiFwd)) {
+    if constexpr (BN >= 128 || (BN == 64 && !A_MN && !B_MN && EPI == kEpiFwd) ||
+                  (BN == 64 && !A_MN && B_MN && EPI == kEpiDgrad)) {
     auto kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>;
     if constexpr (EPI != kEpiWgradSgd && BN >= 128)
       if (g.ext) kern = gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, true>;
@@ -232,8 +233,8 @@ void set_attr() {
     PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, A_MN, B_MN, EPI>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  GemmCfg<BN>::kSmem));
-  if constexpr (BN < 128) {  // single-CTA, plus the forward pair kernel
-    if constexpr (!A_MN && !B_MN && EPI == kEpiFwd)
+  if constexpr (BN < 128) {  // single-CTA, plus the forward / conv-dgrad pair kernel
+    if constexpr (!A_MN && ((!B_MN && EPI == kEpiFwd) || (B_MN && EPI == kEpiDgrad)))
       PB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair<BN, A_MN, B_MN, EPI, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    Gemm2Cfg<BN, EPI>::kSmem));
@@ -796,16 +797,19 @@ CUtensorMap make_patch_tmap(const Nhwc& t, int tw) {
 }
 
 // conv weights [Cout][ld] viewed as [Cout][9][Cin]: box 64 Cin x 1 tap x 64 Cout
-CUtensorMap make_w3d_tmap(const __nv_bfloat16* w, int cout, int cin, int ld) {
+CUtensorMap make_w3d_tmap(const __nv_bfloat16* w, int cout, int cin, int ld, int box_n = 64) {
   if (cin % 64 != 0 || ld % 8 != 0) throw std::invalid_argument("conv weights: Cin % 64, ld % 8");
   CUtensorMap map;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(cin), 9, static_cast<cuuint64_t>(cout)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(cin) * 2, static_cast<cuuint64_t>(ld) * 2};
-  cuuint32_t box[3] = {64, 1, 64};
+  // 64 input channels per box (128-byte swizzle), or 32 (64-byte swizzle:
+  // one CTA's half of a 64-wide MMA)
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_n), 1, 64};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                            const_cast<void*>(static_cast<const void*>(w)), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           box_n == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw cuda_failure("cuTensorMapEncodeTiled (3-D) failed (code " +
@@ -878,8 +882,15 @@ GemmLaunch plan_conv_dgrad(const Nhwc& dz, const __nv_bfloat16* w, int cin, int 
   g.pair = true;
   g.bn = cin > 128 ? 256 : 128;
   const int tw = halo_width(dz.w);
+  // Cin = 64: 64-wide pair tiles (no half-empty 128-wide MMA), the weight
+  // boxes 32 input channels per CTA (PIPESIM_DGRAD_BN64=0: off)
+  static const bool bn64 = [] {
+    const char* e = std::getenv("PIPESIM_DGRAD_BN64");
+    return !(e && std::string(e) == "0");
+  }();
+  if (bn64 && cin == 64 && !tw) g.bn = 64;
   g.ta = tw ? make_patch_tmap(dz, tw) : make_im2col_tmap(dz, 128);
-  g.tb = make_w3d_tmap(w, dz.c, cin, ld_w);
+  g.tb = make_w3d_tmap(w, dz.c, cin, ld_w, g.bn == 64 ? 32 : 64);
   g.sh = GemmShape{dz.n * dz.h * dz.w, cin, 9 * dz.c, 0, 0, 0, 0, 1, 0};
   g.sh.conv = 3;
   g.sh.halo_tw = tw;

@@ -392,6 +392,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr,
   return d;
 }
 
+// Same, 64-byte swizzle (swizzle mode 4): an MN-major operand 32 elements
+// wide per K row (64 B), 8-row core groups 512 B apart.
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr, uint32_t lbo_bytes,
+                                                   uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 D.
 //   [4,6) D format (1 = f32); [7,10) A format (1 = bf16); [10,13) B format;
 //   [15] A major (1 = MN); [16] B major; [17,23) N >> 3; [24,29) M >> 4.
