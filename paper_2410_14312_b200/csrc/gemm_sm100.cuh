@@ -812,6 +812,10 @@ __global__ void __launch_bounds__(128, 1)
                       EpiParams ep, const __grid_constant__ EpiMaps maps) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
+  // 32-wide tiles with an MN-major B: one 64-byte-swizzled box per k-block
+  // (plain 2-D maps only; the conv im2col B path is 64 columns wide)
+  if constexpr (B_MN && BN == 32)
+    if (sh.conv != 0) __trap();
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the shared array
   // itself, so every derived pointer stays in the shared address space.
@@ -887,6 +891,8 @@ __global__ void __launch_bounds__(128, 1)
           ptx::tma_load_im2col(b_dst + h * 8192, &tmap_b, &full_bar[s], c0, pw - 1, ph - 1, pn,
                                tap % 3, tap / 3);
         }
+      } else if constexpr (BN == 32) {
+        ptx::tma_load_2d(b_dst, &tmap_b, &full_bar[s], n0 + sh.b_mn_off, k0 + sh.b_k_off);
       } else {
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h)
@@ -911,7 +917,8 @@ __global__ void __launch_bounds__(128, 1)
             A_MN ? ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024)
                  : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
         const uint64_t b_desc =
-            B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+            B_MN ? (BN == 32 ? ptx::smem_desc_sw64(b_addr + kk * 1024, 4096, 512)
+                             : ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024))
                  : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
         ptx::mma_bf16(tmem_base, a_desc, b_desc, idesc, (kb | kk) != 0);
       }

@@ -59,6 +59,25 @@ CUtensorMap make_operand_tmap(const Mat16& m, bool k_major, int box_mn) {
   return map;
 }
 
+// MN-major operand in 32-column boxes, 64-byte swizzle (32-wide tiles)
+CUtensorMap make_operand_tmap_mn32(const Mat16& m) {
+  if ((m.ld % 8) != 0) throw std::invalid_argument("bf16 leading dimension must be a multiple of 8");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(m.cols), static_cast<cuuint64_t>(m.rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(m.ld) * 2};
+  cuuint32_t box[2] = {32, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+      const_cast<void*>(static_cast<const void*>(m.ptr)), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw cuda_failure("cuTensorMapEncodeTiled (32-wide) failed (code " +
+                       std::to_string(static_cast<int>(r)) + ")");
+  return map;
+}
+
 // Epilogue tensor maps of the TMA SGD epilogue: 2-D row-major, box 32 rows x
 // box_cols (32 fp32 master columns; 64 bf16 columns: one 128-byte row).
 CUtensorMap make_epi_tmap(const void* ptr, CUtensorMapDataType dt, int elem_bytes, int rows,
@@ -253,6 +272,9 @@ template <bool A_MN, bool B_MN, int EPI>
 void launch_bn(const GemmLaunch& g, cudaStream_t st) {
   if constexpr (EPI != kEpiWgradSgd)
     if (g.bn == 512) return launch_one<512, A_MN, B_MN, EPI>(g, st);
+  if constexpr (EPI == kEpiWgradSgd) {
+    if (g.bn == 32 && !g.pair) return launch_one<32, A_MN, B_MN, EPI>(g, st);
+  }
   if (g.bn == 256)
     launch_one<256, A_MN, B_MN, EPI>(g, st);
   else if (g.bn == 64)
@@ -275,6 +297,7 @@ void init_gemm_attributes() {
     set_attr<64, false, false, kEpiFwd>();
     set_attr<64, false, true, kEpiDgrad>();
     set_attr<64, true, true, kEpiWgradSgd>();
+    set_attr<32, true, true, kEpiWgradSgd>();
     set_attr<128, true, true, kEpiWgradSgd>();
     set_attr<256, true, true, kEpiWgradSgd>();
     // conv wgrad: split-K partial slabs (single-CTA, MN / MN operands)
@@ -563,7 +586,7 @@ int latency_wgrad_bn(int out, int in) {
   }();
   (void)out;
   (void)in;
-  if (env == 0 || env == 64 || env == 128) return env;
+  if (env == 0 || env == 32 || env == 64 || env == 128) return env;
   return 64;
 }
 
@@ -591,7 +614,7 @@ GemmLaunch plan_wgrad_sgd(const Mat16& dz, const Mat16& x, int x_row_off,
   g.bn = single_bn > 0 ? single_bn : pick_bn(dz.cols, x.cols);
   g.pair = single_bn > 0 ? false : use_pair(dz.cols);
   g.ta = make_operand_tmap(dz, /*k_major=*/false, 64);
-  g.tb = make_operand_tmap(x, /*k_major=*/false, 64);
+  g.tb = g.bn == 32 ? make_operand_tmap_mn32(x) : make_operand_tmap(x, /*k_major=*/false, 64);
   g.sh = GemmShape{dz.cols, x.cols, dz.rows, 0, 0, 0, x_row_off};
   g.ep = empty_epi(kEpiWgradSgd);
   g.ep.w_cur = w_cur;
