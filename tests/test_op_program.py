@@ -1,0 +1,71 @@
+"""The session's op program on the host (plan-only, no GPU): the
+PIPESIM_DUMP_OPS listing, and transitive pruning of cross-stream waits
+(PIPESIM_PRUNE_EDGES) removing waits only -- the same kernels in the same
+order on every stream -- and fusing the latency-bound stages' layers
+(PIPESIM_FWD_CHAIN / PIPESIM_DGRAD_CHAIN) on C1's stage 2."""
+import os
+import subprocess
+import sys
+from collections import Counter
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CODE = """
+import sys
+sys.path.insert(0, {root!r})
+from paper_2410_14312_b200 import pipesim as P
+net = P.NetworkSpec({widths!r}, {acts!r}, 'softmax_cross_entropy')
+P.plan_memory(net, {W}, {N}, {B}, {M}, mode={mode!r})
+"""
+
+
+def _dump(tmp_path, name, env_extra, widths=(784, 512, 256, 10), acts=("relu", "relu", "linear"),
+          W=2, N=4, B=256, M=12, mode="timeprest"):
+    path = tmp_path / f"{name}.txt"
+    env = dict(os.environ, PIPESIM_DUMP_OPS=str(path), **env_extra)
+    code = CODE.format(root=ROOT, widths=list(widths), acts=list(acts), W=W, N=N, B=B, M=M,
+                       mode=mode)
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, capture_output=True)
+    return [line.split() for line in path.read_text().splitlines()]
+
+
+def _kernels_per_stream(ops):
+    per = {}
+    for o in ops:
+        if o[2] not in ("wait", "record", "mark"):
+            per.setdefault(o[1], []).append(o[2])
+    return per
+
+
+@pytest.mark.parametrize("mode", ["timeprest", "pipedream"])
+def test_pruning_removes_only_waits(tmp_path, mode):
+    full = _dump(tmp_path, "full", {"PIPESIM_PRUNE_EDGES": "0"}, mode=mode)
+    pruned = _dump(tmp_path, "pruned", {"PIPESIM_PRUNE_EDGES": "1"}, mode=mode)
+    assert _kernels_per_stream(full) == _kernels_per_stream(pruned)
+    nw_full = sum(o[2] == "wait" for o in full)
+    nw_pruned = sum(o[2] == "wait" for o in pruned)
+    assert 0 < nw_pruned < nw_full
+
+
+def test_deep_net_program_pruned(tmp_path):
+    kw = dict(widths=[256] * 9, acts=["relu"] * 7 + ["linear"], W=8, N=4, B=128, M=10)
+    full = _dump(tmp_path, "full", {"PIPESIM_PRUNE_EDGES": "0"}, **kw)
+    pruned = _dump(tmp_path, "pruned", {"PIPESIM_PRUNE_EDGES": "1"}, **kw)
+    assert _kernels_per_stream(full) == _kernels_per_stream(pruned)
+    assert sum(o[2] == "wait" for o in pruned) <= sum(o[2] == "wait" for o in full)
+
+
+def test_c1_stage2_is_fused(tmp_path):
+    ops = _dump(tmp_path, "fused", {})
+    kinds = Counter(o[2] for o in ops)
+    M = 12
+    assert kinds["dgrad_chain"] == M  # one per stage-2 backward
+    assert kinds["dgrad"] == 0        # stage 1 needs no delta
+    assert kinds["fwd_chain"] >= M    # every stage-2 forward node
+    unfused = _dump(tmp_path, "unfused", {"PIPESIM_FWD_CHAIN": "0", "PIPESIM_DGRAD_CHAIN": "0"})
+    k2 = Counter(o[2] for o in unfused)
+    assert k2["dgrad_chain"] == 0 and k2["fwd_chain"] == 0
+    assert k2["dgrad"] == 2 * M
+    assert k2["fwd"] == kinds["fwd"] + 2 * kinds["fwd_chain"]
