@@ -69,3 +69,92 @@ def test_c1_stage2_is_fused(tmp_path):
     assert k2["dgrad_chain"] == 0 and k2["fwd_chain"] == 0
     assert k2["dgrad"] == 2 * M
     assert k2["fwd"] == kinds["fwd"] + 2 * kinds["fwd_chain"]
+
+
+def _hb_graph(ops):
+    """Happens-before over op indices: stream order, and record -> wait of
+    the same event (every record creates a fresh event)."""
+    succ = [[] for _ in ops]
+    last_on = {}
+    rec_of = {}
+    for i, o in enumerate(ops):
+        s = o[1]
+        if s in last_on:
+            succ[last_on[s]].append(i)
+        last_on[s] = i
+        if o[2] == "record":
+            rec_of[o[3]] = i
+        elif o[2] == "wait":
+            succ[rec_of[o[3]]].append(i)
+    return succ, rec_of
+
+
+def _kernel_index(ops):
+    """(stream, n-th kernel on it) <-> op index."""
+    fwd, back, count = {}, {}, {}
+    for i, o in enumerate(ops):
+        if o[2] in ("wait", "record", "mark"):
+            continue
+        n = count.get(o[1], 0)
+        count[o[1]] = n + 1
+        fwd[(o[1], n)] = i
+        back[i] = (o[1], n)
+    return fwd, back
+
+
+@pytest.mark.parametrize("mode,kw", [
+    ("timeprest", {}),
+    ("pipedream", {}),
+    ("timeprest", dict(widths=[256] * 9, acts=["relu"] * 7 + ["linear"], W=8, N=4, B=128,
+                       M=10)),
+])
+def test_pruned_program_keeps_every_dependency(tmp_path, mode, kw):
+    full = _dump(tmp_path, "full", {"PIPESIM_PRUNE_EDGES": "0"}, mode=mode, **kw)
+    pruned = _dump(tmp_path, "pruned", {"PIPESIM_PRUNE_EDGES": "1"}, mode=mode, **kw)
+    _, f_back = _kernel_index(full)
+    p_fwd, _ = _kernel_index(pruned)
+    _, f_rec = _hb_graph(full)
+    p_succ, _ = _hb_graph(pruned)
+
+    def prev_kernel(ops, i, stream):
+        for j in range(i - 1, -1, -1):
+            if ops[j][1] == stream and ops[j][0] is not None and ops[j][2] not in (
+                    "wait", "record", "mark"):
+                return j
+        return None
+
+    def next_kernel(ops, i, stream):
+        for j in range(i + 1, len(ops)):
+            if ops[j][1] == stream and ops[j][2] not in ("wait", "record", "mark"):
+                return j
+        return None
+
+    reach_cache = {}
+
+    def reaches(a, b):
+        key = a
+        if key not in reach_cache:
+            seen, stack = {a}, [a]
+            while stack:
+                u = stack.pop()
+                for v in p_succ[u]:
+                    if v not in seen:
+                        seen.add(v)
+                        stack.append(v)
+            reach_cache[key] = seen
+        return b in reach_cache[key]
+
+    checked = 0
+    for i, o in enumerate(full):
+        if o[2] != "wait":
+            continue
+        r = f_rec[o[3]]
+        producer = prev_kernel(full, r, full[r][1])
+        consumer = next_kernel(full, i, o[1])
+        if producer is None or consumer is None:
+            continue
+        a = p_fwd[f_back[producer]]
+        b = p_fwd[f_back[consumer]]
+        assert reaches(a, b), (full[producer], full[consumer])
+        checked += 1
+    assert checked > 50
