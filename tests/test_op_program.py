@@ -158,3 +158,15 @@ def test_pruned_program_keeps_every_dependency(tmp_path, mode, kw):
         assert reaches(a, b), (full[producer], full[consumer])
         checked += 1
     assert checked > 50
+
+
+def test_spare_activation_slot_only_for_latency_bound_nets():
+    """Latency-bound networks (every layer <= 1024 wide) hold one activation
+    slot more per stage where consecutive mini-batches would share one (C1
+    stage 2: 1 -> 2); the 16 x 4096 net keeps the minimal colouring."""
+    from paper_2410_14312_b200 import pipesim as P
+    c1 = P.NetworkSpec([784, 512, 256, 10], ["relu", "relu", "linear"], "softmax_cross_entropy")
+    assert list(P.plan_memory(c1, 2, 4, 256, 32)["act_slots"]) == [2, 2]
+    c3 = P.NetworkSpec([4096] * 17, ["relu"] * 15 + ["linear"], "softmax_cross_entropy")
+    slots = list(P.plan_memory(c3, 8, 8, 1024, 32)["act_slots"])
+    assert slots == [3, 3, 3, 2, 2, 2, 2, 1]
